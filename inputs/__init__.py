@@ -1,0 +1,3 @@
+"""Seeded synthetic inputs (networks, configs, dump-id choices); no method arithmetic."""
+from .networks import (Config, Network, Reaction, config, configs, dimerization, dump_ids,  # noqa: F401
+                       empty_network, hiv, immigration_death, pure_death, synthetic)

@@ -1,0 +1,281 @@
+"""ctypes wrapper for the CPU oracle (oracle/ssa_oracle.c) -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this module.  It shares no code with the product
+library: the model is packed here from the plain `inputs` descriptions
+(dense net-change matrix computed below, independently of
+paper_1007_1768_b200/csrc).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "ssa_oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-fexcess-precision=standard",
+          "-fPIC", "-shared", "-Wall", "-Wextra", "-Wno-unused-parameter"]
+
+MODE_SEQUENTIAL = 0
+MODE_WARP32 = 1
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no FP contraction, no fast-math)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, SRC, "-o", tmp, "-lm"])
+        os.replace(tmp, LIB)
+    return LIB
+
+
+class _Model(C.Structure):
+    _fields_ = [("S", C.c_int32), ("R", C.c_int32),
+                ("x0", C.POINTER(C.c_int64)), ("n_reac", C.POINTER(C.c_int32)),
+                ("reac_sp", C.POINTER(C.c_int32)), ("reac_coef", C.POINTER(C.c_int32)),
+                ("nu", C.POINTER(C.c_int64)), ("rate", C.POINTER(C.c_double)),
+                ("mod_sp", C.POINTER(C.c_int32)), ("mod_coef", C.POINTER(C.c_double))]
+
+
+class Summary(C.Structure):
+    _fields_ = [("events", C.c_uint64), ("hash", C.c_uint64), ("t_last", C.c_double),
+                ("near_ties", C.c_uint64), ("absorbed", C.c_int32), ("status", C.c_int32),
+                ("err_reaction", C.c_int32), ("pad", C.c_int32)]
+
+
+SUMMARY_DTYPE = np.dtype([("events", "<u8"), ("hash", "<u8"), ("t_last", "<f8"),
+                          ("near_ties", "<u8"), ("absorbed", "<i4"), ("status", "<i4"),
+                          ("err_reaction", "<i4"), ("pad", "<i4")])
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        P = C.POINTER
+        L.oracle_philox4x32_10.argtypes = [P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
+        L.oracle_u53.argtypes = [C.c_uint64]
+        L.oracle_u53.restype = C.c_double
+        L.oracle_plog.argtypes = [C.c_double]
+        L.oracle_plog.restype = C.c_double
+        L.oracle_plog_n.argtypes = [C.c_int64, P(C.c_double), P(C.c_double)]
+        L.oracle_philox_n.argtypes = [C.c_int64, P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
+        L.oracle_u53_n.argtypes = [C.c_int64, P(C.c_uint64), P(C.c_double)]
+        L.oracle_propensities.argtypes = [P(_Model), P(C.c_int64), P(C.c_double), P(C.c_int32)]
+        L.oracle_select.argtypes = [P(C.c_double), C.c_int32, C.c_int32, C.c_double,
+                                    P(C.c_double), P(C.c_int32)]
+        L.oracle_step.argtypes = [P(_Model), P(C.c_int64), C.c_double, C.c_double, C.c_int32,
+                                  P(C.c_double), P(C.c_int32)]
+        L.oracle_grid_K.argtypes = [C.c_double, C.c_double]
+        L.oracle_grid_K.restype = C.c_int64
+        L.oracle_align_events.argtypes = [C.c_int32, P(C.c_int64), C.c_int64, P(C.c_double),
+                                          P(C.c_int64), C.c_double, C.c_double, P(C.c_int32),
+                                          P(C.c_uint64), P(C.c_double), P(C.c_uint64)]
+        L.oracle_trajectory.argtypes = [P(_Model), C.c_uint64, C.c_uint64, C.c_double, C.c_double,
+                                        C.c_int32, P(C.c_int32), P(C.c_uint64), P(C.c_double),
+                                        P(Summary)]
+        L.oracle_moments.argtypes = [C.c_int64, C.c_int64, P(C.c_int32), P(C.c_double),
+                                     P(C.c_double)]
+        L.oracle_run.argtypes = [P(_Model), C.c_int64, P(C.c_uint64), C.c_uint64, C.c_double,
+                                 C.c_double, C.c_int32, P(C.c_double), P(C.c_double),
+                                 P(C.c_int32), P(C.c_uint64), P(C.c_double), C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray], ct):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(ct))
+
+
+class OracleModel:
+    """Oracle-side packing of an `inputs.Network` (PAPER.md:157 state vector,
+    stoichiometric matrix, propensity vector)."""
+
+    def __init__(self, net):
+        S, R = net.S, net.R
+        self.S, self.R = S, R
+        self.x0 = np.array(net.x0, dtype=np.int64).reshape(max(S, 0))
+        self.n_reac = np.zeros(max(R, 1), np.int32)
+        self.reac_sp = np.zeros(3 * max(R, 1), np.int32)
+        self.reac_coef = np.zeros(3 * max(R, 1), np.int32)
+        self.nu = np.zeros(max(R, 1) * max(S, 1), np.int64)
+        self.rate = np.zeros(max(R, 1), np.float64)
+        self.mod_sp = np.full(max(R, 1), -1, np.int32)
+        self.mod_coef = np.zeros(max(R, 1), np.float64)
+        for j, rx in enumerate(net.reactions):
+            assert len(rx.reactants) <= 3
+            self.n_reac[j] = len(rx.reactants)
+            for q, (sp, m) in enumerate(rx.reactants):
+                self.reac_sp[3 * j + q] = sp
+                self.reac_coef[3 * j + q] = m
+                self.nu[j * S + sp] -= m
+            for sp, m in rx.products:
+                self.nu[j * S + sp] += m
+            self.rate[j] = rx.rate
+            self.mod_sp[j] = rx.modifier_species
+            self.mod_coef[j] = rx.modifier_coef
+        self._c = _Model(S, R, _ptr(self.x0, C.c_int64), _ptr(self.n_reac, C.c_int32),
+                         _ptr(self.reac_sp, C.c_int32), _ptr(self.reac_coef, C.c_int32),
+                         _ptr(self.nu, C.c_int64), _ptr(self.rate, C.c_double),
+                         _ptr(self.mod_sp, C.c_int32), _ptr(self.mod_coef, C.c_double))
+
+    @property
+    def c(self):
+        return C.byref(self._c)
+
+
+# ---------------------------------------------------------------- primitives
+def philox(ctr: Sequence[int], key: Sequence[int]) -> np.ndarray:
+    c = np.array(ctr, np.uint32)
+    k = np.array(key, np.uint32)
+    o = np.zeros(4, np.uint32)
+    lib().oracle_philox4x32_10(_ptr(c, C.c_uint32), _ptr(k, C.c_uint32), _ptr(o, C.c_uint32))
+    return o
+
+
+def philox_n(ctr: np.ndarray, key: Sequence[int]) -> np.ndarray:
+    ctr = np.ascontiguousarray(ctr, np.uint32).reshape(-1, 4)
+    k = np.array(key, np.uint32)
+    o = np.zeros_like(ctr)
+    lib().oracle_philox_n(len(ctr), _ptr(ctr, C.c_uint32), _ptr(k, C.c_uint32), _ptr(o, C.c_uint32))
+    return o
+
+
+def u53(w: int) -> float:
+    return lib().oracle_u53(w)
+
+
+def u53_n(w: np.ndarray) -> np.ndarray:
+    w = np.ascontiguousarray(w, np.uint64)
+    o = np.zeros(len(w), np.float64)
+    lib().oracle_u53_n(len(w), _ptr(w, C.c_uint64), _ptr(o, C.c_double))
+    return o
+
+
+def plog(u: float) -> float:
+    return lib().oracle_plog(u)
+
+
+def plog_n(u: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(u, np.float64)
+    o = np.zeros(len(u), np.float64)
+    lib().oracle_plog_n(len(u), _ptr(u, C.c_double), _ptr(o, C.c_double))
+    return o
+
+
+def propensities(model: OracleModel, x: Sequence[int]):
+    xa = np.array(x, np.int64)
+    a = np.zeros(max(model.R, 1), np.float64)
+    bad = C.c_int32(-1)
+    st = lib().oracle_propensities(model.c, _ptr(xa, C.c_int64), _ptr(a, C.c_double), C.byref(bad))
+    return st, a[:model.R], bad.value
+
+
+def select(a: Sequence[float], mode: int, u2: float):
+    aa = np.array(a, np.float64)
+    a0 = C.c_double()
+    j = C.c_int32()
+    lib().oracle_select(_ptr(aa, C.c_double), len(aa), mode, u2, C.byref(a0), C.byref(j))
+    return a0.value, j.value
+
+
+def step(model: OracleModel, x: Sequence[int], u1: float, u2: float, mode: int = 0):
+    xa = np.array(x, np.int64)
+    tau = C.c_double()
+    j = C.c_int32()
+    st = lib().oracle_step(model.c, _ptr(xa, C.c_int64), u1, u2, mode, C.byref(tau), C.byref(j))
+    return st, tau.value, j.value
+
+
+def grid_size(t_end: float, dt: float) -> int:
+    return int(lib().oracle_grid_K(t_end, dt)) + 1
+
+
+def align_events(x0: Sequence[int], times: Sequence[float], states: np.ndarray, t_end: float,
+                 dt: float):
+    S = len(x0)
+    G = grid_size(t_end, dt)
+    x0a = np.array(x0, np.int64)
+    ta = np.array(times, np.float64)
+    sa = np.ascontiguousarray(np.array(states, np.int64).reshape(len(ta), S))
+    gx = np.zeros((G, S), np.int32)
+    ge = np.zeros(G, np.uint64)
+    gt = np.zeros(G, np.float64)
+    nt = C.c_uint64()
+    lib().oracle_align_events(S, _ptr(x0a, C.c_int64), len(ta), _ptr(ta, C.c_double),
+                              _ptr(sa, C.c_int64), t_end, dt, _ptr(gx, C.c_int32),
+                              _ptr(ge, C.c_uint64), _ptr(gt, C.c_double), C.byref(nt))
+    return gx, ge, gt, nt.value
+
+
+@dataclass
+class Trajectory:
+    grid_x: np.ndarray   # [G, S] int32
+    grid_e: np.ndarray   # [G] uint64
+    grid_t: np.ndarray   # [G] float64
+    summary: dict
+
+
+def trajectory(model: OracleModel, tid: int, seed: int, t_end: float, dt: float,
+               mode: int = 0) -> Trajectory:
+    G = grid_size(t_end, dt)
+    gx = np.zeros((G, max(model.S, 1)), np.int32)
+    ge = np.zeros(G, np.uint64)
+    gt = np.zeros(G, np.float64)
+    s = Summary()
+    lib().oracle_trajectory(model.c, tid, seed, t_end, dt, mode, _ptr(gx, C.c_int32),
+                            _ptr(ge, C.c_uint64), _ptr(gt, C.c_double), C.byref(s))
+    summ = {f: getattr(s, f) for f, _ in Summary._fields_ if f != "pad"}
+    return Trajectory(gx[:, :model.S], ge, gt, summ)
+
+
+def moments(samples: np.ndarray):
+    """Exact mean and population variance over axis 0 of int32 samples."""
+    s = np.ascontiguousarray(samples, np.int32)
+    n = s.shape[0]
+    cells = int(np.prod(s.shape[1:]))
+    mean = np.zeros(cells, np.float64)
+    var = np.zeros(cells, np.float64)
+    lib().oracle_moments(n, cells, _ptr(s, C.c_int32), _ptr(mean, C.c_double), _ptr(var, C.c_double))
+    return mean.reshape(s.shape[1:]), var.reshape(s.shape[1:])
+
+
+@dataclass
+class RunResult:
+    mean: np.ndarray       # [G, S]
+    var: np.ndarray        # [G, S]
+    status: int
+    grid_x: Optional[np.ndarray] = None   # [n, G, S]
+    grid_e: Optional[np.ndarray] = None   # [n, G]
+    grid_t: Optional[np.ndarray] = None   # [n, G]
+    summaries: Optional[np.ndarray] = None  # structured [n]
+
+
+def run(model: OracleModel, ids, seed: int, t_end: float, dt: float, mode: int = 0,
+        keep: bool = True) -> RunResult:
+    ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
+    n = len(ids)
+    G = grid_size(t_end, dt)
+    S = model.S
+    mean = np.zeros((G, max(S, 1)), np.float64)
+    var = np.zeros((G, max(S, 1)), np.float64)
+    gx = np.zeros((n, G, max(S, 1)), np.int32) if keep else None
+    ge = np.zeros((n, G), np.uint64) if keep else None
+    gt = np.zeros((n, G), np.float64) if keep else None
+    sums = np.zeros(n, SUMMARY_DTYPE) if keep else None
+    st = lib().oracle_run(model.c, n, _ptr(ids, C.c_uint64), seed, t_end, dt, mode,
+                          _ptr(mean, C.c_double), _ptr(var, C.c_double), _ptr(gx, C.c_int32),
+                          _ptr(ge, C.c_uint64), _ptr(gt, C.c_double),
+                          None if sums is None else sums.ctypes.data)
+    return RunResult(mean[:, :S], var[:, :S], st,
+                     None if gx is None else gx[:, :, :S], ge, gt, sums)

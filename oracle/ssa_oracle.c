@@ -1,0 +1,580 @@
+/*
+ * ssa_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU oracle for the StochKit-FF hot path
+ * (arxiv/paper_1007_1768): Gillespie direct-method SSA trajectories of a
+ * mass-action network, aligned online to a sample grid ("selective memory",
+ * PAPER.md:147 §3.2.1) and reduced to per-species mean and variance
+ * (PAPER.md:129, :177).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  The product path
+ * (paper_1007_1768_b200/) never includes, links or calls it, and this file
+ * shares no code, header, table or constant generator with the CUDA path.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared
+ * (x86-64 SSE2 arithmetic, FLT_EVAL_METHOD == 0, round-to-nearest-even;
+ * every floating-point operation below is a single IEEE fp64 operation; the
+ * only fused operations are the explicit fma() calls of plog, R11).
+ *
+ * Readings of the paper used here are the ones listed in DESIGN.md §3
+ * ("readings"), numbered R1..R30 after SURVEY.md §8(c) Q1..Q30.
+ *
+ * Parity pins (tests/test_oracle_*.py):
+ *   philox  -- equal to curand_Philox4x32_10 (cuRAND header, host-compiled)
+ *   u53     -- closed-form endpoints, exactness
+ *   plog    -- <= 2 ulp of logl on >= 1e6 inputs; special values
+ *   propensity -- SPEC.md:87-88 printed values, C(x,2) closed form
+ *   step    -- SPEC.md:174 worked example; frozen-state statistics
+ *   aligner -- SPEC.md:250 example restated on a grid (tests/golden)
+ *   moments -- SPEC.md:270-272 printed example
+ *   trajectory -- closed forms (immigration-death Poisson, pure-death
+ *                 binomial), CME by matrix exponential, structural
+ *                 invariants of the HIV network (U0 == 1, F nondecreasing).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#if defined(__FLT_EVAL_METHOD__) && __FLT_EVAL_METHOD__ != 0
+#error "oracle requires FLT_EVAL_METHOD == 0 (SSE2 double arithmetic)"
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* Status codes (mirror the meaning of ssa_status in include/ssa.h, but are  */
+/* defined here independently).                                              */
+/* ------------------------------------------------------------------------ */
+enum {
+    OR_OK = 0,
+    OR_ERR_INVALID = 1,
+    OR_ERR_NUMERIC = 3,   /* non-finite propensity      */
+    OR_ERR_OVERFLOW = 4,  /* a sampled count > INT32_MAX (R20)    */
+};
+
+/* ------------------------------------------------------------------------ */
+/* Model (parameters, integer state vector, integer            */
+/* stoichiometric matrix, propensity vector).                                */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t S;               /* number of species                          */
+    int32_t R;               /* number of reactions                        */
+    const int64_t *x0;       /* [S] initial counts           */
+    const int32_t *n_reac;   /* [R] number of reactant terms (0..3)        */
+    const int32_t *reac_sp;  /* [R*3] reactant species                     */
+    const int32_t *reac_coef;/* [R*3] reactant coefficient m >= 1          */
+    const int64_t *nu;       /* [R*S] net change, products - reactants     */
+    const double *rate;      /* [R] rate constant k_j                      */
+    const int32_t *mod_sp;   /* [R] modifier species or -1   */
+    const double *mod_coef;  /* [R] modifier coefficient d_j               */
+} oracle_model;
+
+typedef struct {
+    uint64_t events;     /* applied events (t <= s_K)                        */
+    uint64_t hash;       /* FNV-1a style hash of the firing sequence         */
+    double t_last;       /* time of the last applied event (0 if none)       */
+    uint64_t near_ties;  /* grid crossings with an event within 1e-9 rel.    */
+    int32_t absorbed;    /* 1 if a0 == 0 was reached before s_K              */
+    int32_t status;      /* OR_OK or error                                   */
+    int32_t err_reaction;/* reaction index of a non-finite propensity        */
+    int32_t pad;
+} oracle_summary;
+
+/* ------------------------------------------------------------------------ */
+/* a2: Philox4x32-10 (Salmon et al., SC'11), the counter-based RNG that      */
+/* replaces StochKit's non-reentrant sprng (PAPER.md:129, :139 fn.2;         */
+/* DESIGN.md R8).  Key = (seed lo, seed hi); counter = (e lo, e hi, id lo,   */
+/* id hi).                                                                   */
+/* ------------------------------------------------------------------------ */
+#define PH_M0 0xD2511F53u
+#define PH_M1 0xCD9E8D57u
+#define PH_W0 0x9E3779B9u
+#define PH_W1 0xBB67AE85u
+
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int round = 0; round < 10; ++round) {
+        uint64_t p0 = (uint64_t)PH_M0 * (uint64_t)c0;
+        uint64_t p1 = (uint64_t)PH_M1 * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += PH_W0;
+        k1 += PH_W1;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* u53 (R9): the top 52 bits of a 64-bit word mapped to the open
+ * interval: u = (w >> 12) * 2^-52 + 2^-53, exactly (2m+1) * 2^-53,
+ * in [2^-53, 1 - 2^-53]. */
+double oracle_u53(uint64_t w)
+{
+    double m = (double)(w >> 12);           /* exact: < 2^52 */
+    return m * 0x1p-52 + 0x1p-53;           /* both operations exact */
+}
+
+/* ------------------------------------------------------------------------ */
+/* plog (R11): the pinned natural logarithm both sides implement   */
+/* bit-for-bit.  u = 2^e * m, m in [sqrt(1/2), sqrt(2)];  f = m - 1;         */
+/* s = f / (2 + f);  ln(1+f) = 2 atanh(s) = 2s + 2s z P(z), z = s^2,         */
+/* P(z) = sum_{k=1..10} z^(k-1) / (2k+1) (Horner with explicit fma);          */
+/* ln u = e ln2_hi + (e ln2_lo + ln(1+f)).  Defined for positive normal u.   */
+/* ------------------------------------------------------------------------ */
+static double bits_to_double(uint64_t b) { double d; memcpy(&d, &b, 8); return d; }
+static uint64_t double_to_bits(double d) { uint64_t b; memcpy(&b, &d, 8); return b; }
+
+double oracle_plog(double u)
+{
+    /* 1/(2k+1), k = 1..10, each correctly rounded (pinned in tests). */
+    static const double C[11] = {
+        0.0,
+        0x1.5555555555555p-2,  /* 1/3  */
+        0x1.999999999999ap-3,  /* 1/5  */
+        0x1.2492492492492p-3,  /* 1/7  */
+        0x1.c71c71c71c71cp-4,  /* 1/9  */
+        0x1.745d1745d1746p-4,  /* 1/11 */
+        0x1.3b13b13b13b14p-4,  /* 1/13 */
+        0x1.1111111111111p-4,  /* 1/15 */
+        0x1.e1e1e1e1e1e1ep-5,  /* 1/17 */
+        0x1.af286bca1af28p-5,  /* 1/19 */
+        0x1.8618618618618p-5,  /* 1/21 */
+    };
+    const double SQRT2 = 0x1.6a09e667f3bcdp+0;     /* fl(sqrt 2) */
+    const double LN2_HI = 0x1.62e42fee00000p-1;    /* ln 2, 32 significant bits */
+    const double LN2_LO = 0x1.a39ef35793c76p-33;   /* fl(ln 2 - LN2_HI) */
+
+    uint64_t b = double_to_bits(u);
+    int e = (int)((b >> 52) & 0x7FF) - 1023;
+    double m = bits_to_double((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull);
+    if (m > SQRT2) {
+        m = m * 0.5;
+        e = e + 1;
+    }
+    double f = m - 1.0;
+    double s = f / (2.0 + f);
+    double z = s * s;
+    double p = C[10];
+    for (int k = 9; k >= 1; --k)
+        p = fma(p, z, C[k]);
+    double t2 = 2.0 * s;
+    double lm = fma(t2 * z, p, t2);
+    double ed = (double)e;
+    return fma(ed, LN2_HI, fma(ed, LN2_LO, lm));
+}
+
+/* ------------------------------------------------------------------------ */
+/* a3: propensities ("the more the reactants (and the rate) */
+/* the highest the probability", e.g. I4 x pi; PAPER.md:93 state-dependent   */
+/* infectivity).  a_j = k^_j * h_j with                                       */
+/*   h_j = prod over reactant terms, in declared order, of C(x_s, m)         */
+/*         (unordered combinations, R1), each product an fp64 op;  */
+/*   k^_j = k_j, or max(0, k_j + d_j * x_mod) for a modified reaction (R4).  */
+/* Returns OR_OK, or OR_ERR_NUMERIC with *bad = first non-finite reaction.   */
+/* ------------------------------------------------------------------------ */
+static double binom_factor(int64_t xs, int32_t m)
+{
+    double x = (double)xs;                   /* exact: counts < 2^53 */
+    if (m == 1) return x;
+    if (m == 2) return (x * (x - 1.0)) * 0.5;
+    /* m == 3 */
+    return ((x * (x - 1.0)) * (x - 2.0)) / 6.0;
+}
+
+int oracle_propensities(const oracle_model *M, const int64_t *x, double *a, int32_t *bad)
+{
+    for (int j = 0; j < M->R; ++j) {
+        double h = 1.0;
+        for (int q = 0; q < M->n_reac[j]; ++q) {
+            double fct = binom_factor(x[M->reac_sp[3 * j + q]], M->reac_coef[3 * j + q]);
+            h = (q == 0) ? fct : h * fct;
+        }
+        double k = M->rate[j];
+        if (M->mod_sp[j] >= 0) {
+            double xm = (double)x[M->mod_sp[j]];
+            k = k + M->mod_coef[j] * xm;     /* two roundings, no fma */
+            if (k < 0.0) k = 0.0;            /* "0 <= beta_R5" */
+        }
+        a[j] = k * h;
+        if (!isfinite(a[j])) {
+            if (bad) *bad = j;
+            return OR_ERR_NUMERIC;
+        }
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a4 + a7: total propensity and selection, in one of two declared           */
+/* summation orders (R13):                                         */
+/*  mode 0 "sequential": c_j = c_{j-1} + a_j left to right, a0 = c_{R-1},    */
+/*         j* = min{ j : c_j > r }.                                           */
+/*  mode 1 "warp32": P = ceil(R/32) contiguous reactions per lane l;          */
+/*         L_l = sequential sum of lane l's a_j;  Hillis-Steele inclusive     */
+/*         scan over the 32 L_l with offsets 1,2,4,8,16 gives v_l; a0 = v_31; */
+/*         lane* = min{ l : v_l > r };  p = v_{lane*-1} (0 for lane 0), then  */
+/*         p += a_j over lane*'s reactions in order, j* = first j with p > r; */
+/*         if none, j* = the largest j <= lane*'s last index with a_j > 0.    */
+/* r = u2 * a0 ("smallest j with sum_{i<=j} a_i > u2 a0").        */
+/* ------------------------------------------------------------------------ */
+static double total_sequential(const double *a, int R)
+{
+    double c = 0.0;
+    for (int j = 0; j < R; ++j) c = c + a[j];
+    return c;
+}
+
+static int select_sequential(const double *a, int R, double r)
+{
+    double c = 0.0;
+    for (int j = 0; j < R; ++j) {
+        c = c + a[j];
+        if (c > r) return j;
+    }
+    return -1; /* unreachable when r < a0 (R12) */
+}
+
+static void warp32_scan(const double *a, int R, double v[32])
+{
+    int P = (R + 31) / 32;
+    double L[32];
+    for (int l = 0; l < 32; ++l) {
+        double s = 0.0;
+        for (int j = l * P; j < (l + 1) * P && j < R; ++j) s = s + a[j];
+        L[l] = s;
+    }
+    for (int l = 0; l < 32; ++l) v[l] = L[l];
+    for (int o = 1; o < 32; o *= 2) {
+        double nv[32];
+        for (int l = 0; l < 32; ++l) nv[l] = (l >= o) ? (v[l - o] + v[l]) : v[l];
+        for (int l = 0; l < 32; ++l) v[l] = nv[l];
+    }
+}
+
+static int select_warp32(const double *a, int R, const double v[32], double r)
+{
+    int P = (R + 31) / 32;
+    int lane = -1;
+    for (int l = 0; l < 32; ++l) {
+        if (v[l] > r) { lane = l; break; }
+    }
+    if (lane < 0) return -1;
+    double p = (lane > 0) ? v[lane - 1] : 0.0;
+    int last = (lane + 1) * P - 1;
+    if (last > R - 1) last = R - 1;
+    for (int j = lane * P; j <= last; ++j) {
+        p = p + a[j];
+        if (p > r) return j;
+    }
+    for (int j = last; j >= 0; --j)
+        if (a[j] > 0.0) return j;
+    return -1;
+}
+
+/* Computes a0 and j* for given propensities and u2 (mode 0 or 1). */
+int oracle_select(const double *a, int32_t R, int32_t mode, double u2, double *a0_out, int32_t *j_out)
+{
+    double a0, r;
+    int j;
+    if (mode == 0) {
+        a0 = total_sequential(a, R);
+        r = u2 * a0;
+        j = (a0 > 0.0) ? select_sequential(a, R, r) : -1;
+    } else {
+        double v[32];
+        warp32_scan(a, R, v);
+        a0 = v[31];
+        r = u2 * a0;
+        j = (a0 > 0.0) ? select_warp32(a, R, v, r) : -1;
+    }
+    *a0_out = a0;
+    *j_out = j;
+    return OR_OK;
+}
+
+/* One direct-method step with prescribed uniforms:
+ * tau = -plog(u1) / a0; returns *j = -1 and tau = +inf when a0 == 0. */
+int oracle_step(const oracle_model *M, const int64_t *x, double u1, double u2, int32_t mode,
+                double *tau, int32_t *j)
+{
+    double *a = (double *)malloc(sizeof(double) * (M->R > 0 ? M->R : 1));
+    int32_t bad = -1;
+    int st = oracle_propensities(M, x, a, &bad);
+    if (st != OR_OK) { free(a); *j = bad; return st; }
+    double a0;
+    oracle_select(a, M->R, mode, u2, &a0, j);
+    if (a0 == 0.0) {
+        *tau = INFINITY;
+        *j = -1;
+    } else {
+        double E = -oracle_plog(u1);
+        *tau = E / a0;
+    }
+    free(a);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a6: grid alignment -- selective memory on a fixed grid (PAPER.md:143,     */
+/* :147 "aligns simulation points ... according to simulation time";         */
+/* DESIGN.md R14, R15).  Grid s_k = k * dt, k = 0..K, K = floor(t_end/dt +   */
+/* 1e-9).  The state held at s_k is the state just before the first event    */
+/* with time > s_k (an event exactly at s_k is included: right-continuous    */
+/* zero-order hold).                                                          */
+/* ------------------------------------------------------------------------ */
+int64_t oracle_grid_K(double t_end, double dt)
+{
+    return (int64_t)floor(t_end / dt + 1e-9);
+}
+
+typedef struct {
+    int32_t S;
+    int64_t K;
+    double dt;
+    int64_t k;            /* next grid index to emit */
+    int32_t *grid_x;      /* [G*S] or NULL */
+    uint64_t *grid_e;     /* [G] or NULL */
+    double *grid_t;       /* [G] or NULL */
+    uint64_t near_ties;
+    int32_t overflow;
+} grid_cursor;
+
+/* Emit every grid point s_k with s_k < tn (tn = candidate event time, or
+ * +inf for an absorbing state).  x = held state, t = time of the last
+ * applied event (meaningful if e > 0). */
+static void grid_emit_before(grid_cursor *g, const int64_t *x, double t, uint64_t e, double tn)
+{
+    while (g->k <= g->K) {
+        double sk = (double)g->k * g->dt;
+        if (!(tn > sk)) break;
+        double tol = 1e-9 * sk;
+        int near = 0;
+        if (isfinite(tn) && fabs(tn - sk) <= tol) near = 1;
+        if (e > 0 && fabs(t - sk) <= tol) near = 1;
+        g->near_ties += (uint64_t)near;
+        if (g->grid_x) {
+            for (int s = 0; s < g->S; ++s) {
+                if (x[s] > 2147483647LL) g->overflow = 1;
+                g->grid_x[g->k * g->S + s] = (int32_t)x[s];
+            }
+        } else {
+            for (int s = 0; s < g->S; ++s)
+                if (x[s] > 2147483647LL) g->overflow = 1;
+        }
+        if (g->grid_e) g->grid_e[g->k] = e;
+        if (g->grid_t) g->grid_t[g->k] = (e > 0) ? t : 0.0;
+        g->k += 1;
+    }
+}
+
+/* Test hook for the aligner alone: feed a prescribed event stream
+ * (times[i], state after event i) and the initial state; the stream ends at
+ * the first event with time > s_K, or, if exhausted, is held to the end. */
+int oracle_align_events(int32_t S, const int64_t *x0, int64_t n_events, const double *times,
+                        const int64_t *states, double t_end, double dt, int32_t *grid_x,
+                        uint64_t *grid_e, double *grid_t, uint64_t *near_ties)
+{
+    grid_cursor g = {S, oracle_grid_K(t_end, dt), dt, 0, grid_x, grid_e, grid_t, 0, 0};
+    const int64_t *x = x0;
+    double t = 0.0;
+    uint64_t e = 0;
+    for (int64_t i = 0; i < n_events && g.k <= g.K; ++i) {
+        grid_emit_before(&g, x, t, e, times[i]);
+        if (g.k > g.K) break;
+        x = states + i * S;
+        t = times[i];
+        e += 1;
+    }
+    grid_emit_before(&g, x, t, e, INFINITY);
+    if (near_ties) *near_ties = g.near_ties;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a1-a8: one trajectory ("Given the current state of the        */
+/* system, a single transition amongst the possible ones is selected, and    */
+/* the state updated accordingly. The Gillespie's algorithm [8] determines   */
+/* the next transition and the time at which it occurs").                    */
+/* ------------------------------------------------------------------------ */
+#define FNV_OFFSET 0xcbf29ce484222325ull
+#define FNV_PRIME 0x100000001b3ull
+
+int oracle_trajectory(const oracle_model *M, uint64_t id, uint64_t seed, double t_end, double dt,
+                      int32_t mode, int32_t *grid_x, uint64_t *grid_e, double *grid_t,
+                      oracle_summary *sum)
+{
+    int S = M->S, R = M->R;
+    int64_t *x = (int64_t *)malloc(sizeof(int64_t) * (S > 0 ? S : 1));
+    double *a = (double *)malloc(sizeof(double) * (R > 0 ? R : 1));
+    for (int s = 0; s < S; ++s) x[s] = M->x0[s];
+
+    grid_cursor g = {S, oracle_grid_K(t_end, dt), dt, 0, grid_x, grid_e, grid_t, 0, 0};
+    double t = 0.0;
+    uint64_t e = 0;
+    uint64_t hash = FNV_OFFSET;
+    int32_t absorbed = 0, status = OR_OK, bad = -1;
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+
+    for (;;) {
+        /* a2: one Philox block per candidate event */
+        uint32_t ctr[4] = {(uint32_t)e, (uint32_t)(e >> 32), (uint32_t)id, (uint32_t)(id >> 32)};
+        uint32_t o[4];
+        oracle_philox4x32_10(ctr, key, o);
+        double u1 = oracle_u53(((uint64_t)o[1] << 32) | o[0]);
+        double u2 = oracle_u53(((uint64_t)o[3] << 32) | o[2]);
+
+        /* a3 */
+        status = oracle_propensities(M, x, a, &bad);
+        if (status != OR_OK) break;
+
+        /* a4 */
+        double a0, v[32];
+        if (mode == 0) {
+            a0 = total_sequential(a, R);
+        } else {
+            warp32_scan(a, R, v);
+            a0 = v[31];
+        }
+
+        /* a5 */
+        if (a0 == 0.0) {
+            grid_emit_before(&g, x, t, e, INFINITY);
+            absorbed = 1;
+            break;
+        }
+        if (!isfinite(a0)) { status = OR_ERR_NUMERIC; bad = -1; break; }
+        double E = -oracle_plog(u1);
+        double tau = E / a0;
+        double tn = t + tau;
+
+        /* a6 */
+        grid_emit_before(&g, x, t, e, tn);
+        if (g.k > g.K) break;
+
+        /* a7 */
+        double r = u2 * a0;
+        int j = (mode == 0) ? select_sequential(a, R, r) : select_warp32(a, R, v, r);
+
+        /* a8 */
+        for (int s = 0; s < S; ++s) x[s] += M->nu[(int64_t)j * S + s];
+        t = tn;
+        e += 1;
+        hash = (hash ^ (uint64_t)j) * FNV_PRIME;
+    }
+    if (status == OR_OK && g.overflow) status = OR_ERR_OVERFLOW;
+    if (sum) {
+        sum->events = e;
+        sum->hash = hash;
+        sum->t_last = t;
+        sum->near_ties = g.near_ties;
+        sum->absorbed = absorbed;
+        sum->status = status;
+        sum->err_reaction = bad;
+        sum->pad = 0;
+    }
+    free(x);
+    free(a);
+    return status;
+}
+
+/* ------------------------------------------------------------------------ */
+/* a9-a10 (oracle form, R19): exact integer moments               */
+/* S1 = sum x, S2 = sum x^2 (128-bit) per (k, s) over the trajectories, then */
+/* mean = S1 / n and population variance = (n S2 - S1^2) / n^2 (*/
+/* DESIGN.md R18), each rounded once to double from an exact numerator.      */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+    int64_t n;
+    int64_t cells;       /* G*S */
+    int64_t *s1;         /* [cells] */
+    __int128 *s2;        /* [cells] */
+} moment_acc;
+
+static void acc_add(moment_acc *A, const int32_t *sample)
+{
+    for (int64_t c = 0; c < A->cells; ++c) {
+        int64_t v = sample[c];
+        A->s1[c] += v;
+        A->s2[c] += (__int128)v * v;
+    }
+    A->n += 1;
+}
+
+static void acc_finalize(const moment_acc *A, double *mean, double *var)
+{
+    for (int64_t c = 0; c < A->cells; ++c) {
+        if (A->n == 0) { mean[c] = 0.0; var[c] = 0.0; continue; }
+        __int128 n = A->n;
+        __int128 num = n * A->s2[c] - (__int128)A->s1[c] * A->s1[c];
+        long double nl = (long double)A->n;
+        mean[c] = (double)((long double)A->s1[c] / nl);
+        var[c] = (double)((long double)num / (nl * nl));
+    }
+}
+
+/* Exact moments of n given samples (row-major [n][cells]). */
+int oracle_moments(int64_t n, int64_t cells, const int32_t *samples, double *mean, double *var)
+{
+    moment_acc A = {0, cells, calloc((size_t)cells, sizeof(int64_t)),
+                    calloc((size_t)cells, sizeof(__int128))};
+    for (int64_t i = 0; i < n; ++i) acc_add(&A, samples + i * cells);
+    acc_finalize(&A, mean, var);
+    free(A.s1);
+    free(A.s2);
+    return OR_OK;
+}
+
+/* Whole ensemble over an explicit id list: trajectories in the given order,
+ * exact moments, optional per-trajectory outputs (each may be NULL):
+ *   grid_x [n_ids][G][S], grid_e [n_ids][G], grid_t [n_ids][G], sums [n_ids].
+ * Returns the first non-OK trajectory status (all trajectories still run). */
+int oracle_run(const oracle_model *M, int64_t n_ids, const uint64_t *ids, uint64_t seed,
+               double t_end, double dt, int32_t mode, double *mean, double *var,
+               int32_t *grid_x, uint64_t *grid_e, double *grid_t, oracle_summary *sums)
+{
+    int64_t G = oracle_grid_K(t_end, dt) + 1;
+    int64_t cells = G * M->S;
+    moment_acc A = {0, cells, calloc((size_t)(cells ? cells : 1), sizeof(int64_t)),
+                    calloc((size_t)(cells ? cells : 1), sizeof(__int128))};
+    int32_t *gx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(cells ? cells : 1));
+    int first = OR_OK;
+    for (int64_t i = 0; i < n_ids; ++i) {
+        oracle_summary s;
+        int st = oracle_trajectory(M, ids[i], seed, t_end, dt, mode, gx,
+                                   grid_e ? grid_e + i * G : NULL,
+                                   grid_t ? grid_t + i * G : NULL, &s);
+        if (st != OR_OK && first == OR_OK) first = st;
+        acc_add(&A, gx);
+        if (grid_x) memcpy(grid_x + i * cells, gx, sizeof(int32_t) * (size_t)cells);
+        if (sums) sums[i] = s;
+    }
+    if (mean && var) acc_finalize(&A, mean, var);
+    free(gx);
+    free(A.s1);
+    free(A.s2);
+    return first;
+}
+
+/* Array conveniences for the pin tests (plain loops over the scalar forms). */
+void oracle_plog_n(int64_t n, const double *u, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_plog(u[i]);
+}
+
+void oracle_philox_n(int64_t n, const uint32_t *ctr, const uint32_t key[2], uint32_t *out)
+{
+    for (int64_t i = 0; i < n; ++i) oracle_philox4x32_10(ctr + 4 * i, key, out + 4 * i);
+}
+
+void oracle_u53_n(int64_t n, const uint64_t *w, double *out)
+{
+    for (int64_t i = 0; i < n; ++i) out[i] = oracle_u53(w[i]);
+}
+
+int oracle_abi_version(void) { return 1; }

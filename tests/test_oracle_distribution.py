@@ -1,0 +1,229 @@
+"""Distributional pins of the oracle's trajectories (PAPER.md:60 'exactly
+according to the given probability distributions'): closed forms, the chemical
+master equation by matrix exponential on finite state spaces, and structural
+invariants of the HIV network (Table 1)."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import inputs
+from inputs.networks import Network, _rx
+
+Z = 4.0
+
+
+def _zmean(m, mu, var, n):
+    if var == 0:
+        return 0.0 if m == mu else np.inf
+    return abs(m - mu) / math.sqrt(var / n)
+
+
+def _zvar(v, var, mu4, n):
+    # var of the sample (population) variance ~ (mu4 - sigma^4)/n
+    d = mu4 - var * var
+    if d <= 0:
+        return 0.0 if abs(v - var) < 1e-12 else np.inf
+    return abs(v - var) / math.sqrt(d / n)
+
+
+def test_immigration_death_config0_closed_form(oracle_lib):
+    """BASELINE.json configs[0]: X(t) ~ Poisson(100 (1 - e^{-0.1 t})) from X0 = 0."""
+    O = oracle_lib
+    cfg = inputs.config(0)
+    m = O.OracleModel(cfg.network)
+    res = O.run(m, np.arange(cfg.n_trajectories), cfg.seed, cfg.t_end, cfg.dt, keep=False)
+    assert res.status == 0
+    G = O.grid_size(cfg.t_end, cfg.dt)
+    n = cfg.n_trajectories
+    assert res.mean[0, 0] == 0 and res.var[0, 0] == 0
+    for k in range(1, G):
+        t = k * cfg.dt
+        lam = 100.0 * (1 - math.exp(-0.1 * t))
+        assert _zmean(res.mean[k, 0], lam, lam, n) < Z, k
+        assert _zvar(res.var[k, 0], lam, lam + 3 * lam * lam, n) < Z, k
+
+
+def test_immigration_death_spec_acceptance4(oracle_lib):
+    """SPEC.md:186 / :450: lambda=10, delta=1, 1000 trajectories, t=20:
+    mean in [9.7, 10.3], variance in [8.5, 11.5]."""
+    O = oracle_lib
+    m = O.OracleModel(inputs.immigration_death(10.0, 1.0, 0))
+    res = O.run(m, np.arange(1000), 11, 20.0, 20.0, keep=False)
+    assert 9.7 <= res.mean[-1, 0] <= 10.3
+    assert 8.5 <= res.var[-1, 0] <= 11.5
+
+
+def test_pure_death_binomial(oracle_lib):
+    """X -> 0 at rate k: X(t) ~ Binomial(X0, e^{-k t}); every event removes one."""
+    O = oracle_lib
+    x0, k, n = 10, 1.0, 20000
+    m = O.OracleModel(inputs.pure_death(k, x0))
+    res = O.run(m, np.arange(n), 5, 2.0, 0.25)
+    gx = res.grid_x[:, :, 0]
+    assert np.all(np.diff(gx, axis=1) <= 0)
+    assert np.all(res.grid_e[:, :] == (x0 - gx))           # one molecule per event
+    assert np.all(res.summaries["absorbed"][gx[:, -1] == 0] == 1)
+    for kk in range(res.mean.shape[0]):
+        t = kk * 0.25
+        p = math.exp(-k * t)
+        mu, var = x0 * p, x0 * p * (1 - p)
+        mu4 = x0 * p * (1 - p) * (1 + 3 * (x0 - 2) * p * (1 - p))   # binomial 4th central moment
+        assert _zmean(res.mean[kk, 0], mu, var, n) < Z
+        assert _zvar(res.var[kk, 0], var, mu4, n) < Z
+
+
+def test_empty_network_holds_state(oracle_lib):
+    O = oracle_lib
+    m = O.OracleModel(inputs.empty_network((7, 0, 3)))
+    tr = O.trajectory(m, 0, 1, 10.0, 1.0)
+    assert np.all(tr.grid_x == np.array([7, 0, 3]))
+    assert tr.summary["events"] == 0 and tr.summary["absorbed"] == 1
+
+
+# ---------------------------------------------------------------- CME pins
+def _cme_network():
+    """A closed (finite) network exercising C(x,2), C(x,3), both modifier
+    signs and the clamp at 0 (PAPER.md:93 '0 <= beta_R5 <= beta')."""
+    A, B, Cc, P, F, D, E = range(7)
+    return Network(("A", "B", "C", "P", "F", "D", "E"), (5, 4, 0, 3, 0, 0, 0), (
+        _rx([(A, 1), (B, 1)], [(Cc, 1)], 0.3, "A+B->C (k - 0.1 F)", (F, -0.1)),
+        _rx([(Cc, 1)], [(A, 1), (B, 1)], 0.5, "C->A+B"),
+        _rx([(P, 1)], [(F, 1)], 1.0, "P->F"),
+        _rx([(F, 1)], [(P, 1)], 0.5, "F->P"),
+        _rx([(A, 2)], [(D, 1)], 0.05, "2A->D (k + 0.02 F)", (F, +0.02)),
+        _rx([(D, 1)], [(A, 2)], 0.4, "D->2A"),
+        _rx([(B, 3)], [(E, 1)], 0.01, "3B->E"),
+        _rx([(E, 1)], [(B, 3)], 0.3, "E->3B"),
+    ))
+
+
+def _cme_moments(net, times):
+    """Enumerate the reachable states by BFS, build the CTMC generator with
+    propensities written from their definition (math.comb), and return the
+    mean and variance of each species at each time via expm."""
+    def props(x):
+        out = []
+        for rx in net.reactions:
+            h = 1
+            for sp, mm in rx.reactants:
+                h *= math.comb(x[sp], mm)
+            k = rx.rate
+            if rx.modifier_species >= 0:
+                k = max(0.0, k + rx.modifier_coef * x[rx.modifier_species])
+            out.append(k * h)
+        return out
+
+    def apply(x, rx):
+        y = list(x)
+        for sp, mm in rx.reactants:
+            y[sp] -= mm
+        for sp, mm in rx.products:
+            y[sp] += mm
+        return tuple(y)
+
+    x0 = tuple(net.x0)
+    index = {x0: 0}
+    states = [x0]
+    q = [x0]
+    while q:
+        x = q.pop()
+        for rx, a in zip(net.reactions, props(x)):
+            if a > 0:
+                y = apply(x, rx)
+                if y not in index:
+                    index[y] = len(states)
+                    states.append(y)
+                    q.append(y)
+    n = len(states)
+    Q = np.zeros((n, n))
+    for i, x in enumerate(states):
+        for rx, a in zip(net.reactions, props(x)):
+            if a > 0:
+                Q[i, index[apply(x, rx)]] += a
+                Q[i, i] -= a
+    X = np.array(states, dtype=np.float64)
+    p0 = np.zeros(n)
+    p0[0] = 1.0
+    out = []
+    for t in times:
+        p = p0 @ scipy.linalg.expm(Q * t)
+        assert abs(p.sum() - 1) < 1e-9
+        mu = p @ X
+        var = p @ (X - mu) ** 2
+        mu4 = p @ (X - mu) ** 4
+        out.append((mu, var, mu4))
+    return out, n
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_cme_closed_network(oracle_lib, mode):
+    O = oracle_lib
+    net = _cme_network()
+    t_end, dt, n = 3.0, 0.5, 20000
+    times = [k * dt for k in range(int(t_end / dt) + 1)]
+    ref, nstates = _cme_moments(net, times)
+    assert nstates > 50
+    res = O.run(O.OracleModel(net), np.arange(n), 99 + mode, t_end, dt, mode, keep=False)
+    assert res.status == 0
+    for k, (mu, var, mu4) in enumerate(ref):
+        for s in range(net.S):
+            assert _zmean(res.mean[k, s], mu[s], var[s], n) < Z, (k, s)
+            assert _zvar(res.var[k, s], var[s], mu4[s], n) < Z, (k, s)
+
+
+def test_cme_dimerization_pins_binomial_factor(oracle_lib):
+    """Config-1 reaction types with S1(0)=12 (a 140-state chain): the C(x,2)
+    convention is pinned -- the ordered x(x-1) reading doubles the
+    dimerisation rate and fails these z-tests."""
+    O = oracle_lib
+    net = inputs.dimerization(12, c=(0.2, 0.1, 0.5, 0.04))
+    t_end, dt, n = 4.0, 0.5, 20000
+    times = [k * dt for k in range(int(t_end / dt) + 1)]
+    ref, nstates = _cme_moments(net, times)
+    res = O.run(O.OracleModel(net), np.arange(n), 7, t_end, dt, keep=False)
+    for k, (mu, var, mu4) in enumerate(ref):
+        for s in range(3):
+            assert _zmean(res.mean[k, s], mu[s], var[s], n) < Z, (k, s)
+            assert _zvar(res.var[k, s], var[s], mu4[s], n) < Z, (k, s)
+    # the alternative (ordered-pairs) reading is rejected by the same data
+    alt = inputs.dimerization(12, c=(0.2, 0.2, 0.5, 0.04))
+    ref_alt, _ = _cme_moments(alt, times)
+    worst = max(_zmean(res.mean[k, 1], ref_alt[k][0][1], ref_alt[k][1][1], n) for k in range(1, len(times)))
+    assert worst > 10
+
+
+# ---------------------------------------------------------------- HIV
+def test_hiv_structure_and_event_rate(oracle_lib):
+    """Table 1 invariants: U0 is a catalyst (U0 == 1 always); F is never
+    consumed (nondecreasing); counts stay >= 0.  Event-rate calibration:
+    ~150M simulation points per 4000 days = 3.75e6 per 100 d."""
+    O = oracle_lib
+    cfg = inputs.config(2)
+    m = O.OracleModel(cfg.network)
+    res = O.run(m, np.arange(2), cfg.seed, cfg.t_end, cfg.dt)
+    assert res.status == 0
+    gx = res.grid_x
+    assert np.all(gx[:, :, 0] == 1)
+    assert np.all(np.diff(gx[:, :, 9], axis=1) >= 0)
+    assert np.all(gx >= 0)
+    assert np.all(res.var[:, 0] == 0) and np.all(res.mean[:, 0] == 1)
+    ev = res.summaries["events"].astype(float)
+    assert np.all(np.abs(ev / 3.75e6 - 1) < 0.2), ev
+    assert np.all(np.diff(res.grid_e, axis=1) >= 0)
+    assert np.all(res.grid_e[:, -1] == res.summaries["events"])
+
+
+def test_determinism_and_independence(oracle_lib):
+    O = oracle_lib
+    m = O.OracleModel(inputs.dimerization())
+    a = O.trajectory(m, 5, 2, 20.0, 0.1)
+    b = O.trajectory(m, 5, 2, 20.0, 0.1)
+    c = O.trajectory(m, 6, 2, 20.0, 0.1)
+    d = O.trajectory(m, 5, 3, 20.0, 0.1)
+    assert a.summary == b.summary and np.array_equal(a.grid_x, b.grid_x)
+    assert a.summary["hash"] != c.summary["hash"] and a.summary["hash"] != d.summary["hash"]
+    # the grid times of the last applied event are bounded by the grid
+    G = a.grid_t.shape[0]
+    assert np.all(a.grid_t <= np.arange(G) * 0.1 + 1e-15)
