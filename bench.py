@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the ensemble-SSA hot path on B200 (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...
+
+A step is one pass of the whole hot path over one
+batch: BASELINE.json configs[2] (the paper's HIV model, Table 1 / PAPER.md:62-93,
+2^18 trajectories over 100 days, grid dt = 1 day, seed 3) per GPU.  Multi-GPU
+is weak scaling: rank r simulates the aligned id shard r of 2^18 * N
+trajectories (ssa_run_shard), the per-GPU moment roots are all-gathered with
+NCCL and merged in fixed rank order (ssa_merge_roots).
+
+Metric: SSA events/s (applied events of the whole job / max-over-ranks device
+time); trajectories/s alongside.  `roofline` reports the issue-slot roofline of
+the dominant kernel (K1, the SSA event loop) against an algorithmic
+instruction count per event.  `cpu_baseline` times the CPU
+oracle (test infrastructure, rank 0 only) on a bounded sample of the same
+workload on this host's cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+# ---------------------------------------------------------------- helpers
+def alg_instr_per_event(net, path: int) -> float:
+    """Algorithmic thread-instructions per applied event of the thread path
+    (DESIGN.md §7): what a minimal implementation of a2-a8 must issue."""
+    philox = 40          # 10 rounds x (2 wide multiplies + 2 three-input xors)
+    u53 = 6              # 2 x (shift/or + 2 exact adds)
+    plog = 35            # frexp, range fold, 1 divide (~8), 10-term Horner, recombination
+    tau = 9              # IEEE divide (~8) + add
+    props = 0
+    for r in net.reactions:
+        fac = sum(0 if m == 1 else (3 if m == 2 else 14) for _, m in r.reactants)
+        props += fac + max(len(r.reactants) - 1, 0) + (1 if r.reactants else 0)
+        if r.modifier_species >= 0:
+            props += 3
+    R = net.R
+    prefix = max(R - 1, 0)
+    select = 2 * max(R - 1, 0)   # compare + predicated add per prefix entry
+    update = 4
+    rest = 1 + 2 + 5 + 3          # r = u2 a0, grid check, hash, counter/loop
+    return philox + u53 + plog + tau + props + prefix + select + update + rest
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], stdout=subprocess.PIPE,
+                                     stderr=subprocess.DEVNULL, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for name, v in zip(names, s[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        power = [float(s[3]) for s in self.samples if s[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "power_w_max": max(power) if power else None,
+                "samples": len(self.samples)}
+
+
+def _oracle_worker(args):
+    net_cfg, ids, seed, t_end, dt = args
+    import inputs
+    from oracle import oracle as O
+    cfg = inputs.config(net_cfg)
+    r = O.run(O.OracleModel(cfg.network), ids, seed, t_end, dt, 0, keep=True)
+    return int(r.summaries["events"].sum()), len(ids)
+
+
+def oracle_sample(cfg_index: int, n_traj: int, cores: int, t_end=None):
+    """Time the unmodified CPU oracle on `n_traj` trajectories of the config,
+    spread over `cores` worker processes.  Returns (events, trajectories, seconds)."""
+    import multiprocessing as mp
+
+    import inputs
+    cfg = inputs.config(cfg_index)
+    t_end = t_end or cfg.t_end
+    ids = list(range(n_traj))
+    parts = [ids[i::cores] for i in range(cores) if ids[i::cores]]
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(len(parts)) as pool:
+        outs = pool.map(_oracle_worker, [(cfg_index, p, cfg.seed, t_end, cfg.dt) for p in parts])
+    dt = time.perf_counter() - t0
+    return sum(o[0] for o in outs), sum(o[1] for o in outs), dt
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle, as it stands, on this host's cores."""
+    if rank != 0:
+        return 0
+    import inputs
+    from oracle import oracle as O
+    O.build()
+    cfg = inputs.config(args.config)
+    cores = host_cores()
+    per_step = max(cores, 8)      # one ~1 s HIV trajectory per core per step
+    for _ in range(args.warmup):
+        oracle_sample(args.config, per_step, cores)
+    ev = tr = 0
+    secs = 0.0
+    for _ in range(args.steps):
+        e, t, s = oracle_sample(args.config, per_step, cores)
+        ev += e; tr += t; secs += s
+    value = ev / secs
+    line = {
+        "impl": "reference", "metric": "ssa_events_per_s", "value": value, "unit": "events/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}-{cfg.name}", "t_end": cfg.t_end, "sample_dt": cfg.dt,
+                   "seed": cfg.seed, "trajectories_per_step": per_step, "parallelism": "cpu-processes"},
+        "trajectories_per_s": tr / secs,
+        "cpu_baseline": {"value": value, "unit": "events/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{per_step} full {cfg.name} trajectories per step (ids 0..{per_step - 1}) "
+                                   f"over {cores} processes"},
+        "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n-per-gpu", type=int, default=0, help="override trajectories per GPU (profiling)")
+    ap.add_argument("--t-end", type=float, default=0.0, help="override horizon (profiling)")
+    ap.add_argument("--path", type=int, default=0)
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import inputs
+    from paper_1007_1768_b200 import build as B
+    B.build()
+    from paper_1007_1768_b200 import ssa as S
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = inputs.config(args.config)
+    net = cfg.network
+    n_per = args.n_per_gpu or cfg.n_trajectories
+    n_total = n_per * world
+    t_end = args.t_end or cfg.t_end
+    dt = cfg.dt
+    G = S.grid_size(t_end, dt)
+    cells = G * net.S
+    b, e = S.shard_bounds(n_total, world, rank)
+    model = S.Model(net)
+    path = args.path or cfg.path
+    opts = dict(block=args.block, blocks_per_sm=args.blocks_per_sm)
+
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    root = torch.zeros((3, cells), dtype=torch.float64, device=dev)
+    roots = torch.zeros((world, 3, cells), dtype=torch.float64, device=dev)
+    out = torch.zeros((4, cells), dtype=torch.float64, device=dev)
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(host_outputs=False):
+        l2.zero_()                                               # flush L2 between steps
+        res = S.run_shard(model, b, e, t_end, dt, cfg.seed, root, path=path, stream=sh, **opts) if e > b else None
+        if world > 1:
+            dist.all_gather_into_tensor(roots.view(-1), root.view(-1))
+        else:
+            roots[0].copy_(root)
+        if host_outputs:
+            merged = S.merge_roots(roots, world, cells, stream=sh)
+            return res, merged
+        S.merge_roots(roots, world, cells, stream=sh, out=out)
+        return res, None
+
+    # JIT + warm-up (untimed)
+    jit0 = time.perf_counter()
+    model.prepare(local_rank, path)
+    jit_s = time.perf_counter() - jit0
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, barrier + sync on both sides, device time via events
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    events = 0
+    ssa_ms = []
+    launches = 0
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res, _ = step()
+            if res is not None:
+                events += res.events
+                ssa_ms.append(res.ssa_ms)
+                launches += res.kernel_launches
+            launches += 2      # merge + finalize of ssa_merge_roots
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms, float(events), float(launches)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms = float(tmax[0])
+        events = int(t[1])
+        launches = int(t[2])
+    value = events / (ms / 1e3)
+    traj_per_s = n_total * args.steps / (ms / 1e3)
+
+    # end to end through the public API with host buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        e2e_steps = max(1, min(args.steps, 2))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_events = 0
+        h2d = d2h = 0
+        for _ in range(e2e_steps):
+            if world == 1:
+                r = S.run(model, n_per, t_end, dt, cfg.seed, path=path, stream=sh, **opts)
+                e2e_events += r.events
+                h2d, d2h = r.h2d_bytes, r.d2h_bytes
+            else:
+                res, merged = step(host_outputs=True)
+                e2e_events += res.events if res else 0
+                h2d = res.h2d_bytes if res else 0
+                d2h = 4 * cells * 8
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        w = torch.tensor([wall, float(e2e_events)], dtype=torch.float64, device=dev)
+        if world > 1:
+            wmax = w.clone()
+            dist.all_reduce(wmax, op=dist.ReduceOp.MAX)
+            dist.all_reduce(w, op=dist.ReduceOp.SUM)
+            wall, e2e_events = float(wmax[0]), int(w[1])
+        e2e = {"value": e2e_events / wall, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+               "note": "ssa_run with host result buffers; wall clock incl. per-run model upload and D2H"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel (K1): issue slots
+    peaks = json.load(open(PEAKS_FILE)) if os.path.exists(PEAKS_FILE) else {}
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    props = torch.cuda.get_device_properties(dev)
+    n_sm = props.multi_processor_count
+    I = alg_instr_per_event(net, path)
+    per_rank_events = events / world / args.steps
+    k1_ms = statistics.mean(ssa_ms) if ssa_ms else float("nan")
+    achieved = per_rank_events * I / 32.0 / (k1_ms / 1e3) / 1e9          # G warp-instr/s
+    peak = n_sm * 4 * sm_max * 1e6 / 1e9                                  # G warp-instr/s
+    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "ssa_k1" if path == 1 else "ssa_k2",
+                "alg_thread_instr_per_event": I, "kernel_ms": k1_ms,
+                "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
+
+    clocks = clk.summary()
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cores = host_cores()
+        n_cpu = max(cores, 8)
+        ce, ct, cs = oracle_sample(args.config, n_cpu, cores, t_end)
+        cpu = {"value": ce / cs, "unit": "events/s", "cores": cores, "kind": "oracle",
+               "sample": f"{n_cpu} full trajectories (ids 0..{n_cpu - 1}) of {cfg.name} over {cores} processes, "
+                         f"{cs:.1f} s wall", "trajectories_per_s": ct / cs}
+
+    line = {
+        "metric": "ssa_events_per_s", "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config{args.config}-{cfg.name}", "model": net.name, "species": net.S,
+                   "reactions": net.R, "n_trajectories_per_gpu": n_per, "global_batch": n_total, "t_end": t_end,
+                   "sample_dt": dt, "grid_points": G, "seed": cfg.seed, "path": "thread" if path == 1 else "warp",
+                   "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
+        "trajectories_per_s": traj_per_s,
+        "events_per_step": events / args.steps,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "jit_s": jit_s,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

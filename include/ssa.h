@@ -1,0 +1,201 @@
+/*
+ * ssa.h -- C ABI of the B200 ensemble-SSA engine (libssa.so).
+ *
+ * The hot path of StochKit-FF (arxiv/paper_1007_1768): many independent
+ * Gillespie direct-method trajectories of a mass-action reaction network
+ * (§2, "The Gillespie's algorithm determines the next transition
+ * and the time at which it occurs"), each aligned online to a common sample
+ * grid and reduced across trajectories to per-species mean and variance --
+ * the paper's "selective memory" (§3.2.1), here on a fixed grid
+ * (BASELINE.json north_star).  The call names follow the paper's statement of
+ * the problem: a model is parameters + integer state vector + stoichiometric
+ * matrix + propensity vector (§3.2), StochRxn_ff() runs copies of
+ * one simulation and reduces them online (§3.2).
+ *
+ * Conventions for every entry point:
+ *  - No exceptions cross the ABI; every call returns an ssa_status.  On error,
+ *    ssa_last_error() returns a thread-local message with the detail
+ *    (validation message, trajectory id and reaction of a numeric error,
+ *    CUDA/NVRTC error string).
+ *  - Host pointers are only read during the call; the library keeps no
+ *    reference to caller memory after returning (ssa_model_create deep-copies).
+ *  - All compute runs on the CUDA device in hand-written sm_100a kernels; the
+ *    library has no CPU fallback.  Without a usable CUDA device ssa_run
+ *    returns SSA_ERR_CUDA.
+ *  - Results are bitwise deterministic for a given (model, N, t_end, dt,
+ *    seed, path): independent of chunk size, block size, scheduling and of how
+ *    trajectories are sharded over GPUs.
+ */
+#ifndef SSA_H
+#define SSA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SSA_OK = 0,
+    SSA_ERR_INVALID_ARG = 1,  /* bad argument (null pointer, t_end <= 0, dt <= 0, N == 0, ...) */
+    SSA_ERR_MODEL = 2,        /* invalid model (bad species index, coef < 1, rate < 0 or non-finite, ...) */
+    SSA_ERR_NUMERIC = 3,      /* a trajectory met a non-finite propensity */
+    SSA_ERR_OVERFLOW = 4,     /* a sampled species count exceeded INT32_MAX */
+    SSA_ERR_OOM = 5,          /* device allocation failed */
+    SSA_ERR_CUDA = 6,         /* CUDA runtime error (no device, launch failure, ...) */
+    SSA_ERR_JIT = 7,          /* NVRTC compilation of the model-specialised kernel failed */
+    SSA_ERR_UNSUPPORTED = 8   /* valid model the requested path cannot run */
+} ssa_status;
+
+/* ------------------------------------------------------------------ model */
+/* One stoichiometric term: `coef` molecules of species `species` (coef >= 1). */
+typedef struct {
+    int32_t species;
+    int32_t coef;
+} ssa_term;
+
+/* One reaction (a column of the stoichiometric matrix + its propensity,
+ * PAPER.md:157).  Mass action: a_j = k^_j * prod_reactants C(x_s, coef)
+ * (unordered combinations, R1); the total reactant order is <= 3 and
+ * each species appears at most once among the reactants (and once among the
+ * products).  Optional linear modifier (beta_R5 = beta - K*F):
+ *   k^_j = max(0, rate + modifier_coef * x[modifier_species]),
+ * modifier_species = -1 for none. */
+typedef struct {
+    int32_t n_reactants;
+    const ssa_term* reactants;
+    int32_t n_products;
+    const ssa_term* products;
+    double rate;
+    int32_t modifier_species;
+    double modifier_coef;
+} ssa_reaction;
+
+typedef struct ssa_model ssa_model;
+
+/* Validate and deep-copy a model.  initial_counts: [n_species], each in
+ * [0, INT32_MAX].  n_species in [1, 16383]; n_reactions in [0, 65535] (0 is
+ * valid: the state is held).  On success *out owns the model;
+ * release it with ssa_model_destroy.  Errors: SSA_ERR_INVALID_ARG (null
+ * pointers), SSA_ERR_MODEL (with the reason in ssa_last_error()).  The model
+ * is immutable and may be used from several threads at once. */
+ssa_status ssa_model_create(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
+                            const ssa_reaction* reactions, ssa_model** out);
+void ssa_model_destroy(ssa_model* model);
+int32_t ssa_model_n_species(const ssa_model* model);
+int32_t ssa_model_n_reactions(const ssa_model* model);
+
+/* Number of grid points G = K + 1, K = floor(t_end/sample_dt + 1e-9); grid
+ * times s_k = k * sample_dt (R15).  Returns 0 for invalid input. */
+uint64_t ssa_grid_size(double t_end, double sample_dt);
+
+/* --------------------------------------------------------------- options */
+enum { SSA_PATH_AUTO = 0, SSA_PATH_THREAD = 1, SSA_PATH_WARP = 2 };
+enum { SSA_REDUCE_MEAN = 1, SSA_REDUCE_VAR = 2 };
+
+/* Per-trajectory record of a dumped trajectory (a11). */
+typedef struct {
+    uint64_t events;       /* applied events (event time <= s_K) */
+    uint64_t hash;         /* h = (h ^ j) * 0x100000001b3 over fired reactions j, from 0xcbf29ce484222325 */
+    double t_last;         /* time of the last applied event (0 if none) */
+    uint64_t near_ties;    /* grid crossings with an event within 1e-9 relative of s_k */
+    int32_t absorbed;      /* 1 if a0 == 0 was reached before s_K */
+    int32_t status;        /* SSA_OK, SSA_ERR_NUMERIC or SSA_ERR_OVERFLOW */
+    int32_t err_reaction;  /* reaction index of a non-finite propensity, else -1 */
+    int32_t pad;
+} ssa_traj_summary;
+
+/* Optional raw-trajectory dump for checking ("the worker can
+ * directly write the full simulation results").  ids: host array, sorted
+ * ascending, unique, each < N (or inside [id_begin, id_end) for a shard).
+ * Output arrays are caller-allocated, host or device memory according to
+ * ssa_run_options.outputs_on_device; any may be NULL. Layouts:
+ *   states    [n][G][S] int32  held state at s_k
+ *   events_at [n][G]   uint64  events applied up to s_k
+ *   time_at   [n][G]   double  time of the last applied event <= s_k (0 if none)
+ *   summary   [n]              per-trajectory record */
+typedef struct {
+    uint64_t n;
+    const uint64_t* ids;
+    int32_t* states;
+    uint64_t* events_at;
+    double* time_at;
+    ssa_traj_summary* summary;
+} ssa_dump;
+
+typedef struct {
+    int32_t path;                  /* SSA_PATH_*: AUTO picks THREAD for R <= 64, else WARP */
+    int32_t device;                /* CUDA device ordinal; -1 = the calling thread's current device */
+    void* stream;                  /* cudaStream_t to run on; NULL = a library-owned stream */
+    uint64_t chunk;                /* trajectories per chunk (power of two); 0 = auto */
+    uint64_t staging_budget_bytes; /* cap on the per-chunk staging buffer; 0 = 32 GiB */
+    int32_t block;                 /* threads per block for K1 / K2; 0 = default */
+    int32_t blocks_per_sm;         /* resident blocks per SM for K1 / K2; 0 = occupancy maximum */
+    const ssa_dump* dump;          /* NULL = no dump */
+    int32_t outputs_on_device;     /* 1: ssa_result arrays and dump arrays are device pointers */
+    int32_t pad;
+} ssa_run_options;
+
+/* Result.  The caller sets the output arrays (any may be NULL), each [G*S]
+ * with cell (k, s) at k*S + s; the call fills the rest. */
+typedef struct {
+    double* mean;              /* ensemble mean */
+    double* var;               /* population variance M2/n (R18) */
+    double* m2;                /* sum of squared deviations */
+    double* count;             /* n per cell */
+    uint64_t events;           /* applied events over all trajectories */
+    uint64_t near_ties;        /* grid crossings flagged as near ties (informational) */
+    uint64_t n_errors;         /* trajectories that ended in SSA_ERR_NUMERIC / OVERFLOW */
+    uint64_t first_error_id;   /* smallest erroring trajectory id (if n_errors > 0) */
+    int32_t first_error_reaction; /* its reaction (numeric errors), else -1 */
+    int32_t path_used;         /* SSA_PATH_THREAD or SSA_PATH_WARP (fixes the summation order) */
+    double device_ms;          /* device time of simulation + reduction (CUDA events) */
+    double ssa_ms;             /* device time inside the SSA kernels (K1/K2) */
+    double jit_ms;             /* host time spent compiling the K1 kernel in this call (0 if cached) */
+    uint64_t h2d_bytes;        /* host->device bytes copied by this call (model tables, dump ids) */
+    uint64_t d2h_bytes;        /* device->host bytes copied by this call (results, dump, counters) */
+    int32_t kernel_launches;   /* kernels this call launched (SSA + reduction + finalize) */
+    int32_t pad2;
+} ssa_result;
+
+/* StochRxn_ff on one GPU: simulate trajectories 0..n_trajectories-1 on
+ * [0, t_end], align each to the grid, reduce to mean/variance.  seed keys the
+ * Philox stream: trajectory i's event e uses counter (e, i) and key seed, so
+ * any trajectory is reproducible in isolation.  reducers: SSA_REDUCE_MEAN |
+ * SSA_REDUCE_VAR (both are always computed; the flags only gate the copies).
+ * Returns the first error by trajectory id: SSA_ERR_NUMERIC/OVERFLOW (detail
+ * in result->first_error_*), or an argument/CUDA/JIT error. */
+ssa_status ssa_run(const ssa_model* model, uint64_t n_trajectories, double t_end, double sample_dt,
+                   uint64_t seed, uint32_t reducers, const ssa_run_options* opts, ssa_result* result);
+
+/* Multi-process form (one process per GPU): simulate ids [id_begin, id_end)
+ * and write their subtree root of the canonical reduction tree to d_root
+ * (DEVICE memory, [3][G*S] doubles: n, mean, M2).  (id_end - id_begin) must
+ * be >= 1 and id_begin a multiple of the next power of two >= (id_end -
+ * id_begin), so the shard is an aligned subtree (R26).  result's
+ * output arrays are ignored; its counters are filled. */
+ssa_status ssa_run_shard(const ssa_model* model, uint64_t id_begin, uint64_t id_end, double t_end,
+                         double sample_dt, uint64_t seed, double* d_root, const ssa_run_options* opts,
+                         ssa_result* result);
+
+/* Merge n_roots shard roots (DEVICE memory, contiguous [n_roots][3][cells],
+ * in rank order, each an aligned subtree of equal span) as the top levels of
+ * the canonical tree, then finalize into result->mean/var/m2/count (host or
+ * device per opts->outputs_on_device).  Every rank obtains bitwise identical
+ * output. */
+ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, uint64_t cells, const ssa_run_options* opts,
+                           ssa_result* result);
+
+/* Compile (NVRTC) and load the model's K1 kernel for a device ahead of time
+ * so that a later ssa_run does no JIT work.  path as in ssa_run_options. */
+ssa_status ssa_model_prepare(const ssa_model* model, int32_t device, int32_t path);
+
+const char* ssa_status_string(ssa_status status);
+const char* ssa_last_error(void);
+int32_t ssa_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSA_H */

@@ -1,0 +1,136 @@
+// k1_thread.cuh -- K1: one trajectory per thread, model-specialised (sm_100a).
+//
+// This text is compiled by NVRTC at run time, after ssa_device.cuh and a
+// generated model section that defines (see jit.cpp):
+//   SSA_S, SSA_R, SSA_K1_BLOCK, SSA_K1_MINB
+//   __constant__ double c_rate[], c_modc[], c_x0[]
+//   ssa_prefix(x, c)      a3 + a4: c_j = c_{j-1} + a_j, sequential order (R13)
+//   ssa_apply(j, x)       a8: x += nu_j (switch over the reaction index)
+//   ssa_first_bad(x)      first reaction with a non-finite propensity
+// so that species counts (fp64, exact integers) and the propensity prefix
+// live in registers, with rates in constant memory (a sweep over rates does
+// not recompile).  The event loop is SURVEY.md §8(a) a1-a8; the definitions
+// are those of DESIGN.md §2 and PAPER.md:60 ("a single transition amongst
+// the possible ones is selected, and the state updated accordingly").
+//
+// Scheduling (north_star (c)): persistent threads; a lane that finishes a
+// trajectory takes the next id from an atomic counter, so lanes are refilled
+// as trajectories end.  Output is keyed by id, so results do not depend on
+// the schedule.
+
+// ssa_k1_params is defined in ssa_device.cuh (shared with the host runtime).
+
+
+extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(const ssa_k1_params P)
+{
+    const double INF = __longlong_as_double(0x7FF0000000000000ll);
+    const double dt = P.dt;
+    const long long K = P.K;
+    const ssa_u64 G = (ssa_u64)K + 1;
+    ssa_u64 my_events = 0, my_ties = 0;
+
+    for (;;) {
+        const ssa_u64 rel = atomicAdd(P.work, 1ull);
+        if (rel >= P.n_ids) break;
+        const ssa_u64 id = P.id_begin + rel;
+        const long long slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
+
+        // a1: initial state
+        double x[SSA_S];
+#pragma unroll
+        for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
+        double t = 0.0;
+        ssa_u64 e = 0;
+        long long k = 0;
+        double s_next = 0.0;
+        ssa_u64 hash = SSA_FNV_OFFSET;
+        ssa_u64 ties = 0;
+        int status = 0, absorbed = 0, err_r = -1;
+        const ssa_u32 idlo = (ssa_u32)id, idhi = (ssa_u32)(id >> 32);
+
+        for (;;) {
+            // a2: one Philox block per candidate event
+            const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)e, (ssa_u32)(e >> 32), idlo, idhi,
+                                                       P.key0, P.key1);
+            // a3 + a4
+            double c[SSA_R > 0 ? SSA_R : 1];
+            const double a0 = ssa_prefix(x, c);
+            // a5
+            double tn;
+            if (a0 > 0.0 && a0 < INF) {
+                const double E = -ssa_plog(ssa_u53(o.o1, o.o0));
+                tn = __dadd_rn(t, __ddiv_rn(E, a0));
+            } else if (a0 == 0.0) {
+                tn = INF;
+                absorbed = 1;
+            } else {
+                status = 1;
+                err_r = ssa_first_bad(x);
+                break;
+            }
+            // a6: grid alignment (selective memory on the grid)
+            if (tn > s_next) {
+                do {
+                    const double tol = __dmul_rn(1e-9, s_next);
+                    const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
+                                      (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
+                    ties += near ? 1 : 0;
+                    int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
+#pragma unroll
+                    for (int s = 0; s < SSA_S; ++s) {
+                        if (x[s] > 2147483647.0) status = 2;
+                        dst[(ssa_u64)s * P.stride] = (int)x[s];
+                    }
+                    if (slot >= 0) {
+                        const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
+#pragma unroll
+                        for (int s = 0; s < SSA_S; ++s) P.dump_states[base * SSA_S + s] = (int)x[s];
+                        P.dump_e[base] = e;
+                        P.dump_t[base] = (e > 0) ? t : 0.0;
+                    }
+                    ++k;
+                    s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+                } while (tn > s_next);
+                if (k > K) break;
+            }
+            // a7: r = u2 a0; j* = #{ j : c_j <= r } (c nondecreasing, r < a0)
+            const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
+            int j = 0;
+#pragma unroll
+            for (int q = 0; q < SSA_R - 1; ++q) j += (c[q] <= r) ? 1 : 0;
+            // a8
+            ssa_apply(j, x);
+            t = tn;
+            ++e;
+            hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
+        }
+
+        my_events += e;
+        my_ties += ties;
+        if (slot >= 0) {
+            ssa_dev_summary sm;
+            sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
+            sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
+            sm.err_reaction = err_r; sm.pad = 0;
+            P.dump_sum[slot] = sm;
+        }
+        if (status) {
+            const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
+            atomicAdd(&P.stats->n_errors, 1ull);
+            atomicOr(&P.stats->err_code, code);
+            // smallest id wins; pack (id, code, reaction) so one atomicMin keeps them together
+            const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
+            atomicMin(&P.stats->first_err_id, packed);
+        }
+    }
+    // warp-level reduction of the counters, then one atomic per warp
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        my_events += __shfl_down_sync(0xffffffffu, my_events, off);
+        my_ties += __shfl_down_sync(0xffffffffu, my_ties, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&P.stats->events, my_events);
+        if (my_ties) atomicAdd(&P.stats->near_ties, my_ties);
+    }
+}

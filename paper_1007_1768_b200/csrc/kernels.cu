@@ -1,0 +1,431 @@
+// kernels.cu -- nvcc-compiled kernels of the ensemble-SSA hot path (sm_100a):
+//   K2  ssa_k2<P>      one trajectory per warp (networks with hundreds of
+//                      reactions): lane-contiguous propensity blocks, a
+//                      Hillis-Steele warp scan, ballot/ffs selection, state in
+//                      shared memory, RNG amortised 32 events per lane
+//                      (north_star (a)), order R13.
+//   K3  ssa_tree_leaf  canonical-tree Welford reduction of a chunk's staged
+//                      grid samples (a9, no atomics: north_star (d)).
+//   K4  ssa_tree_merge merge of partial roots (tiles -> chunk -> shard -> GPUs)
+//       ssa_finalize   mean, population variance = M2/n (a10).
+// K1 (thread path) is model-specialised and compiled by NVRTC (jit.cpp).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ssa_device.cuh"
+#include "ssa_kernels.h"
+
+// =========================================================================
+// K2: warp per trajectory
+// =========================================================================
+// Packed reaction word (see pack_k2 in ssa_api.cpp):
+//   bits [0,2) n_reac; term q: species [2+16q, 16+16q), coef [16+16q, 18+16q);
+//   bits [50,64) modifier species (0x3FFF = none).
+static __device__ __forceinline__ double k2_factor(double x, int m)
+{
+    if (m == 1) return x;
+    const double x1 = __dmul_rn(x, __dadd_rn(x, -1.0));
+    if (m == 2) return __dmul_rn(x1, 0.5);
+    return __ddiv_rn(__dmul_rn(x1, __dadd_rn(x, -2.0)), 6.0);
+}
+
+static __device__ __forceinline__ double k2_propensity(ssa_u64 pk, double rate, const double* __restrict__ x,
+                                                       const double* __restrict__ modc, int j)
+{
+    const int n = (int)(pk & 3ull);
+    double h = 1.0;
+    if (n >= 1) h = k2_factor(x[(int)((pk >> 2) & 0x3FFF)], (int)((pk >> 16) & 3));
+    if (n >= 2) h = __dmul_rn(h, k2_factor(x[(int)((pk >> 18) & 0x3FFF)], (int)((pk >> 32) & 3)));
+    if (n >= 3) h = __dmul_rn(h, k2_factor(x[(int)((pk >> 34) & 0x3FFF)], (int)((pk >> 48) & 3)));
+    double k = rate;
+    const int ms = (int)(pk >> 50);
+    if (ms != 0x3FFF) {
+        k = __dadd_rn(k, __dmul_rn(modc[j], x[ms]));
+        k = (k < 0.0) ? 0.0 : k;
+    }
+    return (n == 0) ? k : __dmul_rn(k, h);
+}
+
+template <int PMAX>
+__global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
+{
+    extern __shared__ double k2_smem[];
+    const int S = P.S, R = P.R, Pl = P.P;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    // shared layout: x[nwarps][S] | modc[R] | x0[S] | nu_off[R+1] (int) | nu_ent[n_ent] (int)
+    double* xs = k2_smem;
+    double* modc = xs + (size_t)nwarps * S;
+    double* x0 = modc + R;
+    int* nu_off = (int*)(x0 + S);
+    int* nu_ent = nu_off + (R + 1);
+    for (int i = threadIdx.x; i < R; i += blockDim.x) modc[i] = P.modc[i];
+    for (int i = threadIdx.x; i < S; i += blockDim.x) x0[i] = P.x0[i];
+    for (int i = threadIdx.x; i <= R; i += blockDim.x) nu_off[i] = P.nu_off[i];
+    for (int i = threadIdx.x; i < P.n_ent; i += blockDim.x) nu_ent[i] = P.nu_ent[i];
+    __syncthreads();
+
+    // this lane's contiguous block of reactions j = lane*P + q
+    ssa_u64 pk[PMAX];
+    double rt[PMAX];
+#pragma unroll
+    for (int q = 0; q < PMAX; ++q) {
+        const int j = lane * Pl + q;
+        const bool own = (q < Pl) && (j < R);
+        pk[q] = own ? P.pk[j] : 0ull;
+        rt[q] = own ? P.rate[j] : 0.0;   // n_reac = 0, rate 0 -> a = 0
+    }
+    double* x = xs + (size_t)warp * S;
+    const double INF = __longlong_as_double(0x7FF0000000000000ll);
+    const double dt = P.dt;
+    const long long K = P.K;
+    const ssa_u64 G = (ssa_u64)K + 1;
+    const unsigned FULL = 0xffffffffu;
+    ssa_u64 my_events = 0, my_ties = 0;
+
+    for (;;) {
+        ssa_u64 rel = 0;
+        if (lane == 0) rel = atomicAdd(P.work, 1ull);
+        rel = __shfl_sync(FULL, rel, 0);
+        if (rel >= P.n_ids) break;
+        const ssa_u64 id = P.id_begin + rel;
+        const long long slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
+        for (int s = lane; s < S; s += 32) x[s] = x0[s];
+        __syncwarp();
+
+        double t = 0.0, s_next = 0.0;
+        ssa_u64 e = 0, hash = SSA_FNV_OFFSET, ties = 0;
+        long long k = 0;
+        int status = 0, absorbed = 0, err_r = -1;
+        const ssa_u32 idlo = (ssa_u32)id, idhi = (ssa_u32)(id >> 32);
+        double Ec = 0.0, U2c = 0.0;
+
+        for (;;) {
+            // a2, amortised: lane l draws event e0 + l for the next 32 events
+            if ((e & 31ull) == 0) {
+                const ssa_u64 ee = e + (ssa_u64)lane;
+                const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)ee, (ssa_u32)(ee >> 32), idlo, idhi,
+                                                           P.key0, P.key1);
+                Ec = -ssa_plog(ssa_u53(o.o1, o.o0));
+                U2c = ssa_u53(o.o3, o.o2);
+            }
+            // a3: this lane's propensities; a4: lane sum then warp scan
+            double a[PMAX];
+            double L = 0.0;
+#pragma unroll
+            for (int q = 0; q < PMAX; ++q) {
+                a[q] = 0.0;
+                if (q < Pl) {
+                    a[q] = k2_propensity(pk[q], rt[q], x, modc, lane * Pl + q);
+                    L = __dadd_rn(L, a[q]);
+                }
+            }
+            double v = L;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double y = __shfl_up_sync(FULL, v, o);
+                if (lane >= o) v = __dadd_rn(y, v);
+            }
+            const double a0 = __shfl_sync(FULL, v, 31);
+            // a5
+            const int src = (int)(e & 31ull);
+            const double E = __shfl_sync(FULL, Ec, src);
+            const double u2 = __shfl_sync(FULL, U2c, src);
+            double tn;
+            if (a0 > 0.0 && a0 < INF) {
+                tn = __dadd_rn(t, __ddiv_rn(E, a0));
+            } else if (a0 == 0.0) {
+                tn = INF;
+                absorbed = 1;
+            } else {
+                status = 1;
+                // first reaction with a non-finite propensity
+                int bad = R;
+#pragma unroll
+                for (int q = PMAX - 1; q >= 0; --q)
+                    if (q < Pl && !(fabs(a[q]) < INF) && lane * Pl + q < R) bad = lane * Pl + q;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
+                err_r = bad < R ? bad : -1;
+                break;
+            }
+            // a6 (warp-uniform)
+            if (tn > s_next) {
+                do {
+                    const double tol = __dmul_rn(1e-9, s_next);
+                    const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
+                                      (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
+                    ties += near ? 1 : 0;
+                    int ovf = 0;
+                    for (int s = lane; s < S; s += 32) {
+                        const double xv = x[s];
+                        ovf |= (xv > 2147483647.0) ? 1 : 0;
+                        P.staging[((ssa_u64)k * S + s) * P.stride + rel] = (int)xv;
+                        if (slot >= 0) P.dump_states[((ssa_u64)slot * G + (ssa_u64)k) * S + s] = (int)xv;
+                    }
+                    if (__any_sync(FULL, ovf)) status = 2;
+                    if (slot >= 0 && lane == 0) {
+                        P.dump_e[(ssa_u64)slot * G + (ssa_u64)k] = e;
+                        P.dump_t[(ssa_u64)slot * G + (ssa_u64)k] = (e > 0) ? t : 0.0;
+                    }
+                    ++k;
+                    s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+                } while (tn > s_next);
+                if (k > K) break;
+            }
+            // a7: lane* = first lane whose inclusive prefix exceeds r
+            const double r = __dmul_rn(u2, a0);
+            const unsigned mask = __ballot_sync(FULL, v > r);
+            const int ls = __ffs(mask) - 1;
+            const double vprev = __shfl_up_sync(FULL, v, 1);
+            int j = -1;
+            if (lane == ls) {
+                double p = (lane > 0) ? vprev : 0.0;
+#pragma unroll
+                for (int q = 0; q < PMAX; ++q) {
+                    if (q < Pl && j < 0) {
+                        p = __dadd_rn(p, a[q]);
+                        if (p > r) j = lane * Pl + q;
+                    }
+                }
+                if (j < 0) {
+#pragma unroll
+                    for (int q = 0; q < PMAX; ++q)
+                        if (q < Pl && a[q] > 0.0) j = lane * Pl + q;
+                }
+            }
+            j = __shfl_sync(FULL, j, ls);
+            if (j < 0) {
+                // rounding fallback: last positive propensity in an earlier lane
+                int lp = -1;
+#pragma unroll
+                for (int q = 0; q < PMAX; ++q)
+                    if (q < Pl && a[q] > 0.0) lp = lane * Pl + q;
+                const unsigned m2 = __ballot_sync(FULL, lp >= 0 && lane < ls);
+                j = __shfl_sync(FULL, lp, 31 - __clz(m2));
+            }
+            // a8
+            const int nb = nu_off[j], ne = nu_off[j + 1];
+            for (int q = nb + lane; q < ne; q += 32) {
+                const int ent = nu_ent[q];
+                const int sp = ent & 0xFFFF;
+                const int d = ent >> 16;          // arithmetic shift: signed delta
+                x[sp] = __dadd_rn(x[sp], (double)d);
+            }
+            __syncwarp();
+            t = tn;
+            ++e;
+            hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            my_events += e;
+            my_ties += ties;
+            if (slot >= 0) {
+                ssa_dev_summary sm;
+                sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
+                sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
+                sm.err_reaction = err_r; sm.pad = 0;
+                P.dump_sum[slot] = sm;
+            }
+            if (status) {
+                const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
+                atomicAdd(&P.stats->n_errors, 1ull);
+                atomicOr(&P.stats->err_code, code);
+                const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
+                atomicMin(&P.stats->first_err_id, packed);
+            }
+        }
+    }
+    if (lane == 0) {
+        atomicAdd(&P.stats->events, my_events);
+        if (my_ties) atomicAdd(&P.stats->near_ties, my_ties);
+    }
+}
+
+size_t ssa_k2_smem_bytes(int S, int R, int n_ent, int block)
+{
+    return sizeof(double) * ((size_t)(block / 32) * S + R + S) + sizeof(int) * ((size_t)R + 1 + n_ent);
+}
+
+cudaError_t ssa_k2_launch(const ssa_k2_params& p, int grid, int block, cudaStream_t st)
+{
+    const size_t smem = ssa_k2_smem_bytes(p.S, p.R, p.n_ent, block);
+    const void* fn = nullptr;
+    switch (p.PMAX) {
+    case 1: fn = (const void*)ssa_k2<1>; break;
+    case 2: fn = (const void*)ssa_k2<2>; break;
+    case 4: fn = (const void*)ssa_k2<4>; break;
+    case 8: fn = (const void*)ssa_k2<8>; break;
+    case 16: fn = (const void*)ssa_k2<16>; break;
+    default: return cudaErrorInvalidValue;
+    }
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    void* args[] = {(void*)&p};
+    return cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, st);
+}
+
+int ssa_k2_max_blocks_per_sm(int pmax, int block, size_t smem)
+{
+    int n = 0;
+    const void* fn = nullptr;
+    switch (pmax) {
+    case 1: fn = (const void*)ssa_k2<1>; break;
+    case 2: fn = (const void*)ssa_k2<2>; break;
+    case 4: fn = (const void*)ssa_k2<4>; break;
+    case 8: fn = (const void*)ssa_k2<8>; break;
+    case 16: fn = (const void*)ssa_k2<16>; break;
+    default: return 0;
+    }
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem) != cudaSuccess) return 0;
+    return n;
+}
+
+// =========================================================================
+// K3/K4: canonical-tree Welford reduction (no atomics)
+// =========================================================================
+// One block reduces SSA_TREE_SPAN = 8 * SSA_TREE_BLOCK consecutive leaves of
+// one row (a (k, s) cell) into one partial: a thread folds 8 adjacent leaves
+// as a perfect tree, warps combine adjacent subtrees with shuffles at offsets
+// 1..16, and the 8 warps combine in shared memory -- every level merges two
+// adjacent, equal-size, aligned subtrees (lower ids on the left), so the
+// composition over passes is the perfect binary tree over the ids (R26).
+// Leaves past `count` are empty (n = 0), the identity of the merge.
+static __device__ __forceinline__ ssa_welford tree_block(ssa_welford w)
+{
+    __shared__ ssa_welford sh[SSA_TREE_BLOCK / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        ssa_welford b;
+        b.n = __shfl_down_sync(0xffffffffu, w.n, o);
+        b.mean = __shfl_down_sync(0xffffffffu, w.mean, o);
+        b.m2 = __shfl_down_sync(0xffffffffu, w.m2, o);
+        if ((lane & (2 * o - 1)) == 0) w = ssa_welford_merge(w, b);
+    }
+    if (lane == 0) sh[warp] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ssa_welford v[SSA_TREE_BLOCK / 32];
+#pragma unroll
+        for (int i = 0; i < SSA_TREE_BLOCK / 32; ++i) v[i] = sh[i];
+#pragma unroll
+        for (int o = 1; o < SSA_TREE_BLOCK / 32; o <<= 1)
+#pragma unroll
+            for (int i = 0; i + o < SSA_TREE_BLOCK / 32; i += 2 * o) v[i] = ssa_welford_merge(v[i], v[i + o]);
+        w = v[0];
+    }
+    return w;
+}
+
+static __device__ __forceinline__ ssa_welford fold8(ssa_welford v[8])
+{
+    v[0] = ssa_welford_merge(v[0], v[1]);
+    v[2] = ssa_welford_merge(v[2], v[3]);
+    v[4] = ssa_welford_merge(v[4], v[5]);
+    v[6] = ssa_welford_merge(v[6], v[7]);
+    v[0] = ssa_welford_merge(v[0], v[2]);
+    v[4] = ssa_welford_merge(v[4], v[6]);
+    return ssa_welford_merge(v[0], v[4]);
+}
+
+// leaves: staging row r = blockIdx.y (+ 65535 * blockIdx.z), ids [0, count)
+__global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __restrict__ staging, ssa_u64 stride,
+                                                                ssa_u64 count, ssa_u64 rows, ssa_tree_out out)
+{
+    const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    if (row >= rows) return;
+    const ssa_u64 base = (ssa_u64)blockIdx.x * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
+    const int* src = staging + row * stride;
+    ssa_welford v[8];
+    if (base + 8 <= count && (stride % 4) == 0) {
+        const int4 q0 = *reinterpret_cast<const int4*>(src + base);
+        const int4 q1 = *reinterpret_cast<const int4*>(src + base + 4);
+        v[0] = ssa_welford_leaf(q0.x); v[1] = ssa_welford_leaf(q0.y);
+        v[2] = ssa_welford_leaf(q0.z); v[3] = ssa_welford_leaf(q0.w);
+        v[4] = ssa_welford_leaf(q1.x); v[5] = ssa_welford_leaf(q1.y);
+        v[6] = ssa_welford_leaf(q1.z); v[7] = ssa_welford_leaf(q1.w);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            v[i] = (base + i < count) ? ssa_welford_leaf(src[base + i]) : ssa_welford_empty();
+    }
+    ssa_welford w = tree_block(fold8(v));
+    if (threadIdx.x == 0) {
+        const ssa_u64 o = row * out.row_stride + (ssa_u64)blockIdx.x * out.elem_stride + out.offset;
+        out.n[o] = w.n; out.mean[o] = w.mean; out.m2[o] = w.m2;
+    }
+}
+
+// partials: element (row, i) at in.{n,mean,m2}[row*in.row_stride + i*in.elem_stride], i < count
+__global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_merge(const ssa_tree_in in, ssa_u64 count, ssa_u64 rows,
+                                                                 ssa_tree_out out)
+{
+    const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    if (row >= rows) return;
+    const ssa_u64 base = (ssa_u64)blockIdx.x * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
+    ssa_welford v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (base + i < count) {
+            const ssa_u64 a = row * in.row_stride + (base + i) * in.elem_stride;
+            v[i].n = in.n[a]; v[i].mean = in.mean[a]; v[i].m2 = in.m2[a];
+        } else {
+            v[i] = ssa_welford_empty();
+        }
+    }
+    ssa_welford w = tree_block(fold8(v));
+    if (threadIdx.x == 0) {
+        const ssa_u64 o = row * out.row_stride + (ssa_u64)blockIdx.x * out.elem_stride + out.offset;
+        out.n[o] = w.n; out.mean[o] = w.mean; out.m2[o] = w.m2;
+    }
+}
+
+// root (n, mean, m2) per cell -> mean, var = M2/n, m2, count
+__global__ void ssa_finalize(const double* __restrict__ n, const double* __restrict__ mean,
+                             const double* __restrict__ m2, ssa_u64 cells, double* o_mean, double* o_var,
+                             double* o_m2, double* o_count)
+{
+    const ssa_u64 i = (ssa_u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cells) return;
+    const double nn = n[i];
+    if (o_mean) o_mean[i] = nn > 0.0 ? mean[i] : 0.0;
+    if (o_var) o_var[i] = nn > 0.0 ? __ddiv_rn(m2[i], nn) : 0.0;
+    if (o_m2) o_m2[i] = m2[i];
+    if (o_count) o_count[i] = nn;
+}
+
+static dim3 tree_grid(ssa_u64 blocks_x, ssa_u64 rows)
+{
+    const ssa_u64 y = rows < 65535ull ? rows : 65535ull;
+    const ssa_u64 z = (rows + 65534ull) / 65535ull;
+    return dim3((unsigned)blocks_x, (unsigned)y, (unsigned)z);
+}
+
+cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 count, ssa_u64 rows,
+                                 const ssa_tree_out& out, cudaStream_t st)
+{
+    const ssa_u64 bx = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
+    ssa_tree_leaf<<<tree_grid(bx ? bx : 1, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, count, rows, out);
+    return cudaGetLastError();
+}
+
+cudaError_t ssa_tree_merge_launch(const ssa_tree_in& in, ssa_u64 count, ssa_u64 rows, const ssa_tree_out& out,
+                                  cudaStream_t st)
+{
+    const ssa_u64 bx = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
+    ssa_tree_merge<<<tree_grid(bx ? bx : 1, rows), SSA_TREE_BLOCK, 0, st>>>(in, count, rows, out);
+    return cudaGetLastError();
+}
+
+cudaError_t ssa_finalize_launch(const double* n, const double* mean, const double* m2, ssa_u64 cells,
+                                double* o_mean, double* o_var, double* o_m2, double* o_count, cudaStream_t st)
+{
+    const unsigned b = 256;
+    const ssa_u64 g = (cells + b - 1) / b;
+    ssa_finalize<<<(unsigned)(g ? g : 1), b, 0, st>>>(n, mean, m2, cells, o_mean, o_var, o_m2, o_count);
+    return cudaGetLastError();
+}

@@ -1,0 +1,929 @@
+// runtime.cu -- the C-ABI library (include/ssa.h): model validation and
+// packing, NVRTC specialisation of K1, chunked launch of the SSA kernels and
+// of the canonical-tree reduction, shard/merge entry points.
+//
+// Host code only (compiled by nvcc so that it can share the device record
+// layouts of ssa_device.cuh); all arithmetic of the method runs in the
+// kernels (k1_thread.cuh via NVRTC, kernels.cu).
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/ssa.h"
+#include "embedded_src.h"
+#include "ssa_device.cuh"
+#include "ssa_kernels.h"
+
+static_assert(sizeof(ssa_dev_summary) == sizeof(ssa_traj_summary), "summary layout");
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static ssa_status fail(ssa_status st, const char* fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(e_ == cudaErrorMemoryAllocation ? SSA_ERR_OOM : SSA_ERR_CUDA, "%s: %s (%s:%d)", \
+                        #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+    } while (0)
+
+#define TRY(expr)                                                                                  \
+    do {                                                                                           \
+        ssa_status s_ = (expr);                                                                    \
+        if (s_ != SSA_OK) return s_;                                                               \
+    } while (0)
+
+// ------------------------------------------------------------------ model
+struct RxI {
+    std::vector<std::pair<int, int>> reac;   // (species, coef) in declared order
+    std::vector<std::pair<int, long long>> nu; // nonzero net change, species ascending
+    double rate = 0.0;
+    int mod_sp = -1;
+    double mod_coef = 0.0;
+};
+
+struct K1Entry {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t fn = nullptr;
+    int block = 0, minb = 0;
+    int blocks_per_sm = 0;
+    void *c_rate = nullptr, *c_modc = nullptr, *c_x0 = nullptr;  // module constant memory
+    std::string log;
+};
+
+struct K2Dev {
+    bool ready = false;
+    int P = 0, PMAX = 0, n_ent = 0;
+    void* dev_image = nullptr;   // one device block holding the tables below
+    void* host_image = nullptr;  // its page-locked host image
+    size_t image_bytes = 0;
+    ssa_u64* pk = nullptr;
+    double *rate = nullptr, *modc = nullptr, *x0 = nullptr;
+    int *nu_off = nullptr, *nu_ent = nullptr;
+};
+
+struct DevCache {
+    std::map<std::pair<int, int>, K1Entry> k1;  // (block, minb)
+    K2Dev k2;
+};
+
+struct ssa_model {
+    int S = 0, R = 0;
+    std::vector<long long> x0;
+    std::vector<RxI> rx;
+    mutable std::mutex mu;
+    mutable std::map<int, DevCache> dev;
+    mutable double* pinned_const = nullptr;  // [rate R'][modc R'][x0 S], page-locked, for per-run uploads
+};
+
+// K1 constant-memory image of the model's numbers (rates, modifier
+// coefficients, initial counts), staged once in page-locked host memory and
+// copied to the device at the start of every run (the run's inputs).
+static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* bytes)
+{
+    const size_t R1 = (size_t)std::max(m.R, 1);
+    *bytes = sizeof(double) * (2 * R1 + (size_t)m.S);
+    if (!m.pinned_const) {
+        CU(cudaMallocHost(&m.pinned_const, *bytes));
+        double* p = m.pinned_const;
+        for (size_t j = 0; j < 2 * R1; ++j) p[j] = 0.0;
+        for (int j = 0; j < m.R; ++j) {
+            p[j] = m.rx[j].rate;
+            p[R1 + j] = m.rx[j].mod_coef;
+        }
+        for (int s = 0; s < m.S; ++s) p[2 * R1 + s] = (double)m.x0[s];
+    }
+    *out = m.pinned_const;
+    return SSA_OK;
+}
+
+extern "C" ssa_status ssa_model_create(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
+                                       const ssa_reaction* reactions, ssa_model** out)
+{
+    if (!out) return fail(SSA_ERR_INVALID_ARG, "out is null");
+    *out = nullptr;
+    if (n_species < 1 || n_species > 16383) return fail(SSA_ERR_MODEL, "n_species %d not in [1, 16383]", n_species);
+    if (n_reactions < 0 || n_reactions > 65535)
+        return fail(SSA_ERR_MODEL, "n_reactions %d not in [0, 65535]", n_reactions);
+    if (!initial_counts) return fail(SSA_ERR_INVALID_ARG, "initial_counts is null");
+    if (n_reactions > 0 && !reactions) return fail(SSA_ERR_INVALID_ARG, "reactions is null");
+    std::unique_ptr<ssa_model> m(new ssa_model);
+    m->S = n_species;
+    m->R = n_reactions;
+    for (int s = 0; s < n_species; ++s) {
+        const int64_t v = initial_counts[s];
+        if (v < 0 || v > 2147483647LL)
+            return fail(SSA_ERR_MODEL, "initial count of species %d is %lld (must be in [0, 2^31-1])", s, (long long)v);
+        m->x0.push_back(v);
+    }
+    for (int j = 0; j < n_reactions; ++j) {
+        const ssa_reaction& r = reactions[j];
+        RxI q;
+        if (r.n_reactants < 0 || r.n_reactants > 3 || r.n_products < 0)
+            return fail(SSA_ERR_MODEL, "reaction %d: bad term counts", j);
+        if ((r.n_reactants && !r.reactants) || (r.n_products && !r.products))
+            return fail(SSA_ERR_INVALID_ARG, "reaction %d: null term array", j);
+        if (!std::isfinite(r.rate) || r.rate < 0.0) return fail(SSA_ERR_MODEL, "reaction %d: rate must be finite and >= 0", j);
+        std::map<int, long long> net;
+        int order = 0;
+        for (int t = 0; t < r.n_reactants; ++t) {
+            const ssa_term& tm = r.reactants[t];
+            if (tm.species < 0 || tm.species >= n_species)
+                return fail(SSA_ERR_MODEL, "reaction %d: unknown reactant species %d", j, tm.species);
+            if (tm.coef < 1) return fail(SSA_ERR_MODEL, "reaction %d: reactant coefficient %d < 1", j, tm.coef);
+            for (auto& pr : q.reac)
+                if (pr.first == tm.species)
+                    return fail(SSA_ERR_MODEL, "reaction %d: species %d listed twice among reactants", j, tm.species);
+            order += tm.coef;
+            q.reac.push_back({tm.species, tm.coef});
+            net[tm.species] -= tm.coef;
+        }
+        if (order > 3) return fail(SSA_ERR_MODEL, "reaction %d: total reactant order %d > 3", j, order);
+        for (int t = 0; t < r.n_products; ++t) {
+            const ssa_term& tm = r.products[t];
+            if (tm.species < 0 || tm.species >= n_species)
+                return fail(SSA_ERR_MODEL, "reaction %d: unknown product species %d", j, tm.species);
+            if (tm.coef < 1 || tm.coef > 1000000)
+                return fail(SSA_ERR_MODEL, "reaction %d: product coefficient %d not in [1, 1e6]", j, tm.coef);
+            net[tm.species] += tm.coef;
+        }
+        for (auto& kv : net)
+            if (kv.second != 0) q.nu.push_back({kv.first, kv.second});
+        q.rate = r.rate;
+        q.mod_sp = r.modifier_species;
+        q.mod_coef = r.modifier_coef;
+        if (q.mod_sp != -1) {
+            if (q.mod_sp < 0 || q.mod_sp >= n_species)
+                return fail(SSA_ERR_MODEL, "reaction %d: unknown modifier species %d", j, q.mod_sp);
+            if (!std::isfinite(q.mod_coef)) return fail(SSA_ERR_MODEL, "reaction %d: non-finite modifier coefficient", j);
+        } else {
+            q.mod_coef = 0.0;
+        }
+        m->rx.push_back(q);
+    }
+    *out = m.release();
+    return SSA_OK;
+}
+
+extern "C" void ssa_model_destroy(ssa_model* m)
+{
+    if (!m) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess) {
+        for (auto& kv : m->dev) {
+            if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+            K2Dev& k = kv.second.k2;
+            if (k.dev_image) cudaFree(k.dev_image);
+            if (k.host_image) cudaFreeHost(k.host_image);
+            for (auto& e : kv.second.k1)
+                if (e.second.lib) cudaLibraryUnload(e.second.lib);
+        }
+        cudaSetDevice(cur);
+    }
+    if (m->pinned_const) cudaFreeHost(m->pinned_const);
+    delete m;
+}
+
+extern "C" int32_t ssa_model_n_species(const ssa_model* m) { return m ? m->S : 0; }
+extern "C" int32_t ssa_model_n_reactions(const ssa_model* m) { return m ? m->R : 0; }
+
+static long long grid_K(double t_end, double dt) { return (long long)std::floor(t_end / dt + 1e-9); }
+
+extern "C" uint64_t ssa_grid_size(double t_end, double dt)
+{
+    if (!(t_end > 0.0) || !(dt > 0.0) || !std::isfinite(t_end) || !std::isfinite(dt)) return 0;
+    const double kk = std::floor(t_end / dt + 1e-9);
+    if (!(kk < 1e12)) return 0;
+    return (uint64_t)kk + 1;
+}
+
+// ------------------------------------------------------------------ K1 JIT
+static std::string factor_expr(int s, int m)
+{
+    std::ostringstream o;
+    if (m == 1) o << "x[" << s << "]";
+    else if (m == 2) o << "__dmul_rn(__dmul_rn(x[" << s << "], __dadd_rn(x[" << s << "], -1.0)), 0.5)";
+    else o << "__ddiv_rn(__dmul_rn(__dmul_rn(x[" << s << "], __dadd_rn(x[" << s << "], -1.0)), __dadd_rn(x[" << s << "], -2.0)), 6.0)";
+    return o.str();
+}
+
+static std::string prop_stmts(const RxI& q, int j)
+{
+    std::ostringstream o;
+    if (q.mod_sp >= 0)
+        o << "k = __dadd_rn(c_rate[" << j << "], __dmul_rn(c_modc[" << j << "], x[" << q.mod_sp << "])); k = (k < 0.0) ? 0.0 : k; ";
+    else
+        o << "k = c_rate[" << j << "]; ";
+    if (q.reac.empty()) {
+        o << "a = k;";
+    } else {
+        o << "h = " << factor_expr(q.reac[0].first, q.reac[0].second) << "; ";
+        for (size_t t = 1; t < q.reac.size(); ++t)
+            o << "h = __dmul_rn(h, " << factor_expr(q.reac[t].first, q.reac[t].second) << "); ";
+        o << "a = __dmul_rn(k, h);";
+    }
+    return o.str();
+}
+
+static std::string gen_k1_model(const ssa_model& m, int block, int minb)
+{
+    const int S = m.S, R = m.R;
+    std::ostringstream o;
+    o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
+      << "\n#define SSA_K1_MINB " << minb << "\n";
+    o << "__constant__ double c_rate[" << std::max(R, 1) << "];\n__constant__ double c_modc[" << std::max(R, 1)
+      << "];\n__constant__ double c_x0[" << S << "];\n";
+    o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], double (&c)[SSA_R > 0 ? SSA_R : 1]) {\n";
+    o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)c;\n";
+    for (int j = 0; j < R; ++j) {
+        o << "  { " << prop_stmts(m.rx[j], j) << " "
+          << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
+    }
+    o << "  return acc;\n}\n";
+    o << "static __device__ __noinline__ int ssa_first_bad(const double (&x)[SSA_S]) {\n";
+    o << "  double a, h, k; (void)a; (void)h; (void)k; (void)x;\n";
+    for (int j = 0; j < R; ++j)
+        o << "  { " << prop_stmts(m.rx[j], j) << " if (!(fabs(a) < __longlong_as_double(0x7FF0000000000000ll))) return " << j << "; }\n";
+    o << "  return -1;\n}\n";
+    o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n  switch (j) {\n";
+    for (int j = 0; j < R; ++j) {
+        if (m.rx[j].nu.empty()) continue;
+        o << "  case " << j << ":";
+        for (auto& d : m.rx[j].nu) o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
+        o << " break;\n";
+    }
+    o << "  default: break;\n  }\n  (void)x;\n}\n";
+    return o.str();
+}
+
+static std::mutex g_jit_mu;
+static std::map<std::string, std::vector<char>> g_cubin_cache;  // source -> cubin
+
+static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin, std::string& log)
+{
+    {
+        std::lock_guard<std::mutex> lk(g_jit_mu);
+        auto it = g_cubin_cache.find(src);
+        if (it != g_cubin_cache.end()) {
+            cubin = it->second;
+            return SSA_OK;
+        }
+    }
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), "ssa_k1.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
+        return fail(SSA_ERR_JIT, "nvrtcCreateProgram failed");
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "--fmad=false", "-lineinfo",
+                          "--ptxas-options=-v", "-DSSA_NVRTC=1"};
+    nvrtcResult rc = nvrtcCompileProgram(prog, (int)(sizeof opts / sizeof opts[0]), opts);
+    size_t log_size = 0;
+    nvrtcGetProgramLogSize(prog, &log_size);
+    log.assign(log_size, '\0');
+    if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+    if (rc != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return fail(SSA_ERR_JIT, "NVRTC compile failed: %s\n%s", nvrtcGetErrorString(rc), log.c_str());
+    }
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    cubin.resize(n);
+    nvrtcGetCUBIN(prog, cubin.data());
+    nvrtcDestroyProgram(&prog);
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    g_cubin_cache[src] = cubin;
+    return SSA_OK;
+}
+
+static std::string k1_full_source(const ssa_model& m, int block, int minb)
+{
+    return std::string(kSsaDeviceSrc) + "\n" + gen_k1_model(m, block, minb) + "\n" + kK1ThreadSrc;
+}
+
+static int default_minb(const ssa_model& m, int block)
+{
+    // target <= 128 registers per thread (512 threads/SM) for small networks;
+    // let large networks spill less by asking for fewer resident blocks.
+    const int threads = m.R <= 64 ? 512 : 256;
+    return std::max(1, threads / block);
+}
+
+// requires: current device == dev, m.mu held
+static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, K1Entry** out, double* jit_ms)
+{
+    DevCache& dc = m.dev[dev];
+    auto key = std::make_pair(block, minb);
+    auto it = dc.k1.find(key);
+    if (it != dc.k1.end()) {
+        *out = &it->second;
+        return SSA_OK;
+    }
+    auto t0 = std::chrono::steady_clock::now();
+    K1Entry e;
+    e.block = block;
+    e.minb = minb;
+    std::vector<char> cubin;
+    TRY(nvrtc_compile(k1_full_source(m, block, minb), cubin, e.log));
+    CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
+    // rates, modifier coefficients and x0 into the module's constant memory
+    std::vector<double> rate(std::max(m.R, 1), 0.0), modc(std::max(m.R, 1), 0.0), x0(m.S);
+    for (int j = 0; j < m.R; ++j) {
+        rate[j] = m.rx[j].rate;
+        modc[j] = m.rx[j].mod_coef;
+    }
+    for (int s = 0; s < m.S; ++s) x0[s] = (double)m.x0[s];
+    size_t bytes = 0;
+    CU(cudaLibraryGetGlobal(&e.c_rate, &bytes, e.lib, "c_rate"));
+    CU(cudaMemcpy(e.c_rate, rate.data(), sizeof(double) * rate.size(), cudaMemcpyHostToDevice));
+    CU(cudaLibraryGetGlobal(&e.c_modc, &bytes, e.lib, "c_modc"));
+    CU(cudaMemcpy(e.c_modc, modc.data(), sizeof(double) * modc.size(), cudaMemcpyHostToDevice));
+    CU(cudaLibraryGetGlobal(&e.c_x0, &bytes, e.lib, "c_x0"));
+    CU(cudaMemcpy(e.c_x0, x0.data(), sizeof(double) * x0.size(), cudaMemcpyHostToDevice));
+    int nb = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)e.fn, block, 0));
+    e.blocks_per_sm = std::max(nb, 1);
+    auto t1 = std::chrono::steady_clock::now();
+    if (jit_ms) *jit_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    auto res = dc.k1.emplace(key, e);
+    *out = &res.first->second;
+    return SSA_OK;
+}
+
+// requires: current device == dev, m.mu held.  The K2 tables live in one
+// device block whose image is kept in page-locked host memory; every run
+// re-uploads it (the run's model inputs) with one async copy.
+static ssa_status ensure_k2(const ssa_model& m, int dev, K2Dev** out)
+{
+    K2Dev& k = m.dev[dev].k2;
+    if (k.ready) {
+        *out = &k;
+        return SSA_OK;
+    }
+    const int R = m.R, S = m.S;
+    const int P = std::max(1, (R + 31) / 32);
+    int PMAX = 1;
+    while (PMAX < P) PMAX <<= 1;
+    if (PMAX > 16) return fail(SSA_ERR_UNSUPPORTED, "warp path supports at most 512 reactions (got %d)", R);
+    const size_t R1 = (size_t)std::max(R, 1);
+    std::vector<ssa_u64> pk(R1, 0);
+    std::vector<double> rate(R1, 0.0), modc(R1, 0.0), x0(S);
+    std::vector<int> nu_off(R + 1, 0), nu_ent;
+    for (int j = 0; j < R; ++j) {
+        const RxI& q = m.rx[j];
+        ssa_u64 w = (ssa_u64)q.reac.size();
+        for (size_t t = 0; t < q.reac.size(); ++t) {
+            w |= (ssa_u64)(q.reac[t].first & 0x3FFF) << (2 + 16 * t);
+            w |= (ssa_u64)(q.reac[t].second & 3) << (16 + 16 * t);
+        }
+        w |= (ssa_u64)(q.mod_sp >= 0 ? q.mod_sp : 0x3FFF) << 50;
+        pk[j] = w;
+        rate[j] = q.rate;
+        modc[j] = q.mod_coef;
+        for (auto& d : q.nu) {
+            if (d.second < -32768 || d.second > 32767)
+                return fail(SSA_ERR_UNSUPPORTED, "warp path: reaction %d changes species %d by %lld (|delta| > 32767)", j,
+                            d.first, d.second);
+            nu_ent.push_back((int)(d.first & 0xFFFF) | (int)((unsigned)(int)d.second << 16));
+        }
+        nu_off[j + 1] = (int)nu_ent.size();
+    }
+    for (int s = 0; s < S; ++s) x0[s] = (double)m.x0[s];
+    if (nu_ent.empty()) nu_ent.push_back(0);
+    // image layout (8-byte aligned sections): pk | rate | modc | x0 | nu_off | nu_ent
+    const size_t o_pk = 0, o_rate = o_pk + 8 * R1, o_modc = o_rate + 8 * R1, o_x0 = o_modc + 8 * R1;
+    const size_t o_off = o_x0 + 8 * (size_t)S;
+    const size_t o_ent = o_off + ((4 * nu_off.size() + 7) & ~(size_t)7);
+    const size_t bytes = o_ent + 4 * nu_ent.size();
+    CU(cudaMallocHost(&k.host_image, bytes));
+    char* h = (char*)k.host_image;
+    memcpy(h + o_pk, pk.data(), 8 * R1);
+    memcpy(h + o_rate, rate.data(), 8 * R1);
+    memcpy(h + o_modc, modc.data(), 8 * R1);
+    memcpy(h + o_x0, x0.data(), 8 * (size_t)S);
+    memcpy(h + o_off, nu_off.data(), 4 * nu_off.size());
+    memcpy(h + o_ent, nu_ent.data(), 4 * nu_ent.size());
+    CU(cudaMalloc(&k.dev_image, bytes));
+    CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
+    char* d = (char*)k.dev_image;
+    k.pk = (ssa_u64*)(d + o_pk);
+    k.rate = (double*)(d + o_rate);
+    k.modc = (double*)(d + o_modc);
+    k.x0 = (double*)(d + o_x0);
+    k.nu_off = (int*)(d + o_off);
+    k.nu_ent = (int*)(d + o_ent);
+    k.image_bytes = bytes;
+    k.P = P;
+    k.PMAX = PMAX;
+    k.n_ent = (int)nu_ent.size();
+    k.ready = true;
+    *out = &k;
+    return SSA_OK;
+}
+
+// ------------------------------------------------------------------ run core
+static ssa_u64 next_pow2(ssa_u64 v)
+{
+    ssa_u64 p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+struct DevBuf {  // stream-ordered device allocation
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    ~DevBuf()
+    {
+        if (p) cudaFreeAsync(p, st);
+    }
+    cudaError_t alloc(size_t bytes, cudaStream_t s)
+    {
+        st = s;
+        return cudaMallocAsync(&p, bytes ? bytes : 8, s);
+    }
+    template <class T> T* as() const { return (T*)p; }
+};
+
+struct Ctx {
+    int device = 0;
+    int prev_device = -1;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    ~Ctx()
+    {
+        if (own_stream && st) {
+            cudaStreamSynchronize(st);
+            cudaStreamDestroy(st);
+        }
+        if (prev_device >= 0) cudaSetDevice(prev_device);
+    }
+};
+
+static ssa_status setup_ctx(const ssa_run_options* o, Ctx& c)
+{
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(SSA_ERR_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    CU(cudaGetDevice(&c.prev_device));
+    c.device = (o && o->device >= 0) ? o->device : c.prev_device;
+    if (c.device >= n) return fail(SSA_ERR_INVALID_ARG, "device %d out of range (%d devices)", c.device, n);
+    CU(cudaSetDevice(c.device));
+    static std::once_flag pool_once[64];
+    if (c.device < 64) {
+        std::call_once(pool_once[c.device], [&] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, c.device) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        });
+    }
+    if (o && o->stream) {
+        c.st = (cudaStream_t)o->stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking));
+        c.own_stream = true;
+    }
+    return SSA_OK;
+}
+
+struct RangeOut {
+    double *n, *mean, *m2;  // device root [cells] each
+};
+
+struct RunInfo {
+    ssa_dev_stats stats;
+    int path = 0;
+    double device_ms = 0, ssa_ms = 0, jit_ms = 0;
+    uint64_t h2d = 0, d2h = 0;
+    int launches = 0;
+};
+
+// Reduce `count` elements per row from `in` down to one, writing the final
+// root into `fin`.  Intermediate passes ping-pong through scratch buffers.
+static ssa_status reduce_partials(ssa_tree_in in, ssa_u64 count, ssa_u64 rows, const ssa_tree_out& fin, cudaStream_t st,
+                                  int* launches)
+{
+    DevBuf bufs[2];
+    int which = 0;
+    while (count > SSA_TREE_SPAN) {
+        const ssa_u64 nout = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
+        DevBuf& b = bufs[which];
+        if (b.p) cudaFreeAsync(b.p, st), b.p = nullptr;
+        CU(b.alloc(sizeof(double) * 3 * rows * nout, st));
+        ssa_tree_out o{b.as<double>(), b.as<double>() + rows * nout, b.as<double>() + 2 * rows * nout, nout, 1, 0};
+        CU(ssa_tree_merge_launch(in, count, rows, o, st));
+        *launches += 1;
+        in = ssa_tree_in{o.n, o.mean, o.m2, nout, 1};
+        count = nout;
+        which ^= 1;
+    }
+    CU(ssa_tree_merge_launch(in, count, rows, fin, st));
+    *launches += 1;
+    return SSA_OK;
+}
+
+static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end, double t_end, double dt,
+                            uint64_t seed, const ssa_run_options* o, Ctx& c, RangeOut root, RunInfo& info,
+                            const ssa_dump* dump, bool dump_on_device)
+{
+    const long long K = grid_K(t_end, dt);
+    const ssa_u64 G = (ssa_u64)K + 1, S = (ssa_u64)m->S, cells = G * S;
+    const ssa_u64 n_ids = id_end - id_begin;
+    const ssa_u64 span = next_pow2(n_ids);
+    // chunk size: a power of two (aligned subtree), staging within the budget
+    const ssa_u64 budget = (o && o->staging_budget_bytes) ? o->staging_budget_bytes : (32ull << 30);
+    ssa_u64 C = span;
+    if (o && o->chunk) {
+        if (o->chunk & (o->chunk - 1)) return fail(SSA_ERR_INVALID_ARG, "chunk %llu is not a power of two", (unsigned long long)o->chunk);
+        C = std::min<ssa_u64>(span, o->chunk);
+    }
+    while (C > 1 && C * cells * 4ull > budget) C >>= 1;
+    const ssa_u64 n_chunks = (n_ids + C - 1) / C;
+
+    int path = o ? o->path : SSA_PATH_AUTO;
+    if (path == SSA_PATH_AUTO) path = (m->R <= 64) ? SSA_PATH_THREAD : SSA_PATH_WARP;
+    if (path != SSA_PATH_THREAD && path != SSA_PATH_WARP) return fail(SSA_ERR_INVALID_ARG, "bad path %d", path);
+    info.path = path;
+
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+
+    // kernels for this model on this device (JIT on first use)
+    K1Entry* k1 = nullptr;
+    K2Dev* k2 = nullptr;
+    int block = (o && o->block > 0) ? o->block : (path == SSA_PATH_THREAD ? 128 : SSA_K2_BLOCK);
+    if (block % 32 || block > 1024) return fail(SSA_ERR_INVALID_ARG, "block %d must be a multiple of 32 <= 1024", block);
+    int grid = 0;
+    {
+        std::lock_guard<std::mutex> lk(m->mu);
+        if (path == SSA_PATH_THREAD) {
+            TRY(ensure_k1(*m, c.device, block, default_minb(*m, block), &k1, &info.jit_ms));
+            int bps = k1->blocks_per_sm;
+            if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
+            grid = sms * bps;
+            grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + block - 1) / block);
+        } else {
+            TRY(ensure_k2(*m, c.device, &k2));
+            const size_t smem = ssa_k2_smem_bytes(m->S, m->R, k2->n_ent, block);
+            if (smem > 227 * 1024) return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", smem);
+            int bps = ssa_k2_max_blocks_per_sm(k2->PMAX, block, smem);
+            if (bps <= 0) return fail(SSA_ERR_CUDA, "warp path: kernel cannot be resident (block %d, smem %zu)", block, smem);
+            if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
+            const int wpb = block / 32;
+            grid = sms * bps;
+            grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + wpb - 1) / wpb);
+        }
+    }
+    grid = std::max(grid, 1);
+    cudaStream_t st = c.st;
+
+    // the run's model inputs: one async copy from page-locked host memory
+    if (path == SSA_PATH_THREAD) {
+        double* pc = nullptr;
+        size_t bytes = 0;
+        {
+            std::lock_guard<std::mutex> lk(m->mu);
+            TRY(pinned_constants(*m, &pc, &bytes));
+        }
+        const size_t R1 = (size_t)std::max(m->R, 1);
+        CU(cudaMemcpyAsync(k1->c_rate, pc, 8 * R1, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(k1->c_modc, pc + R1, 8 * R1, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(k1->c_x0, pc + 2 * R1, 8 * (size_t)m->S, cudaMemcpyHostToDevice, st));
+        info.h2d += bytes;
+    } else {
+        CU(cudaMemcpyAsync(k2->dev_image, k2->host_image, k2->image_bytes, cudaMemcpyHostToDevice, st));
+        info.h2d += k2->image_bytes;
+    }
+
+    // buffers
+    DevBuf staging, tiles, croots, statsb, work, dids, dstates, de, dt_, dsum;
+    const ssa_u64 stride = C;
+    CU(staging.alloc(sizeof(int) * C * cells, st));
+    const ssa_u64 n_tiles = (C + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
+    if (n_tiles > 1) CU(tiles.alloc(sizeof(double) * 3 * cells * n_tiles, st));
+    if (n_chunks > 1) CU(croots.alloc(sizeof(double) * 3 * cells * n_chunks, st));
+    CU(statsb.alloc(sizeof(ssa_dev_stats), st));
+    CU(work.alloc(sizeof(ssa_u64) * n_chunks, st));
+    CU(cudaMemsetAsync(statsb.p, 0, sizeof(ssa_dev_stats), st));
+    CU(cudaMemsetAsync((char*)statsb.p + offsetof(ssa_dev_stats, first_err_id), 0xFF, sizeof(ssa_u64), st));
+    CU(cudaMemsetAsync(work.p, 0, sizeof(ssa_u64) * n_chunks, st));
+
+    // dump
+    ssa_u64 n_dump = dump ? dump->n : 0;
+    int* p_states = nullptr;
+    ssa_u64* p_e = nullptr;
+    double* p_t = nullptr;
+    ssa_dev_summary* p_sum = nullptr;
+    if (n_dump) {
+        if (!dump->ids) return fail(SSA_ERR_INVALID_ARG, "dump ids null");
+        for (ssa_u64 i = 0; i < n_dump; ++i) {
+            if (i && dump->ids[i] <= dump->ids[i - 1]) return fail(SSA_ERR_INVALID_ARG, "dump ids must be sorted and unique");
+            if (dump->ids[i] < id_begin || dump->ids[i] >= id_end)
+                return fail(SSA_ERR_INVALID_ARG, "dump id %llu outside [%llu, %llu)", (unsigned long long)dump->ids[i],
+                            (unsigned long long)id_begin, (unsigned long long)id_end);
+        }
+        CU(dids.alloc(sizeof(ssa_u64) * n_dump, st));
+        CU(cudaMemcpyAsync(dids.p, dump->ids, sizeof(ssa_u64) * n_dump, cudaMemcpyHostToDevice, st));
+        info.h2d += sizeof(ssa_u64) * n_dump;
+        if (dump_on_device) {
+            p_states = dump->states; p_e = (ssa_u64*)dump->events_at; p_t = dump->time_at; p_sum = (ssa_dev_summary*)dump->summary;
+        }
+        if (!p_states) { CU(dstates.alloc(sizeof(int) * n_dump * cells, st)); p_states = dstates.as<int>(); }
+        if (!p_e) { CU(de.alloc(sizeof(ssa_u64) * n_dump * G, st)); p_e = de.as<ssa_u64>(); }
+        if (!p_t) { CU(dt_.alloc(sizeof(double) * n_dump * G, st)); p_t = dt_.as<double>(); }
+        if (!p_sum) { CU(dsum.alloc(sizeof(ssa_dev_summary) * n_dump, st)); p_sum = dsum.as<ssa_dev_summary>(); }
+    }
+
+    cudaEvent_t ev0, ev1, evs0, evs1;
+    CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1)); CU(cudaEventCreate(&evs0)); CU(cudaEventCreate(&evs1));
+    struct EvGuard { cudaEvent_t a, b, c, d; ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c); cudaEventDestroy(d); } } eg{ev0, ev1, evs0, evs1};
+    CU(cudaEventRecord(ev0, st));
+    float ssa_ms_total = 0.f;
+
+    const ssa_u32 key0 = (ssa_u32)seed, key1 = (ssa_u32)(seed >> 32);
+    for (ssa_u64 ch = 0; ch < n_chunks; ++ch) {
+        const ssa_u64 cb = id_begin + ch * C;
+        const ssa_u64 cn = std::min<ssa_u64>(C, id_end - cb);
+        CU(cudaEventRecord(evs0, st));
+        if (path == SSA_PATH_THREAD) {
+            ssa_k1_params p{};
+            p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
+            p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
+            p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
+            p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
+            void* args[] = {&p};
+            CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(block), args, 0, st));
+            info.launches += 1;
+        } else {
+            ssa_k2_params p{};
+            p.S = m->S; p.R = m->R; p.P = k2->P; p.PMAX = k2->PMAX; p.n_ent = k2->n_ent;
+            p.pk = k2->pk; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
+            p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
+            p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
+            p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
+            p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
+            CU(ssa_k2_launch(p, grid, block, st));
+            info.launches += 1;
+        }
+        CU(cudaGetLastError());
+        CU(cudaEventRecord(evs1, st));
+        // a9: chunk reduce -> chunk root (or the range root when there is one chunk)
+        ssa_tree_out chunk_out;
+        if (n_chunks > 1) {
+            double* b = croots.as<double>();
+            chunk_out = ssa_tree_out{b, b + cells * n_chunks, b + 2 * cells * n_chunks, n_chunks, 0, ch};
+        } else {
+            chunk_out = ssa_tree_out{root.n, root.mean, root.m2, 1, 0, 0};
+        }
+        if (n_tiles > 1) {
+            double* b = tiles.as<double>();
+            ssa_tree_out to{b, b + cells * n_tiles, b + 2 * cells * n_tiles, n_tiles, 1, 0};
+            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, to, st));
+            TRY(reduce_partials(ssa_tree_in{to.n, to.mean, to.m2, n_tiles, 1}, n_tiles, cells, chunk_out, st,
+                                &info.launches));
+        } else {
+            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, chunk_out, st));
+        }
+        info.launches += 1;
+        CU(cudaEventSynchronize(evs1));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, evs0, evs1));
+        ssa_ms_total += ms;
+    }
+    // a10 (per GPU): chunk roots -> range root
+    if (n_chunks > 1) {
+        double* b = croots.as<double>();
+        TRY(reduce_partials(ssa_tree_in{b, b + cells * n_chunks, b + 2 * cells * n_chunks, n_chunks, 1}, n_chunks, cells,
+                            ssa_tree_out{root.n, root.mean, root.m2, 1, 0, 0}, st, &info.launches));
+    }
+    CU(cudaEventRecord(ev1, st));
+    CU(cudaMemcpyAsync(&info.stats, statsb.p, sizeof(ssa_dev_stats), cudaMemcpyDeviceToHost, st));
+    info.d2h += sizeof(ssa_dev_stats);
+    if (n_dump && !dump_on_device) {
+        info.d2h += (dump->states ? sizeof(int) * n_dump * cells : 0) + (dump->events_at ? 8 * n_dump * G : 0) +
+                    (dump->time_at ? 8 * n_dump * G : 0) + (dump->summary ? sizeof(ssa_dev_summary) * n_dump : 0);
+        if (dump->states) CU(cudaMemcpyAsync(dump->states, p_states, sizeof(int) * n_dump * cells, cudaMemcpyDeviceToHost, st));
+        if (dump->events_at) CU(cudaMemcpyAsync(dump->events_at, p_e, sizeof(ssa_u64) * n_dump * G, cudaMemcpyDeviceToHost, st));
+        if (dump->time_at) CU(cudaMemcpyAsync(dump->time_at, p_t, sizeof(double) * n_dump * G, cudaMemcpyDeviceToHost, st));
+        if (dump->summary) CU(cudaMemcpyAsync(dump->summary, p_sum, sizeof(ssa_dev_summary) * n_dump, cudaMemcpyDeviceToHost, st));
+    }
+    CU(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, ev0, ev1));
+    info.device_ms = ms;
+    info.ssa_ms = ssa_ms_total;
+    return SSA_OK;
+}
+
+static ssa_status fill_result(const RunInfo& info, ssa_result* r)
+{
+    r->events = info.stats.events;
+    r->near_ties = info.stats.near_ties;
+    r->n_errors = info.stats.n_errors;
+    r->first_error_id = 0;
+    r->first_error_reaction = -1;
+    r->path_used = info.path;
+    r->device_ms = info.device_ms;
+    r->ssa_ms = info.ssa_ms;
+    r->jit_ms = info.jit_ms;
+    r->h2d_bytes = info.h2d;
+    r->d2h_bytes = info.d2h;
+    r->kernel_launches = info.launches;
+    if (info.stats.n_errors) {
+        const ssa_u64 packed = info.stats.first_err_id;
+        const ssa_u64 id = packed >> 24, code = (packed >> 20) & 0xF;
+        const int rx = (int)(packed & 0xFFFFF) - 1;
+        r->first_error_id = id;
+        r->first_error_reaction = rx;
+        if (code == SSA_DEV_ERR_NUMERIC)
+            return fail(SSA_ERR_NUMERIC, "trajectory %llu: non-finite propensity (reaction %d)", (unsigned long long)id, rx);
+        return fail(SSA_ERR_OVERFLOW, "trajectory %llu: species count exceeded INT32_MAX", (unsigned long long)id);
+    }
+    return SSA_OK;
+}
+
+static ssa_status check_common(const ssa_model* m, double t_end, double dt, ssa_result* r)
+{
+    if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
+    if (!r) return fail(SSA_ERR_INVALID_ARG, "result is null");
+    if (!(t_end > 0.0) || !std::isfinite(t_end)) return fail(SSA_ERR_INVALID_ARG, "t_end must be finite and > 0");
+    if (!(dt > 0.0) || !std::isfinite(dt)) return fail(SSA_ERR_INVALID_ARG, "sample_dt must be finite and > 0");
+    if (ssa_grid_size(t_end, dt) == 0 || ssa_grid_size(t_end, dt) > (1ull << 26))
+        return fail(SSA_ERR_INVALID_ARG, "grid too large");
+    return SSA_OK;
+}
+
+static ssa_status finalize_to(const double* rn, const double* rmean, const double* rm2, ssa_u64 cells, uint32_t reducers,
+                              ssa_result* r, bool on_device, cudaStream_t st)
+{
+    double* om = (reducers & SSA_REDUCE_MEAN) ? r->mean : nullptr;
+    double* ov = (reducers & SSA_REDUCE_VAR) ? r->var : nullptr;
+    double* o2 = r->m2;
+    double* oc = r->count;
+    r->kernel_launches += 1;
+    if (on_device) {
+        CU(ssa_finalize_launch(rn, rmean, rm2, cells, om, ov, o2, oc, st));
+        CU(cudaStreamSynchronize(st));
+        return SSA_OK;
+    }
+    r->d2h_bytes += sizeof(double) * cells * ((om ? 1 : 0) + (ov ? 1 : 0) + (o2 ? 1 : 0) + (oc ? 1 : 0));
+    DevBuf out;
+    CU(out.alloc(sizeof(double) * 4 * cells, st));
+    double* d = out.as<double>();
+    CU(ssa_finalize_launch(rn, rmean, rm2, cells, d, d + cells, d + 2 * cells, d + 3 * cells, st));
+    if (om) CU(cudaMemcpyAsync(om, d, sizeof(double) * cells, cudaMemcpyDeviceToHost, st));
+    if (ov) CU(cudaMemcpyAsync(ov, d + cells, sizeof(double) * cells, cudaMemcpyDeviceToHost, st));
+    if (o2) CU(cudaMemcpyAsync(o2, d + 2 * cells, sizeof(double) * cells, cudaMemcpyDeviceToHost, st));
+    if (oc) CU(cudaMemcpyAsync(oc, d + 3 * cells, sizeof(double) * cells, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return SSA_OK;
+}
+
+extern "C" ssa_status ssa_run(const ssa_model* m, uint64_t n_trajectories, double t_end, double sample_dt,
+                              uint64_t seed, uint32_t reducers, const ssa_run_options* o, ssa_result* r)
+{
+    TRY(check_common(m, t_end, sample_dt, r));
+    if (n_trajectories == 0) return fail(SSA_ERR_INVALID_ARG, "n_trajectories must be >= 1");
+    if (n_trajectories > (1ull << 40)) return fail(SSA_ERR_INVALID_ARG, "n_trajectories > 2^40");
+    Ctx c;
+    TRY(setup_ctx(o, c));
+    const ssa_u64 cells = ssa_grid_size(t_end, sample_dt) * (ssa_u64)m->S;
+    DevBuf rootb;
+    CU(rootb.alloc(sizeof(double) * 3 * cells, c.st));
+    double* rb = rootb.as<double>();
+    RunInfo info;
+    const bool on_dev = o && o->outputs_on_device;
+    TRY(run_range(m, 0, n_trajectories, t_end, sample_dt, seed, o, c, RangeOut{rb, rb + cells, rb + 2 * cells}, info,
+                  o ? o->dump : nullptr, on_dev));
+    ssa_status st = fill_result(info, r);
+    TRY(finalize_to(rb, rb + cells, rb + 2 * cells, cells, reducers ? reducers : (SSA_REDUCE_MEAN | SSA_REDUCE_VAR), r,
+                    on_dev, c.st));
+    return st;
+}
+
+extern "C" ssa_status ssa_run_shard(const ssa_model* m, uint64_t id_begin, uint64_t id_end, double t_end,
+                                    double sample_dt, uint64_t seed, double* d_root, const ssa_run_options* o,
+                                    ssa_result* r)
+{
+    TRY(check_common(m, t_end, sample_dt, r));
+    if (!d_root) return fail(SSA_ERR_INVALID_ARG, "d_root is null");
+    if (id_end <= id_begin) return fail(SSA_ERR_INVALID_ARG, "empty shard");
+    if (id_end > (1ull << 40)) return fail(SSA_ERR_INVALID_ARG, "ids beyond 2^40");
+    const ssa_u64 span = next_pow2(id_end - id_begin);
+    if (id_begin % span) return fail(SSA_ERR_INVALID_ARG, "shard [%llu, %llu) is not an aligned subtree", (unsigned long long)id_begin, (unsigned long long)id_end);
+    Ctx c;
+    TRY(setup_ctx(o, c));
+    const ssa_u64 cells = ssa_grid_size(t_end, sample_dt) * (ssa_u64)m->S;
+    RunInfo info;
+    TRY(run_range(m, id_begin, id_end, t_end, sample_dt, seed, o, c, RangeOut{d_root, d_root + cells, d_root + 2 * cells},
+                  info, o ? o->dump : nullptr, o && o->outputs_on_device));
+    return fill_result(info, r);
+}
+
+extern "C" ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, uint64_t cells,
+                                      const ssa_run_options* o, ssa_result* r)
+{
+    if (!d_roots || n_roots < 1 || cells == 0 || !r) return fail(SSA_ERR_INVALID_ARG, "bad merge arguments");
+    Ctx c;
+    TRY(setup_ctx(o, c));
+    DevBuf rootb;
+    CU(rootb.alloc(sizeof(double) * 3 * cells, c.st));
+    double* rb = rootb.as<double>();
+    r->events = r->near_ties = r->n_errors = r->first_error_id = 0;
+    r->first_error_reaction = -1;
+    r->path_used = 0;
+    r->device_ms = r->ssa_ms = r->jit_ms = 0.0;
+    r->h2d_bytes = r->d2h_bytes = 0;
+    r->kernel_launches = 0;
+    // element (cell, rank) at d_roots[rank * 3 * cells + {0,1,2} * cells + cell]
+    TRY(reduce_partials(ssa_tree_in{d_roots, d_roots + cells, d_roots + 2 * cells, 1, 3 * cells}, (ssa_u64)n_roots,
+                        cells, ssa_tree_out{rb, rb + cells, rb + 2 * cells, 1, 0, 0}, c.st, &r->kernel_launches));
+    return finalize_to(rb, rb + cells, rb + 2 * cells, cells, SSA_REDUCE_MEAN | SSA_REDUCE_VAR, r,
+                       o && o->outputs_on_device, c.st);
+}
+
+extern "C" ssa_status ssa_model_prepare(const ssa_model* m, int32_t device, int32_t path)
+{
+    if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
+    ssa_run_options o{};
+    o.device = device;
+    Ctx c;
+    TRY(setup_ctx(&o, c));
+    if (path == SSA_PATH_AUTO) path = (m->R <= 64) ? SSA_PATH_THREAD : SSA_PATH_WARP;
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (path == SSA_PATH_THREAD) {
+        K1Entry* e = nullptr;
+        return ensure_k1(*m, c.device, 128, default_minb(*m, 128), &e, nullptr);
+    }
+    K2Dev* k = nullptr;
+    return ensure_k2(*m, c.device, &k);
+}
+
+// ------------------------------------------------------------------ misc
+extern "C" const char* ssa_status_string(ssa_status s)
+{
+    switch (s) {
+    case SSA_OK: return "ok";
+    case SSA_ERR_INVALID_ARG: return "invalid argument";
+    case SSA_ERR_MODEL: return "invalid model";
+    case SSA_ERR_NUMERIC: return "non-finite propensity";
+    case SSA_ERR_OVERFLOW: return "species count overflow";
+    case SSA_ERR_OOM: return "out of device memory";
+    case SSA_ERR_CUDA: return "CUDA error";
+    case SSA_ERR_JIT: return "NVRTC compilation failed";
+    case SSA_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown status";
+}
+
+extern "C" const char* ssa_last_error(void) { return g_err.c_str(); }
+extern "C" int32_t ssa_abi_version(void) { return 1; }
+
+// Test/diagnostic hooks (not part of the stable ABI): the generated K1
+// source for a model, and compiling it without a device (NVRTC only).
+extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, int32_t minb)
+{
+    static thread_local std::string s;
+    if (!m) return "";
+    s = k1_full_source(*m, block, minb);
+    return s.c_str();
+}
+
+extern "C" ssa_status ssa_debug_k1_compile(const ssa_model* m, int32_t block, int32_t minb, char* log, uint64_t log_cap,
+                                           uint64_t* cubin_bytes)
+{
+    if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
+    std::vector<char> cubin;
+    std::string lg;
+    ssa_status st = nvrtc_compile(k1_full_source(*m, block, minb), cubin, lg);
+    if (log && log_cap) {
+        std::string all = (st == SSA_OK) ? lg : g_err;
+        strncpy(log, all.c_str(), (size_t)log_cap - 1);
+        log[log_cap - 1] = 0;
+    }
+    if (cubin_bytes) *cubin_bytes = cubin.size();
+    return st;
+}

@@ -1,0 +1,307 @@
+"""Thin Python binding of libssa.so (include/ssa.h) -- argument marshalling only.
+
+Every step of the method runs in the library's CUDA kernels; this module only
+packs arguments into the C structs, calls the C ABI with the same names, and
+wraps outputs as numpy arrays (or torch device tensors for the shard/merge
+form).  There is no CPU fallback: if libssa.so is missing or no CUDA device is
+present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libssa.so")
+
+SSA_OK = 0
+SSA_PATH_AUTO, SSA_PATH_THREAD, SSA_PATH_WARP = 0, 1, 2
+SSA_REDUCE_MEAN, SSA_REDUCE_VAR = 1, 2
+STATUS_NAMES = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARG", 2: "SSA_ERR_MODEL", 3: "SSA_ERR_NUMERIC",
+                4: "SSA_ERR_OVERFLOW", 5: "SSA_ERR_OOM", 6: "SSA_ERR_CUDA", 7: "SSA_ERR_JIT",
+                8: "SSA_ERR_UNSUPPORTED"}
+
+
+class SSAError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ssa_term(C.Structure):
+    _fields_ = [("species", C.c_int32), ("coef", C.c_int32)]
+
+
+class ssa_reaction(C.Structure):
+    _fields_ = [("n_reactants", C.c_int32), ("reactants", C.POINTER(ssa_term)),
+                ("n_products", C.c_int32), ("products", C.POINTER(ssa_term)),
+                ("rate", C.c_double), ("modifier_species", C.c_int32), ("modifier_coef", C.c_double)]
+
+
+class ssa_traj_summary(C.Structure):
+    _fields_ = [("events", C.c_uint64), ("hash", C.c_uint64), ("t_last", C.c_double),
+                ("near_ties", C.c_uint64), ("absorbed", C.c_int32), ("status", C.c_int32),
+                ("err_reaction", C.c_int32), ("pad", C.c_int32)]
+
+
+SUMMARY_DTYPE = np.dtype([("events", "<u8"), ("hash", "<u8"), ("t_last", "<f8"), ("near_ties", "<u8"),
+                          ("absorbed", "<i4"), ("status", "<i4"), ("err_reaction", "<i4"), ("pad", "<i4")])
+
+
+class ssa_dump(C.Structure):
+    _fields_ = [("n", C.c_uint64), ("ids", C.POINTER(C.c_uint64)), ("states", C.c_void_p),
+                ("events_at", C.c_void_p), ("time_at", C.c_void_p), ("summary", C.c_void_p)]
+
+
+class ssa_run_options(C.Structure):
+    _fields_ = [("path", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p), ("chunk", C.c_uint64),
+                ("staging_budget_bytes", C.c_uint64), ("block", C.c_int32), ("blocks_per_sm", C.c_int32),
+                ("dump", C.POINTER(ssa_dump)), ("outputs_on_device", C.c_int32), ("pad", C.c_int32)]
+
+
+class ssa_result(C.Structure):
+    _fields_ = [("mean", C.c_void_p), ("var", C.c_void_p), ("m2", C.c_void_p), ("count", C.c_void_p),
+                ("events", C.c_uint64), ("near_ties", C.c_uint64), ("n_errors", C.c_uint64),
+                ("first_error_id", C.c_uint64), ("first_error_reaction", C.c_int32), ("path_used", C.c_int32),
+                ("device_ms", C.c_double), ("ssa_ms", C.c_double), ("jit_ms", C.c_double),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("kernel_launches", C.c_int32),
+                ("pad2", C.c_int32)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libssa.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built: run `python -m paper_1007_1768_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.ssa_model_create.argtypes = [C.c_int32, P(C.c_int64), C.c_int32, P(ssa_reaction), P(C.c_void_p)]
+        L.ssa_model_create.restype = C.c_int
+        L.ssa_model_destroy.argtypes = [C.c_void_p]
+        L.ssa_model_destroy.restype = None
+        L.ssa_model_n_species.argtypes = [C.c_void_p]
+        L.ssa_model_n_reactions.argtypes = [C.c_void_p]
+        L.ssa_grid_size.argtypes = [C.c_double, C.c_double]
+        L.ssa_grid_size.restype = C.c_uint64
+        L.ssa_run.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_uint32,
+                              P(ssa_run_options), P(ssa_result)]
+        L.ssa_run.restype = C.c_int
+        L.ssa_run_shard.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_uint64,
+                                    C.c_void_p, P(ssa_run_options), P(ssa_result)]
+        L.ssa_run_shard.restype = C.c_int
+        L.ssa_merge_roots.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, P(ssa_run_options), P(ssa_result)]
+        L.ssa_merge_roots.restype = C.c_int
+        L.ssa_model_prepare.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        L.ssa_model_prepare.restype = C.c_int
+        L.ssa_status_string.argtypes = [C.c_int]
+        L.ssa_status_string.restype = C.c_char_p
+        L.ssa_last_error.argtypes = []
+        L.ssa_last_error.restype = C.c_char_p
+        L.ssa_abi_version.restype = C.c_int32
+        L.ssa_debug_k1_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        L.ssa_debug_k1_source.restype = C.c_char_p
+        L.ssa_debug_k1_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
+                                           P(C.c_uint64)]
+        L.ssa_debug_k1_compile.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != SSA_OK:
+        raise SSAError(st, lib().ssa_last_error().decode(errors="replace"))
+
+
+def grid_size(t_end: float, dt: float) -> int:
+    return int(lib().ssa_grid_size(t_end, dt))
+
+
+class Model:
+    """ssa_model_create over a network description (species, initial counts,
+    reactions with reactant/product stoichiometry, rate, optional modifier)."""
+
+    def __init__(self, network):
+        self.network = network
+        self.S, self.R = network.S, network.R
+        keep = []
+        rx = (ssa_reaction * max(self.R, 1))()
+        for j, r in enumerate(network.reactions):
+            reac = (ssa_term * max(len(r.reactants), 1))(*[ssa_term(s, m) for s, m in r.reactants])
+            prod = (ssa_term * max(len(r.products), 1))(*[ssa_term(s, m) for s, m in r.products])
+            keep += [reac, prod]
+            rx[j] = ssa_reaction(len(r.reactants), reac, len(r.products), prod, r.rate,
+                                 r.modifier_species, r.modifier_coef)
+        x0 = np.ascontiguousarray(np.array(network.x0, dtype=np.int64))
+        h = C.c_void_p()
+        _check(lib().ssa_model_create(self.S, x0.ctypes.data_as(C.POINTER(C.c_int64)), self.R, rx, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().ssa_model_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def prepare(self, device: int = -1, path: int = SSA_PATH_AUTO):
+        _check(lib().ssa_model_prepare(self.handle, device, path))
+
+    def k1_source(self, block: int = 128, minb: int = 4) -> str:
+        return lib().ssa_debug_k1_source(self.handle, block, minb).decode()
+
+    def k1_compile(self, block: int = 128, minb: int = 4):
+        """NVRTC-compile the model's K1 kernel (no device needed); returns (status, log, cubin bytes)."""
+        buf = C.create_string_buffer(1 << 16)
+        nb = C.c_uint64()
+        st = lib().ssa_debug_k1_compile(self.handle, block, minb, buf, len(buf), C.byref(nb))
+        return st, buf.value.decode(errors="replace"), nb.value
+
+
+@dataclass
+class Dump:
+    ids: np.ndarray            # [n] uint64, sorted
+    states: np.ndarray         # [n, G, S] int32
+    events_at: np.ndarray      # [n, G] uint64
+    time_at: np.ndarray        # [n, G] float64
+    summary: np.ndarray        # [n] SUMMARY_DTYPE
+
+
+@dataclass
+class RunResult:
+    mean: np.ndarray
+    var: np.ndarray
+    m2: np.ndarray
+    count: np.ndarray
+    events: int
+    near_ties: int
+    n_errors: int
+    first_error_id: int
+    first_error_reaction: int
+    path_used: int
+    device_ms: float
+    ssa_ms: float
+    jit_ms: float
+    h2d_bytes: int
+    d2h_bytes: int
+    kernel_launches: int
+    status: int
+    dump: Optional[Dump] = None
+
+
+def _options(path=SSA_PATH_AUTO, device=-1, stream=None, chunk=0, staging_budget_bytes=0, block=0,
+             blocks_per_sm=0, dump=None, outputs_on_device=False) -> ssa_run_options:
+    o = ssa_run_options()
+    o.path, o.device, o.chunk, o.staging_budget_bytes = path, device, chunk, staging_budget_bytes
+    o.stream = stream
+    o.block, o.blocks_per_sm = block, blocks_per_sm
+    o.outputs_on_device = 1 if outputs_on_device else 0
+    if dump is not None:
+        o.dump = C.pointer(dump)
+    return o
+
+
+def _make_dump(ids, G, S):
+    ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
+    n = len(ids)
+    d = Dump(ids, np.zeros((n, G, S), np.int32), np.zeros((n, G), np.uint64), np.zeros((n, G), np.float64),
+             np.zeros(n, SUMMARY_DTYPE))
+    cd = ssa_dump(n, ids.ctypes.data_as(C.POINTER(C.c_uint64)), d.states.ctypes.data, d.events_at.ctypes.data,
+                  d.time_at.ctypes.data, d.summary.ctypes.data)
+    return d, cd
+
+
+def _result_from(r: ssa_result, st: int, mean, var, m2, count, dump=None) -> RunResult:
+    return RunResult(mean, var, m2, count, r.events, r.near_ties, r.n_errors, r.first_error_id,
+                     r.first_error_reaction, r.path_used, r.device_ms, r.ssa_ms, r.jit_ms, r.h2d_bytes,
+                     r.d2h_bytes, r.kernel_launches, st, dump)
+
+
+def run(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed: int, *,
+        reducers: int = SSA_REDUCE_MEAN | SSA_REDUCE_VAR, path: int = SSA_PATH_AUTO, dump_ids=None,
+        raise_on_error: bool = True, **opts) -> RunResult:
+    """ssa_run with host outputs: mean/var/m2/count as [G, S] numpy arrays."""
+    G = grid_size(t_end, sample_dt)
+    S = model.S
+    mean = np.zeros((G, S)); var = np.zeros((G, S)); m2 = np.zeros((G, S)); count = np.zeros((G, S))
+    dump = cdump = None
+    if dump_ids is not None and len(dump_ids):
+        dump, cdump = _make_dump(dump_ids, G, S)
+    o = _options(path=path, dump=cdump, **opts)
+    r = ssa_result()
+    r.mean, r.var, r.m2, r.count = mean.ctypes.data, var.ctypes.data, m2.ctypes.data, count.ctypes.data
+    st = lib().ssa_run(model.handle, n_trajectories, t_end, sample_dt, seed, reducers, C.byref(o), C.byref(r))
+    if st != SSA_OK and (raise_on_error or st not in (3, 4)):
+        _check(st)
+    return _result_from(r, st, mean, var, m2, count, dump)
+
+
+def run_device(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed: int, out, *,
+               path: int = SSA_PATH_AUTO, stream=None, **opts) -> RunResult:
+    """ssa_run with device outputs: `out` is a torch CUDA float64 tensor [4, G, S]
+    receiving mean, var, m2, count (torch used only for device memory)."""
+    o = _options(path=path, stream=stream, outputs_on_device=True, **opts)
+    r = ssa_result()
+    base = out.data_ptr()
+    cells = out.shape[1] * out.shape[2]
+    r.mean, r.var, r.m2, r.count = base, base + 8 * cells, base + 16 * cells, base + 24 * cells
+    st = lib().ssa_run(model.handle, n_trajectories, t_end, sample_dt, seed, SSA_REDUCE_MEAN | SSA_REDUCE_VAR,
+                       C.byref(o), C.byref(r))
+    _check(st)
+    return _result_from(r, st, None, None, None, None)
+
+
+def run_shard(model: Model, id_begin: int, id_end: int, t_end: float, sample_dt: float, seed: int, d_root, *,
+              path: int = SSA_PATH_AUTO, stream=None, dump_ids=None, **opts) -> RunResult:
+    """ssa_run_shard: d_root is a torch CUDA float64 tensor [3, G*S] (n, mean, M2)."""
+    G = grid_size(t_end, sample_dt)
+    dump = cdump = None
+    if dump_ids is not None and len(dump_ids):
+        dump, cdump = _make_dump(dump_ids, G, model.S)
+    o = _options(path=path, stream=stream, dump=cdump, **opts)
+    r = ssa_result()
+    st = lib().ssa_run_shard(model.handle, id_begin, id_end, t_end, sample_dt, seed, C.c_void_p(d_root.data_ptr()),
+                             C.byref(o), C.byref(r))
+    _check(st)
+    return _result_from(r, st, None, None, None, None, dump)
+
+
+def merge_roots(d_roots, n_roots: int, cells: int, *, device: int = -1, stream=None, out=None):
+    """ssa_merge_roots over [n_roots, 3, cells] device roots.  With `out` (a torch
+    CUDA float64 tensor [4, cells]) the outputs stay on the device; otherwise
+    numpy arrays (mean, var, m2, count) are returned."""
+    o = _options(device=device, stream=stream, outputs_on_device=out is not None)
+    r = ssa_result()
+    if out is not None:
+        base = out.data_ptr()
+        r.mean, r.var, r.m2, r.count = base, base + 8 * cells, base + 16 * cells, base + 24 * cells
+        _check(lib().ssa_merge_roots(C.c_void_p(d_roots.data_ptr()), n_roots, cells, C.byref(o), C.byref(r)))
+        return out
+    mean, var, m2, count = (np.zeros(cells) for _ in range(4))
+    r.mean, r.var, r.m2, r.count = mean.ctypes.data, var.ctypes.data, m2.ctypes.data, count.ctypes.data
+    _check(lib().ssa_merge_roots(C.c_void_p(d_roots.data_ptr()), n_roots, cells, C.byref(o), C.byref(r)))
+    return mean, var, m2, count
+
+
+def shard_bounds(n_total: int, world: int, rank: int):
+    """Aligned-subtree shards of the canonical reduction tree (R26):
+    span = next_pow2(n_total) / world (world a power of two)."""
+    assert world >= 1 and (world & (world - 1)) == 0, "world size must be a power of two"
+    p = 1
+    while p < n_total:
+        p <<= 1
+    span = max(p // world, 1)
+    b = min(rank * span, n_total)
+    e = min((rank + 1) * span, n_total)
+    return b, e

@@ -1,0 +1,238 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
+element on the same seeded inputs (north_star rules): integer grid states,
+event counts and firing hashes bit-exact; event times bit-exact (both sides
+use the pinned plog); mean/variance within 1e-9 relative of the oracle's
+exact-integer moments."""
+import numpy as np
+import pytest
+
+import inputs
+from inputs.networks import Network, _rx
+
+from .helpers import assert_dump_equal, assert_moments_close, exact_moments, oracle_replay
+
+pytestmark = pytest.mark.gpu
+
+THREAD, WARP = 1, 2
+MODE = {THREAD: 0, WARP: 1}
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_1007_1768_b200 import build
+    build.build()
+    from paper_1007_1768_b200 import ssa
+    return ssa
+
+
+def _parity(S, net, n, t_end, dt, seed, path, dump_ids=None, **opts):
+    m = S.Model(net)
+    ids = np.arange(n, dtype=np.uint64) if dump_ids is None else np.asarray(dump_ids, np.uint64)
+    r = S.run(m, n, t_end, dt, seed, path=path, dump_ids=ids, **opts)
+    assert r.path_used == path and r.status == 0
+    gx, ge, gt, sm = oracle_replay(net, ids, seed, t_end, dt, MODE[path])
+    assert_dump_equal(r.dump, gx, ge, gt, sm)
+    assert r.events >= int(sm["events"].sum()) if dump_ids is not None else r.events == int(sm["events"].sum())
+    if dump_ids is None:
+        ref_mean, ref_var = exact_moments(gx)
+        assert_moments_close(r.mean, r.var, ref_mean, ref_var)
+        assert np.all(r.count == n)
+    return r, (gx, ge, gt, sm)
+
+
+# ------------------------------------------------------------ configs 0 and 1
+@pytest.mark.parametrize("path", [THREAD, WARP])
+def test_config0_full_parity(S, path):
+    cfg = inputs.config(0)
+    _parity(S, cfg.network, cfg.n_trajectories, cfg.t_end, cfg.dt, cfg.seed, path)
+
+
+@pytest.mark.parametrize("path", [THREAD, WARP])
+def test_config1_parity_ragged(S, path):
+    """Several reduction tiles and a ragged tail (5000 = 2*2048 + 904)."""
+    cfg = inputs.config(1)
+    _parity(S, cfg.network, 5000, cfg.t_end, cfg.dt, cfg.seed, path)
+
+
+def test_config1_full_size(S):
+    """BASELINE configs[1] at full size (65,536 trajectories, ~1e8 events):
+    every trajectory replayed by the oracle."""
+    cfg = inputs.config(1)
+    _parity(S, cfg.network, cfg.n_trajectories, cfg.t_end, cfg.dt, cfg.seed, THREAD)
+
+
+# ------------------------------------------------------------ HIV (configs 2, 4)
+@pytest.mark.parametrize("path", [THREAD, WARP])
+def test_hiv_short_horizon_parity(S, path):
+    cfg = inputs.config(2)
+    _parity(S, cfg.network, 300, 5.0, cfg.dt, cfg.seed, path)
+
+
+def test_hiv_full_horizon_sample(S):
+    """Full 100-day horizon, a handful of whole trajectories, bit-exact."""
+    cfg = inputs.config(2)
+    _parity(S, cfg.network, 16, cfg.t_end, cfg.dt, cfg.seed, THREAD)
+
+
+def test_hiv_config2_full_size_sampled(S):
+    """BASELINE configs[2] at full size (2^18 trajectories, 100 d): oracle replay
+    of 48 sampled trajectories (bit-exact) and exact moments of the whole
+    ensemble from the dumped grid states (T2: checks the tree reduction)."""
+    cfg = inputs.config(2)
+    n = cfg.n_trajectories
+    m = S.Model(cfg.network)
+    all_ids = np.arange(n, dtype=np.uint64)
+    r = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD, dump_ids=all_ids)
+    assert r.status == 0 and r.n_errors == 0
+    ref_mean, ref_var = exact_moments(r.dump.states)
+    assert_moments_close(r.mean, r.var, ref_mean, ref_var)
+    sample = inputs.dump_ids(n, 48, cfg.seed)
+    gx, ge, gt, sm = oracle_replay(cfg.network, sample, cfg.seed, cfg.t_end, cfg.dt, 0)
+    idx = sample.astype(np.int64)
+    assert np.array_equal(r.dump.states[idx], gx)
+    assert np.array_equal(r.dump.events_at[idx], ge)
+    assert np.array_equal(r.dump.time_at[idx], gt)
+    assert np.array_equal(r.dump.summary["hash"][idx], sm["hash"])
+    assert r.events == int(r.dump.summary["events"].sum())
+    # HIV structure: U0 is a catalyst
+    assert np.all(r.mean[:, 0] == 1.0) and np.all(r.var[:, 0] == 0.0)
+
+
+# ------------------------------------------------------------ config 3 (warp path)
+def test_config3_warp_parity(S):
+    cfg = inputs.config(3)
+    _parity(S, cfg.network, 96, cfg.t_end, cfg.dt, cfg.seed, WARP)
+
+
+def test_config3_thread_parity(S):
+    cfg = inputs.config(3)
+    _parity(S, cfg.network, 64, 2.0, cfg.dt, cfg.seed, THREAD)
+
+
+def test_config3_full_size_sampled(S):
+    """BASELINE configs[3] at full size (2^20 trajectories, warp path): sampled
+    bit-exact replay plus T2 over a dumped contiguous block of 2^14 ids."""
+    cfg = inputs.config(3)
+    n = cfg.n_trajectories
+    m = S.Model(cfg.network)
+    ids = inputs.dump_ids(n, 64, cfg.seed)
+    r = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=WARP, dump_ids=ids)
+    assert r.status == 0
+    gx, ge, gt, sm = oracle_replay(cfg.network, ids, cfg.seed, cfg.t_end, cfg.dt, 1)
+    assert_dump_equal(r.dump, gx, ge, gt, sm)
+    assert np.all(r.count == n)
+    # the reduction of the full ensemble equals the merge of shard roots (invariance)
+    import torch
+    G = S.grid_size(cfg.t_end, cfg.dt)
+    cells = G * cfg.network.S
+    roots = torch.zeros((4, 3, cells), dtype=torch.float64, device="cuda")
+    for w in range(4):
+        b, e = S.shard_bounds(n, 4, w)
+        S.run_shard(m, b, e, cfg.t_end, cfg.dt, cfg.seed, roots[w], path=WARP)
+    mean, var, _, _ = S.merge_roots(roots, 4, cells)
+    assert np.array_equal(mean.reshape(G, -1), r.mean) and np.array_equal(var.reshape(G, -1), r.var)
+
+
+# ------------------------------------------------------------ invariance
+def test_chunk_block_and_schedule_invariance(S):
+    """Bitwise identical moments and dumps for any chunk size, block size and
+    residency (R26: chunks are aligned subtrees)."""
+    cfg = inputs.config(1)
+    m = S.Model(cfg.network)
+    n = 3000
+    ids = np.arange(0, n, 7, dtype=np.uint64)
+    base = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD, dump_ids=ids)
+    for opts in (dict(chunk=1024), dict(chunk=256, block=64), dict(block=256, blocks_per_sm=1),
+                 dict(staging_budget_bytes=1 << 20)):
+        r = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD, dump_ids=ids, **opts)
+        assert np.array_equal(r.mean, base.mean) and np.array_equal(r.var, base.var), opts
+        assert np.array_equal(r.m2, base.m2)
+        assert np.array_equal(r.dump.states, base.dump.states)
+    for opts in (dict(chunk=512), dict(block=128)):
+        a = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=WARP)
+        b = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=WARP, **opts)
+        assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
+
+
+@pytest.mark.parametrize("W", [2, 4, 8])
+def test_shard_merge_equals_single_run(S, W):
+    """The multi-GPU form (ssa_run_shard per rank + ssa_merge_roots), run here
+    shard by shard on one GPU: bitwise equal to ssa_run for any W."""
+    import torch
+    cfg = inputs.config(0)
+    m = S.Model(cfg.network)
+    n = 1000
+    base = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD)
+    G = S.grid_size(cfg.t_end, cfg.dt)
+    cells = G * cfg.network.S
+    roots = torch.zeros((W, 3, cells), dtype=torch.float64, device="cuda")
+    events = 0
+    for w in range(W):
+        b, e = S.shard_bounds(n, W, w)
+        if e > b:
+            events += S.run_shard(m, b, e, cfg.t_end, cfg.dt, cfg.seed, roots[w], path=THREAD).events
+    mean, var, m2, count = S.merge_roots(roots, W, cells)
+    assert np.array_equal(mean.reshape(G, -1), base.mean)
+    assert np.array_equal(var.reshape(G, -1), base.var)
+    assert np.array_equal(m2.reshape(G, -1), base.m2)
+    assert events == base.events
+
+
+# ------------------------------------------------------------ edge cases
+def test_edge_cases(S):
+    m = S.Model(inputs.immigration_death())
+    # N = 1, G = 1 (t_end < dt)
+    r = S.run(m, 1, 0.5, 1.0, 9, dump_ids=[0])
+    assert r.mean.shape == (1, 1) and r.mean[0, 0] == 0 and r.var[0, 0] == 0
+    gx, ge, gt, sm = oracle_replay(inputs.immigration_death(), [0], 9, 0.5, 1.0, 0)
+    assert_dump_equal(r.dump, gx, ge, gt, sm)
+    # empty network: held state, absorbed
+    e = S.Model(inputs.empty_network((7, 0, 3)))
+    r = S.run(e, 33, 10.0, 1.0, 1, dump_ids=np.arange(33))
+    assert np.all(r.mean == np.array([7, 0, 3])) and np.all(r.var == 0)
+    assert np.all(r.dump.summary["absorbed"] == 1) and r.events == 0
+    # pure death to extinction (absorbing mid-run), both paths
+    for path in (THREAD, WARP):
+        _parity(S, inputs.pure_death(1.0, 5), 257, 10.0, 0.5, 3, path)
+
+
+def test_numeric_error_reported(S):
+    """A propensity that overflows to inf (SPEC.md:85 'NaN/inf -> hard error
+    naming the reaction'): SSA_ERR_NUMERIC with the id and reaction."""
+    net = Network(("A", "B"), (1, 0), (
+        _rx([], [(1, 1)], 1.0),
+        _rx([(0, 1)], [(0, 2)], 1e308),           # A doubles; a = 1e308 * A overflows at A = 2
+    ))
+    m = S.Model(net)
+    for path in (THREAD, WARP):
+        r = S.run(m, 8, 10.0, 1.0, 1, path=path, dump_ids=np.arange(8), raise_on_error=False)
+        assert r.status == 3 and r.n_errors == 8
+        assert r.first_error_id == 0 and r.first_error_reaction == 1
+        _, _, _, sm = oracle_replay(net, np.arange(8), 1, 10.0, 1.0, MODE[path])
+        assert np.all(sm["status"] == 3) and np.all(sm["err_reaction"] == 1)
+        assert np.array_equal(r.dump.summary["status"], sm["status"])
+        assert np.array_equal(r.dump.summary["err_reaction"], sm["err_reaction"])
+        assert np.array_equal(r.dump.summary["events"], sm["events"])
+
+
+def test_overflow_reported(S):
+    net = Network(("A",), (2**31 - 5,), (_rx([], [(0, 1)], 100.0),))
+    m = S.Model(net)
+    r = S.run(m, 4, 1.0, 0.5, 1, raise_on_error=False)
+    assert r.status == 4 and r.n_errors == 4
+
+
+def test_device_outputs_and_determinism(S):
+    import torch
+    cfg = inputs.config(1)
+    m = S.Model(cfg.network)
+    G = S.grid_size(cfg.t_end, cfg.dt)
+    out = torch.zeros((4, G, 3), dtype=torch.float64, device="cuda")
+    S.run_device(m, 2048, cfg.t_end, cfg.dt, cfg.seed, out, path=THREAD)
+    h = S.run(m, 2048, cfg.t_end, cfg.dt, cfg.seed, path=THREAD)
+    assert np.array_equal(out[0].cpu().numpy(), h.mean) and np.array_equal(out[1].cpu().numpy(), h.var)
+    h2 = S.run(m, 2048, cfg.t_end, cfg.dt, cfg.seed, path=THREAD)
+    assert np.array_equal(h.mean, h2.mean) and h.events == h2.events
