@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
     for (int q = 0; q < PMAX; ++q) {
         const int j = lane * Pl + q;
         const bool own = (q < Pl) && (j < R);
-        pk[q] = own ? P.pk[j] : 0ull;
-        rt[q] = own ? P.rate[j] : 0.0;   // n_reac = 0, rate 0 -> a = 0
+        pk[q] = own ? P.pk[j] : (0x3FFFull << 50);   // no reactants, no modifier
+        rt[q] = own ? P.rate[j] : 0.0;                // rate 0 -> a = 0
     }
     double* x = xs + (size_t)warp * S;
     const double INF = __longlong_as_double(0x7FF0000000000000ll);
