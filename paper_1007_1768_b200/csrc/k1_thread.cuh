@@ -29,98 +29,115 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     const ssa_u64 G = (ssa_u64)K + 1;
     ssa_u64 my_events = 0, my_ties = 0;
 
+    // Per-lane trajectory state.  ONE loop iteration = one candidate event of
+    // the lane's current trajectory; a lane whose trajectory ended refills at
+    // the top of the same loop.  (A nested trajectory/event loop would let
+    // lanes that refilled drift into separate divergent groups that never
+    // reconverge -- here every iteration reconverges at the loop head.)
+    double x[SSA_S];
+    double t = 0.0, s_next = 0.0;
+    ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0;
+    long long k = 0, slot = -1;
+    int status = 0, absorbed = 0, err_r = -1;
+    bool need = true, have = true;
+
     for (;;) {
-        const ssa_u64 rel = atomicAdd(P.work, 1ull);
-        if (rel >= P.n_ids) break;
-        const ssa_u64 id = P.id_begin + rel;
-        const long long slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
-
-        // a1: initial state
-        double x[SSA_S];
+        if (need) {
+            // a1: take the next trajectory id and initialise it.  This block
+            // has a single exit (no break) so the lanes that refill reconverge
+            // with the others right after it.
+            rel = atomicAdd(P.work, 1ull);
+            have = rel < P.n_ids;
+            id = P.id_begin + rel;
+            slot = (have && P.n_dump) ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
 #pragma unroll
-        for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
-        double t = 0.0;
-        ssa_u64 e = 0;
-        long long k = 0;
-        double s_next = 0.0;
-        ssa_u64 hash = SSA_FNV_OFFSET;
-        ssa_u64 ties = 0;
-        int status = 0, absorbed = 0, err_r = -1;
-        const ssa_u32 idlo = (ssa_u32)id, idhi = (ssa_u32)(id >> 32);
-
-        for (;;) {
-            // a2: one Philox block per candidate event
-            const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)e, (ssa_u32)(e >> 32), idlo, idhi,
-                                                       P.key0, P.key1);
-            // a3 + a4
-            double c[SSA_R > 0 ? SSA_R : 1];
-            const double a0 = ssa_prefix(x, c);
-            // a5
-            double tn;
-            if (a0 > 0.0 && a0 < INF) {
-                const double E = -ssa_plog(ssa_u53(o.o1, o.o0));
-                tn = __dadd_rn(t, __ddiv_rn(E, a0));
-            } else if (a0 == 0.0) {
-                tn = INF;
-                absorbed = 1;
-            } else {
-                status = 1;
-                err_r = ssa_first_bad(x);
-                break;
-            }
-            // a6: grid alignment (selective memory on the grid)
-            if (tn > s_next) {
-                do {
-                    const double tol = __dmul_rn(1e-9, s_next);
-                    const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
-                                      (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
-                    ties += near ? 1 : 0;
-                    int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
+            for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
+            t = 0.0; s_next = 0.0; e = 0; k = 0; hash = SSA_FNV_OFFSET; ties = 0;
+            status = 0; absorbed = 0; err_r = -1;
+            need = false;
+        }
+        if (!have) break;   // no work left: this lane is done for good
+        // a2: one Philox block per candidate event, counter (e, id)
+        const ssa_philox_out o = ssa_philox4x32_10_ks((ssa_u32)e, (ssa_u32)(e >> 32), (ssa_u32)id,
+                                                      (ssa_u32)(id >> 32), P.ks);
+        // a3 + a4
+        double c[SSA_R > 0 ? SSA_R : 1];
+        const double a0 = ssa_prefix(x, c);
+        // keep the prefix in registers: without this barrier the compiler
+        // recomputes the whole propensity chain for the selection (a7)
 #pragma unroll
-                    for (int s = 0; s < SSA_S; ++s) {
-                        if (x[s] > 2147483647.0) status = 2;
-                        dst[(ssa_u64)s * P.stride] = (int)x[s];
-                    }
-                    if (slot >= 0) {
-                        const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
+        for (int q = 0; q < SSA_R - 1; ++q) asm volatile("" : "+d"(c[q]));
+        // a5
+        bool fin = false;
+        double tn = INF;
+        if (a0 > 0.0 && a0 < INF) {
+            const double E = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
+            tn = __dadd_rn(t, ssa_div_tau(E, a0));
+        } else if (a0 == 0.0) {
+            absorbed = 1;
+        } else {
+            status = 1;
+            err_r = ssa_first_bad(x);
+            fin = true;
+        }
+        // a6: grid alignment (selective memory on the grid)
+        if (!fin && tn > s_next) {
+            do {
+                const double tol = __dmul_rn(1e-9, s_next);
+                const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
+                                  (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
+                ties += near ? 1 : 0;
+                int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
 #pragma unroll
-                        for (int s = 0; s < SSA_S; ++s) P.dump_states[base * SSA_S + s] = (int)x[s];
-                        P.dump_e[base] = e;
-                        P.dump_t[base] = (e > 0) ? t : 0.0;
-                    }
-                    ++k;
-                    s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
-                } while (tn > s_next);
-                if (k > K) break;
-            }
+                for (int s = 0; s < SSA_S; ++s) {
+                    if (x[s] > 2147483647.0) status = 2;
+                    dst[(ssa_u64)s * P.stride] = (int)x[s];
+                }
+                if (slot >= 0) {
+                    const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
+#pragma unroll
+                    for (int s = 0; s < SSA_S; ++s) P.dump_states[base * SSA_S + s] = (int)x[s];
+                    P.dump_e[base] = e;
+                    P.dump_t[base] = (e > 0) ? t : 0.0;
+                }
+                ++k;
+                s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+            } while (tn > s_next);
+            fin = (k > K);
+        }
+        if (!fin) {
             // a7: r = u2 a0; j* = #{ j : c_j <= r } (c nondecreasing, r < a0)
             const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
             int j = 0;
 #pragma unroll
-            for (int q = 0; q < SSA_R - 1; ++q) j += (c[q] <= r) ? 1 : 0;
+            for (int q = 0; q < SSA_R - 1; ++q)   // compare + predicated increment
+                asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                    : "+r"(j) : "d"(c[q]), "d"(r));
             // a8
             ssa_apply(j, x);
             t = tn;
             ++e;
             hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
-        }
-
-        my_events += e;
-        my_ties += ties;
-        if (slot >= 0) {
-            ssa_dev_summary sm;
-            sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
-            sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
-            sm.err_reaction = err_r; sm.pad = 0;
-            P.dump_sum[slot] = sm;
-        }
-        if (status) {
-            const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
-            atomicAdd(&P.stats->n_errors, 1ull);
-            atomicOr(&P.stats->err_code, code);
-            // smallest id wins; pack (id, code, reaction) so one atomicMin keeps them together
-            const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
-            atomicMin(&P.stats->first_err_id, packed);
+        } else {
+            // trajectory done: per-trajectory records, then refill
+            my_events += e;
+            my_ties += ties;
+            if (slot >= 0) {
+                ssa_dev_summary sm;
+                sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
+                sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
+                sm.err_reaction = err_r; sm.pad = 0;
+                P.dump_sum[slot] = sm;
+            }
+            if (status) {
+                const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
+                atomicAdd(&P.stats->n_errors, 1ull);
+                atomicOr(&P.stats->err_code, code);
+                // smallest id wins; pack (id, code, reaction) so one atomicMin keeps them together
+                const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
+                atomicMin(&P.stats->first_err_id, packed);
+            }
+            need = true;
         }
     }
     // warp-level reduction of the counters, then one atomic per warp

@@ -15,6 +15,8 @@
 #include "ssa_device.cuh"
 #include "ssa_kernels.h"
 
+__constant__ double k2_plog[14] = SSA_PLOG_COEF_INIT;
+
 // =========================================================================
 // K2: warp per trajectory
 // =========================================================================
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
                 const ssa_u64 ee = e + (ssa_u64)lane;
                 const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)ee, (ssa_u32)(ee >> 32), idlo, idhi,
                                                            P.key0, P.key1);
-                Ec = -ssa_plog(ssa_u53(o.o1, o.o0));
+                Ec = -ssa_plog(ssa_u53(o.o1, o.o0), k2_plog);
                 U2c = ssa_u53(o.o3, o.o2);
             }
             // a3: this lane's propensities; a4: lane sum then warp scan
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
             const double u2 = __shfl_sync(FULL, U2c, src);
             double tn;
             if (a0 > 0.0 && a0 < INF) {
-                tn = __dadd_rn(t, __ddiv_rn(E, a0));
+                tn = __dadd_rn(t, ssa_div_tau(E, a0));
             } else if (a0 == 0.0) {
                 tn = INF;
                 absorbed = 1;

@@ -256,6 +256,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb)
       << "\n#define SSA_K1_MINB " << minb << "\n";
     o << "__constant__ double c_rate[" << std::max(R, 1) << "];\n__constant__ double c_modc[" << std::max(R, 1)
       << "];\n__constant__ double c_x0[" << S << "];\n";
+    o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
     o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], double (&c)[SSA_R > 0 ? SSA_R : 1]) {\n";
     o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)c;\n";
     for (int j = 0; j < R; ++j) {
@@ -263,11 +264,18 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb)
           << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
     }
     o << "  return acc;\n}\n";
-    o << "static __device__ __noinline__ int ssa_first_bad(const double (&x)[SSA_S]) {\n";
+    // error path only: out of line, state passed by value so the caller's
+    // counts never need an addressable (stack) copy
+    o << "struct ssa_state_v { double v[SSA_S]; };\n";
+    o << "static __device__ __noinline__ int ssa_first_bad_v(const ssa_state_v xs) {\n";
+    o << "  const double* x = xs.v;\n";
     o << "  double a, h, k; (void)a; (void)h; (void)k; (void)x;\n";
     for (int j = 0; j < R; ++j)
         o << "  { " << prop_stmts(m.rx[j], j) << " if (!(fabs(a) < __longlong_as_double(0x7FF0000000000000ll))) return " << j << "; }\n";
     o << "  return -1;\n}\n";
+    o << "static __device__ __forceinline__ int ssa_first_bad(const double (&x)[SSA_S]) {\n";
+    o << "  ssa_state_v xs;\n#pragma unroll\n  for (int s = 0; s < SSA_S; ++s) xs.v[s] = x[s];\n";
+    o << "  return ssa_first_bad_v(xs);\n}\n";
     o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n  switch (j) {\n";
     for (int j = 0; j < R; ++j) {
         if (m.rx[j].nu.empty()) continue;
@@ -580,7 +588,10 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     {
         std::lock_guard<std::mutex> lk(m->mu);
         if (path == SSA_PATH_THREAD) {
-            TRY(ensure_k1(*m, c.device, block, default_minb(*m, block), &k1, &info.jit_ms));
+            // blocks_per_sm > 0 also sets the K1 variant's __launch_bounds__ residency
+            // target (its register budget is 64K / (block * blocks_per_sm))
+            const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : default_minb(*m, block);
+            TRY(ensure_k1(*m, c.device, block, minb, &k1, &info.jit_ms));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
@@ -672,6 +683,10 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             ssa_k1_params p{};
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
+            for (int r = 0; r < 10; ++r) {  // Philox key schedule (mod 2^32)
+                p.ks[2 * r] = key0 + (ssa_u32)r * 0x9E3779B9u;
+                p.ks[2 * r + 1] = key1 + (ssa_u32)r * 0xBB67AE85u;
+            }
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
             p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
             void* args[] = {&p};
