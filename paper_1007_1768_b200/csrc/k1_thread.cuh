@@ -60,22 +60,39 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // a2: one Philox block per candidate event, counter (e, id)
         const ssa_philox_out o = ssa_philox4x32_10_ks((ssa_u32)e, (ssa_u32)(e >> 32), (ssa_u32)id,
                                                       (ssa_u32)(id >> 32), P.ks);
-        // a3 + a4
+        // a3 + a4 (the propensity prefix chain) and a5's logarithm are
+        // independent dependency chains: both are issued in one basic block
+        // so the scheduler interleaves them.
         double c[SSA_R > 0 ? SSA_R : 1];
         const double a0 = ssa_prefix(x, c);
         // keep the prefix in registers: without this barrier the compiler
         // recomputes the whole propensity chain for the selection (a7)
 #pragma unroll
         for (int q = 0; q < SSA_R - 1; ++q) asm volatile("" : "+d"(c[q]));
-        // a5
+        const double E = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
+        // a7, speculatively (used only if the event is applied): r = u2 a0,
+        // j* = #{ j : c_j <= r } (c nondecreasing, r < a0), counted in four
+        // independent partial sums to shorten the dependency chain.
+        const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
+        int jp[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < SSA_R - 1; ++q)   // compare + predicated increment
+            asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                : "+r"(jp[q & 3]) : "d"(c[q]), "d"(r));
+        const int j = (jp[0] + jp[1]) + (jp[2] + jp[3]);
+        // a5: tau = E / a0 (fast in-range division; the rare cases branch)
         bool fin = false;
-        double tn = INF;
-        if (a0 > 0.0 && a0 < INF) {
-            const double E = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
-            tn = __dadd_rn(t, ssa_div_tau(E, a0));
+        double tn;
+        const unsigned a0hi = (unsigned)__double2hiint(a0);
+        if (a0hi - (123u << 20) < ((1923u - 123u) << 20)) {   // a0 in [2^-900, 2^901)
+            tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
+        } else if (a0 > 0.0 && a0 < INF) {
+            tn = __dadd_rn(t, __ddiv_rn(E, a0));
         } else if (a0 == 0.0) {
+            tn = INF;
             absorbed = 1;
         } else {
+            tn = INF;
             status = 1;
             err_r = ssa_first_bad(x);
             fin = true;
@@ -106,13 +123,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             fin = (k > K);
         }
         if (!fin) {
-            // a7: r = u2 a0; j* = #{ j : c_j <= r } (c nondecreasing, r < a0)
-            const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
-            int j = 0;
-#pragma unroll
-            for (int q = 0; q < SSA_R - 1; ++q)   // compare + predicated increment
-                asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
-                    : "+r"(j) : "d"(c[q]), "d"(r));
             // a8
             ssa_apply(j, x);
             t = tn;
