@@ -20,70 +20,91 @@ __constant__ double k2_plog[14] = SSA_PLOG_COEF_INIT;
 // =========================================================================
 // K2: warp per trajectory
 // =========================================================================
-// Packed reaction word (see pack_k2 in ssa_api.cpp):
+// Propensities live in shared memory, laid out [q][lane] for the lane-
+// contiguous blocks j = lane*P + q (conflict-free), and after each event only
+// the reactions that read a changed species are recomputed (dependency graph,
+// a_j is a pure function of x, so the cached values are
+// bit-identical to a full recompute).  The summation order is the warp32
+// order of DESIGN.md §2.
+//
+// Packed reaction word (see ensure_k2 in runtime.cu):
 //   bits [0,2) n_reac; term q: species [2+16q, 16+16q), coef [16+16q, 18+16q);
 //   bits [50,64) modifier species (0x3FFF = none).
+struct k2_rx {
+    ssa_u64 pk;
+    double rate;
+    double modc;
+};
+
+// C(x, m) for m in {1, 2}; m == 3 is rare and branches.
 static __device__ __forceinline__ double k2_factor(double x, int m)
 {
-    if (m == 1) return x;
     const double x1 = __dmul_rn(x, __dadd_rn(x, -1.0));
-    if (m == 2) return __dmul_rn(x1, 0.5);
-    return __ddiv_rn(__dmul_rn(x1, __dadd_rn(x, -2.0)), 6.0);
+    double f = (m == 1) ? x : __dmul_rn(x1, 0.5);
+    if (m == 3) f = __ddiv_rn(__dmul_rn(x1, __dadd_rn(x, -2.0)), 6.0);
+    return f;
 }
 
-static __device__ __forceinline__ double k2_propensity(ssa_u64 pk, double rate, const double* __restrict__ x,
-                                                       const double* __restrict__ modc, int j)
+static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const double* __restrict__ x)
 {
+    const ssa_u64 pk = q.pk;
     const int n = (int)(pk & 3ull);
     double h = 1.0;
     if (n >= 1) h = k2_factor(x[(int)((pk >> 2) & 0x3FFF)], (int)((pk >> 16) & 3));
     if (n >= 2) h = __dmul_rn(h, k2_factor(x[(int)((pk >> 18) & 0x3FFF)], (int)((pk >> 32) & 3)));
     if (n >= 3) h = __dmul_rn(h, k2_factor(x[(int)((pk >> 34) & 0x3FFF)], (int)((pk >> 48) & 3)));
-    double k = rate;
+    double k = q.rate;
     const int ms = (int)(pk >> 50);
     if (ms != 0x3FFF) {
-        k = __dadd_rn(k, __dmul_rn(modc[j], x[ms]));
+        k = __dadd_rn(k, __dmul_rn(q.modc, x[ms]));
         k = (k < 0.0) ? 0.0 : k;
     }
     return (n == 0) ? k : __dmul_rn(k, h);
 }
 
-template <int PMAX>
-__global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
+size_t ssa_k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
 {
-    extern __shared__ double k2_smem[];
+    const size_t warps = (size_t)(block / 32);
+    return sizeof(k2_rx) * (size_t)R + sizeof(double) * (size_t)S                    // tables, x0
+           + warps * sizeof(double) * ((size_t)S + 32 * (size_t)P)                    // x, a per warp
+           + sizeof(int) * ((size_t)R + 1 + n_ent + (size_t)S + 1 + n_dep);           // nu, dep CSR
+}
+
+template <int PMAX>
+__global__ void __launch_bounds__(SSA_K2_BLOCK, 4) ssa_k2(const ssa_k2_params P)
+{
+    extern __shared__ __align__(16) unsigned char k2_smem_raw[];
     const int S = P.S, R = P.R, Pl = P.P;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
-    // shared layout: x[nwarps][S] | modc[R] | x0[S] | nu_off[R+1] (int) | nu_ent[n_ent] (int)
-    double* xs = k2_smem;
-    double* modc = xs + (size_t)nwarps * S;
-    double* x0 = modc + R;
-    int* nu_off = (int*)(x0 + S);
+    const unsigned FULL = 0xffffffffu;
+    // shared layout: rx[R] | x0[S] | (x[S] | a[32 P]) per warp | nu_off[R+1] | nu_ent | dep_off[S+1] | dep_ent
+    k2_rx* rx = (k2_rx*)k2_smem_raw;
+    double* x0 = (double*)(rx + R);
+    double* wbase = x0 + S;
+    double* x = wbase + (size_t)warp * (S + 32 * Pl);
+    double* a = x + S;                                   // a[q*32 + l] = propensity of j = l*P + q
+    int* nu_off = (int*)(wbase + (size_t)nwarps * (S + 32 * Pl));
     int* nu_ent = nu_off + (R + 1);
-    for (int i = threadIdx.x; i < R; i += blockDim.x) modc[i] = P.modc[i];
+    int* dep_off = nu_ent + P.n_ent;
+    int* dep_ent = dep_off + (S + 1);
+    for (int i = threadIdx.x; i < R; i += blockDim.x) {
+        k2_rx q;
+        q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i];
+        rx[i] = q;
+    }
     for (int i = threadIdx.x; i < S; i += blockDim.x) x0[i] = P.x0[i];
     for (int i = threadIdx.x; i <= R; i += blockDim.x) nu_off[i] = P.nu_off[i];
     for (int i = threadIdx.x; i < P.n_ent; i += blockDim.x) nu_ent[i] = P.nu_ent[i];
+    for (int i = threadIdx.x; i <= S; i += blockDim.x) dep_off[i] = P.dep_off[i];
+    for (int i = threadIdx.x; i < P.n_dep; i += blockDim.x) dep_ent[i] = P.dep_ent[i];
     __syncthreads();
 
-    // this lane's contiguous block of reactions j = lane*P + q
-    ssa_u64 pk[PMAX];
-    double rt[PMAX];
-#pragma unroll
-    for (int q = 0; q < PMAX; ++q) {
-        const int j = lane * Pl + q;
-        const bool own = (q < Pl) && (j < R);
-        pk[q] = own ? P.pk[j] : (0x3FFFull << 50);   // no reactants, no modifier
-        rt[q] = own ? P.rate[j] : 0.0;                // rate 0 -> a = 0
-    }
-    double* x = xs + (size_t)warp * S;
     const double INF = __longlong_as_double(0x7FF0000000000000ll);
     const double dt = P.dt;
     const long long K = P.K;
     const ssa_u64 G = (ssa_u64)K + 1;
-    const unsigned FULL = 0xffffffffu;
     ssa_u64 my_events = 0, my_ties = 0;
 
     for (;;) {
@@ -94,6 +115,15 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
         const ssa_u64 id = P.id_begin + rel;
         const long long slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
         for (int s = lane; s < S; s += 32) x[s] = x0[s];
+        __syncwarp();
+        // a3 at the initial state: every propensity of this lane's block
+#pragma unroll
+        for (int q = 0; q < PMAX; ++q) {
+            if (q < Pl) {
+                const int j = lane * Pl + q;
+                a[q * 32 + lane] = (j < R) ? k2_propensity(rx[j], x) : 0.0;
+            }
+        }
         __syncwarp();
 
         double t = 0.0, s_next = 0.0;
@@ -112,17 +142,11 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
                 Ec = -ssa_plog(ssa_u53(o.o1, o.o0), k2_plog);
                 U2c = ssa_u53(o.o3, o.o2);
             }
-            // a3: this lane's propensities; a4: lane sum then warp scan
-            double a[PMAX];
+            // a4: lane sum (sequential over the lane's block), then warp scan
             double L = 0.0;
 #pragma unroll
-            for (int q = 0; q < PMAX; ++q) {
-                a[q] = 0.0;
-                if (q < Pl) {
-                    a[q] = k2_propensity(pk[q], rt[q], x, modc, lane * Pl + q);
-                    L = __dadd_rn(L, a[q]);
-                }
-            }
+            for (int q = 0; q < PMAX; ++q)
+                if (q < Pl) L = __dadd_rn(L, a[q * 32 + lane]);
             double v = L;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -142,11 +166,10 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
                 absorbed = 1;
             } else {
                 status = 1;
-                // first reaction with a non-finite propensity
-                int bad = R;
+                int bad = R;   // first reaction with a non-finite propensity
 #pragma unroll
                 for (int q = PMAX - 1; q >= 0; --q)
-                    if (q < Pl && !(fabs(a[q]) < INF) && lane * Pl + q < R) bad = lane * Pl + q;
+                    if (q < Pl && lane * Pl + q < R && !(fabs(a[q * 32 + lane]) < INF)) bad = lane * Pl + q;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
                 err_r = bad < R ? bad : -1;
@@ -184,36 +207,50 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
             int j = -1;
             if (lane == ls) {
                 double p = (lane > 0) ? vprev : 0.0;
-#pragma unroll
-                for (int q = 0; q < PMAX; ++q) {
-                    if (q < Pl && j < 0) {
-                        p = __dadd_rn(p, a[q]);
-                        if (p > r) j = lane * Pl + q;
-                    }
+                for (int q = 0; q < Pl; ++q) {
+                    p = __dadd_rn(p, a[q * 32 + lane]);
+                    if (p > r) { j = lane * Pl + q; break; }
                 }
-                if (j < 0) {
-#pragma unroll
-                    for (int q = 0; q < PMAX; ++q)
-                        if (q < Pl && a[q] > 0.0) j = lane * Pl + q;
-                }
+                if (j < 0)
+                    for (int q = Pl - 1; q >= 0; --q)
+                        if (a[q * 32 + lane] > 0.0) { j = lane * Pl + q; break; }
             }
             j = __shfl_sync(FULL, j, ls);
             if (j < 0) {
                 // rounding fallback: last positive propensity in an earlier lane
                 int lp = -1;
-#pragma unroll
-                for (int q = 0; q < PMAX; ++q)
-                    if (q < Pl && a[q] > 0.0) lp = lane * Pl + q;
+                for (int q = 0; q < Pl; ++q)
+                    if (a[q * 32 + lane] > 0.0) lp = lane * Pl + q;
                 const unsigned m2 = __ballot_sync(FULL, lp >= 0 && lane < ls);
                 j = __shfl_sync(FULL, lp, 31 - __clz(m2));
             }
-            // a8
+            // a8: state update
             const int nb = nu_off[j], ne = nu_off[j + 1];
             for (int q = nb + lane; q < ne; q += 32) {
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
-                const int d = ent >> 16;          // arithmetic shift: signed delta
-                x[sp] = __dadd_rn(x[sp], (double)d);
+                x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));   // arithmetic shift: signed delta
+            }
+            __syncwarp();
+            // a3 for the reactions that read a changed species (lane t takes
+            // the t-th entry of the concatenated dependency lists)
+            int T = 0;
+            for (int q = nb; q < ne; ++q) {
+                const int sp = nu_ent[q] & 0xFFFF;
+                T += dep_off[sp + 1] - dep_off[sp];
+            }
+            for (int base = 0; base < T; base += 32) {
+                int rem = base + lane, jj = -1;
+                for (int q = nb; q < ne; ++q) {
+                    const int sp = nu_ent[q] & 0xFFFF;
+                    const int o = dep_off[sp], len = dep_off[sp + 1] - o;
+                    if (rem >= 0 && rem < len) jj = dep_ent[o + rem];
+                    rem -= len;
+                }
+                if (jj >= 0) {
+                    const int l = jj / Pl, q = jj - l * Pl;
+                    a[q * 32 + l] = k2_propensity(rx[jj], x);
+                }
             }
             __syncwarp();
             t = tn;
@@ -246,23 +283,23 @@ __global__ void __launch_bounds__(SSA_K2_BLOCK) ssa_k2(const ssa_k2_params P)
     }
 }
 
-size_t ssa_k2_smem_bytes(int S, int R, int n_ent, int block)
+static const void* k2_fn(int pmax)
 {
-    return sizeof(double) * ((size_t)(block / 32) * S + R + S) + sizeof(int) * ((size_t)R + 1 + n_ent);
+    switch (pmax) {
+    case 1: return (const void*)ssa_k2<1>;
+    case 2: return (const void*)ssa_k2<2>;
+    case 4: return (const void*)ssa_k2<4>;
+    case 8: return (const void*)ssa_k2<8>;
+    case 16: return (const void*)ssa_k2<16>;
+    default: return nullptr;
+    }
 }
 
 cudaError_t ssa_k2_launch(const ssa_k2_params& p, int grid, int block, cudaStream_t st)
 {
-    const size_t smem = ssa_k2_smem_bytes(p.S, p.R, p.n_ent, block);
-    const void* fn = nullptr;
-    switch (p.PMAX) {
-    case 1: fn = (const void*)ssa_k2<1>; break;
-    case 2: fn = (const void*)ssa_k2<2>; break;
-    case 4: fn = (const void*)ssa_k2<4>; break;
-    case 8: fn = (const void*)ssa_k2<8>; break;
-    case 16: fn = (const void*)ssa_k2<16>; break;
-    default: return cudaErrorInvalidValue;
-    }
+    const size_t smem = ssa_k2_smem_bytes(p.S, p.R, p.P, p.n_ent, p.n_dep, block);
+    const void* fn = k2_fn(p.PMAX);
+    if (!fn) return cudaErrorInvalidValue;
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
     void* args[] = {(void*)&p};
@@ -272,15 +309,8 @@ cudaError_t ssa_k2_launch(const ssa_k2_params& p, int grid, int block, cudaStrea
 int ssa_k2_max_blocks_per_sm(int pmax, int block, size_t smem)
 {
     int n = 0;
-    const void* fn = nullptr;
-    switch (pmax) {
-    case 1: fn = (const void*)ssa_k2<1>; break;
-    case 2: fn = (const void*)ssa_k2<2>; break;
-    case 4: fn = (const void*)ssa_k2<4>; break;
-    case 8: fn = (const void*)ssa_k2<8>; break;
-    case 16: fn = (const void*)ssa_k2<16>; break;
-    default: return 0;
-    }
+    const void* fn = k2_fn(pmax);
+    if (!fn) return 0;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem) != cudaSuccess) return 0;
     return n;

@@ -83,6 +83,8 @@ struct K2Dev {
     ssa_u64* pk = nullptr;
     double *rate = nullptr, *modc = nullptr, *x0 = nullptr;
     int *nu_off = nullptr, *nu_ent = nullptr;
+    int *dep_off = nullptr, *dep_ent = nullptr;
+    int n_dep = 0;
 };
 
 struct DevCache {
@@ -418,12 +420,30 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, K2Dev** out)
         nu_off[j + 1] = (int)nu_ent.size();
     }
     for (int s = 0; s < S; ++s) x0[s] = (double)m.x0[s];
+    const int n_ent_real = (int)nu_ent.size();
     if (nu_ent.empty()) nu_ent.push_back(0);
-    // image layout (8-byte aligned sections): pk | rate | modc | x0 | nu_off | nu_ent
+    // dependency graph: species -> reactions whose propensity reads it (as a
+    // reactant or as the modifier species), ascending reaction index
+    std::vector<std::vector<int>> deps(S);
+    for (int j = 0; j < R; ++j) {
+        const RxI& q = m.rx[j];
+        for (auto& t : q.reac) deps[t.first].push_back(j);
+        if (q.mod_sp >= 0 && (deps[q.mod_sp].empty() || deps[q.mod_sp].back() != j)) deps[q.mod_sp].push_back(j);
+    }
+    std::vector<int> dep_off(S + 1, 0), dep_ent;
+    for (int s = 0; s < S; ++s) {
+        for (int j : deps[s]) dep_ent.push_back(j);
+        dep_off[s + 1] = (int)dep_ent.size();
+    }
+    const int n_dep_real = (int)dep_ent.size();
+    if (dep_ent.empty()) dep_ent.push_back(0);
+    // image layout (8-byte aligned sections): pk | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
     const size_t o_pk = 0, o_rate = o_pk + 8 * R1, o_modc = o_rate + 8 * R1, o_x0 = o_modc + 8 * R1;
     const size_t o_off = o_x0 + 8 * (size_t)S;
     const size_t o_ent = o_off + ((4 * nu_off.size() + 7) & ~(size_t)7);
-    const size_t bytes = o_ent + 4 * nu_ent.size();
+    const size_t o_doff = o_ent + ((4 * nu_ent.size() + 7) & ~(size_t)7);
+    const size_t o_dent = o_doff + ((4 * dep_off.size() + 7) & ~(size_t)7);
+    const size_t bytes = o_dent + 4 * dep_ent.size();
     CU(cudaMallocHost(&k.host_image, bytes));
     char* h = (char*)k.host_image;
     memcpy(h + o_pk, pk.data(), 8 * R1);
@@ -432,6 +452,8 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, K2Dev** out)
     memcpy(h + o_x0, x0.data(), 8 * (size_t)S);
     memcpy(h + o_off, nu_off.data(), 4 * nu_off.size());
     memcpy(h + o_ent, nu_ent.data(), 4 * nu_ent.size());
+    memcpy(h + o_doff, dep_off.data(), 4 * dep_off.size());
+    memcpy(h + o_dent, dep_ent.data(), 4 * dep_ent.size());
     CU(cudaMalloc(&k.dev_image, bytes));
     CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
     char* d = (char*)k.dev_image;
@@ -441,10 +463,13 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, K2Dev** out)
     k.x0 = (double*)(d + o_x0);
     k.nu_off = (int*)(d + o_off);
     k.nu_ent = (int*)(d + o_ent);
+    k.dep_off = (int*)(d + o_doff);
+    k.dep_ent = (int*)(d + o_dent);
     k.image_bytes = bytes;
     k.P = P;
     k.PMAX = PMAX;
-    k.n_ent = (int)nu_ent.size();
+    k.n_ent = n_ent_real;
+    k.n_dep = n_dep_real;
     k.ready = true;
     *out = &k;
     return SSA_OK;
@@ -598,7 +623,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + block - 1) / block);
         } else {
             TRY(ensure_k2(*m, c.device, &k2));
-            const size_t smem = ssa_k2_smem_bytes(m->S, m->R, k2->n_ent, block);
+            const size_t smem = ssa_k2_smem_bytes(m->S, m->R, k2->P, k2->n_ent, k2->n_dep, block);
             if (smem > 227 * 1024) return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", smem);
             int bps = ssa_k2_max_blocks_per_sm(k2->PMAX, block, smem);
             if (bps <= 0) return fail(SSA_ERR_CUDA, "warp path: kernel cannot be resident (block %d, smem %zu)", block, smem);
@@ -696,6 +721,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             ssa_k2_params p{};
             p.S = m->S; p.R = m->R; p.P = k2->P; p.PMAX = k2->PMAX; p.n_ent = k2->n_ent;
             p.pk = k2->pk; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
+            p.n_dep = k2->n_dep; p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;

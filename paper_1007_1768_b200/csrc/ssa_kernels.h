@@ -28,6 +28,9 @@ struct ssa_k2_params {
     const double* x0;        // [S]
     const int* nu_off;       // [R+1]
     const int* nu_ent;       // [n_ent] (species | delta << 16)
+    int n_dep;
+    const int* dep_off;      // [S+1] species -> reactions whose propensity reads it
+    const int* dep_ent;      // [n_dep] reaction indices
     // run
     ssa_u64 id_begin, n_ids;
     int* staging;
@@ -55,7 +58,7 @@ struct ssa_tree_out {
     ssa_u64 row_stride, elem_stride, offset;
 };
 
-size_t ssa_k2_smem_bytes(int S, int R, int n_ent, int block);
+size_t ssa_k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block);
 cudaError_t ssa_k2_launch(const ssa_k2_params& p, int grid, int block, cudaStream_t st);
 int ssa_k2_max_blocks_per_sm(int pmax, int block, size_t smem);
 
