@@ -207,6 +207,7 @@ def main():
     import inputs
     from paper_1007_1768_b200 import build as B
     B.build()
+    from paper_1007_1768_b200 import dist as D
     from paper_1007_1768_b200 import ssa as S
 
     torch.cuda.set_device(local_rank)
@@ -221,31 +222,20 @@ def main():
     t_end = args.t_end or cfg.t_end
     dt = cfg.dt
     G = S.grid_size(t_end, dt)
-    cells = G * net.S
-    b, e = S.shard_bounds(n_total, world, rank)
     model = S.Model(net)
     path = args.path or cfg.path
     opts = dict(block=args.block, blocks_per_sm=args.blocks_per_sm)
 
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
-    root = torch.zeros((3, cells), dtype=torch.float64, device=dev)
-    roots = torch.zeros((world, 3, cells), dtype=torch.float64, device=dev)
-    out = torch.zeros((4, cells), dtype=torch.float64, device=dev)
+    # rank r owns the aligned id shard r; roots all-gathered over NCCL, merged in rank order
+    ens = D.ShardedEnsemble.for_model(model, n_total, t_end, dt, cfg.seed, dev, path=path, stream=sh, **opts)
+    cells = ens.cells
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    def step(host_outputs=False):
+    def step():
         l2.zero_()                                               # flush L2 between steps
-        res = S.run_shard(model, b, e, t_end, dt, cfg.seed, root, path=path, stream=sh, **opts) if e > b else None
-        if world > 1:
-            dist.all_gather_into_tensor(roots.view(-1), root.view(-1))
-        else:
-            roots[0].copy_(root)
-        if host_outputs:
-            merged = S.merge_roots(roots, world, cells, stream=sh)
-            return res, merged
-        S.merge_roots(roots, world, cells, stream=sh, out=out)
-        return res, None
+        return ens.step()
 
     # JIT + warm-up (untimed)
     jit0 = time.perf_counter()
@@ -267,7 +257,7 @@ def main():
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            res, _ = step()
+            res = step()
             if res is not None:
                 events += res.events
                 ssa_ms.append(res.ssa_ms)
@@ -278,14 +268,8 @@ def main():
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms, float(events), float(launches)], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        ms = float(tmax[0])
-        events = int(t[1])
-        launches = int(t[2])
+    ms, events, launches = D.max_and_sum([ms, events, launches], dev)   # max-over-ranks time, summed counters
+    events, launches = int(events), int(launches)
     value = events / (ms / 1e3)
     traj_per_s = n_total * args.steps / (ms / 1e3)
 
@@ -305,18 +289,14 @@ def main():
                 e2e_events += r.events
                 h2d, d2h = r.h2d_bytes, r.d2h_bytes
             else:
-                res, merged = step(host_outputs=True)
+                res = step()
                 e2e_events += res.events if res else 0
+                merged = ens.out.cpu()                 # D2H of this step's mean/var/M2/n grids
                 h2d = res.h2d_bytes if res else 0
-                d2h = 4 * cells * 8
+                d2h = merged.numel() * merged.element_size()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        w = torch.tensor([wall, float(e2e_events)], dtype=torch.float64, device=dev)
-        if world > 1:
-            wmax = w.clone()
-            dist.all_reduce(wmax, op=dist.ReduceOp.MAX)
-            dist.all_reduce(w, op=dist.ReduceOp.SUM)
-            wall, e2e_events = float(wmax[0]), int(w[1])
+        wall, e2e_events = D.max_and_sum([wall, e2e_events], dev)
         e2e = {"value": e2e_events / wall, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                "note": "ssa_run with host result buffers; wall clock incl. per-run model upload and D2H"}

@@ -296,8 +296,13 @@ def merge_roots(d_roots, n_roots: int, cells: int, *, device: int = -1, stream=N
 
 def shard_bounds(n_total: int, world: int, rank: int):
     """Aligned-subtree shards of the canonical reduction tree (R26):
-    span = next_pow2(n_total) / world (world a power of two)."""
-    assert world >= 1 and (world & (world - 1)) == 0, "world size must be a power of two"
+    span = next_pow2(n_total) / world (world a power of two).  Shards are
+    contiguous, in rank order, cover [0, n_total) exactly once, and each is a
+    whole subtree of the canonical perfect binary tree over ids."""
+    if world < 1 or (world & (world - 1)) != 0:
+        raise ValueError("world size must be a power of two (shards are subtrees of a binary tree)")
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
     p = 1
     while p < n_total:
         p <<= 1
