@@ -253,6 +253,7 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     events = 0
     ssa_ms = []
+    red_ms, red_bytes = [], 0
     launches = 0
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
@@ -261,6 +262,8 @@ def main():
             if res is not None:
                 events += res.events
                 ssa_ms.append(res.ssa_ms)
+                red_ms.append(res.reduce_ms)
+                red_bytes = res.reduce_bytes
                 launches += res.kernel_launches
             launches += 2      # merge + finalize of ssa_merge_roots
         ev1.record(stream)
@@ -321,6 +324,15 @@ def main():
                 "alg_thread_instr_per_event": I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
 
+    # secondary: the chunk reduction (K3) reads the staged grid samples once -- HBM bound
+    hbm_peak = float(peaks.get("hbm_gbs", 7700.0))
+    r_ms = statistics.mean(red_ms) if red_ms else float("nan")
+    r_gbs = red_bytes / (r_ms / 1e3) / 1e9 if red_ms and r_ms > 0 else None
+    roofline_reduce = {"bound": "hbm", "achieved": r_gbs, "peak": hbm_peak, "unit": "GB/s",
+                       "frac": (r_gbs / hbm_peak) if r_gbs else None, "traffic": None, "kernel": "ssa_tree_leaf",
+                       "bytes_per_launch": red_bytes, "kernel_ms": r_ms,
+                       "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200 nominal"}
+
     clocks = clk.summary()
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -342,6 +354,7 @@ def main():
         "trajectories_per_s": traj_per_s,
         "events_per_step": events / args.steps,
         "roofline": roofline,
+        "roofline_reduce": roofline_reduce,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -156,6 +156,8 @@ typedef struct {
     uint64_t d2h_bytes;        /* device->host bytes copied by this call (results, dump, counters) */
     int32_t kernel_launches;   /* kernels this call launched (SSA + reduction + finalize) */
     int32_t pad2;
+    double reduce_ms;          /* device time of the chunk reductions (K3 + tile merges, CUDA events) */
+    uint64_t reduce_bytes;     /* staged sample bytes those reductions read (4 per trajectory x grid cell) */
 } ssa_result;
 
 /* StochRxn_ff on one GPU: simulate trajectories 0..n_trajectories-1 on

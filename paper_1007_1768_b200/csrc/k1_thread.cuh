@@ -1,25 +1,30 @@
 // k1_thread.cuh -- K1: one trajectory per thread, model-specialised (sm_100a).
 //
 // This text is compiled by NVRTC at run time, after ssa_device.cuh and a
-// generated model section that defines (see jit.cpp):
+// generated model section (runtime.cu: gen_k1_model) that defines
 //   SSA_S, SSA_R, SSA_K1_BLOCK, SSA_K1_MINB
-//   __constant__ double c_rate[], c_modc[], c_x0[]
+//   __constant__ double c_k[] (distinct rate / modifier constants), c_x0[]
 //   ssa_prefix(x, c)      a3 + a4: c_j = c_{j-1} + a_j, sequential order (R13)
-//   ssa_apply(j, x)       a8: x += nu_j (switch over the reaction index)
+//   ssa_apply(j, x)       a8: x += nu_j (one indirect branch through a table)
 //   ssa_first_bad(x)      first reaction with a non-finite propensity
 // so that species counts (fp64, exact integers) and the propensity prefix
-// live in registers, with rates in constant memory (a sweep over rates does
-// not recompile).  The event loop is SURVEY.md §8(a) a1-a8; the definitions
-// are those of DESIGN.md §2 and PAPER.md:60 ("a single transition amongst
-// the possible ones is selected, and the state updated accordingly").
+// live in registers, with the model's constants in constant memory.  The
+// event loop is SURVEY.md §8(a) a1-a8; the definitions are those of
+// DESIGN.md §2 and PAPER.md:60 ("a single transition amongst the possible
+// ones is selected, and the state updated accordingly").
 //
 // Scheduling (north_star (c)): persistent threads; a lane that finishes a
 // trajectory takes the next id from an atomic counter, so lanes are refilled
 // as trajectories end.  Output is keyed by id, so results do not depend on
 // the schedule.
+//
+// Control flow: one loop iteration = one candidate event.  The common case
+// (a0 in the fast-division range, no grid point crossed) runs straight
+// through to the update with a single, rarely taken branch; everything else
+// -- a grid crossing (a6), absorbing state, non-finite propensity, end of the
+// trajectory and the refill (a1) -- lives on that rare path.
 
 // ssa_k1_params is defined in ssa_device.cuh (shared with the host runtime).
-
 
 extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(const ssa_k1_params P)
 {
@@ -29,40 +34,33 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     const ssa_u64 G = (ssa_u64)K + 1;
     ssa_u64 my_events = 0, my_ties = 0;
 
-    // Per-lane trajectory state.  ONE loop iteration = one candidate event of
-    // the lane's current trajectory; a lane whose trajectory ended refills at
-    // the top of the same loop.  (A nested trajectory/event loop would let
-    // lanes that refilled drift into separate divergent groups that never
-    // reconverge -- here every iteration reconverges at the loop head.)
     double x[SSA_S];
     double t = 0.0, s_next = 0.0;
     ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0;
     long long k = 0, slot = -1;
     int status = 0, absorbed = 0, err_r = -1;
-    bool need = true, have = true;
 
-    for (;;) {
-        if (need) {
-            // a1: take the next trajectory id and initialise it.  This block
-            // has a single exit (no break) so the lanes that refill reconverge
-            // with the others right after it.
-            rel = atomicAdd(P.work, 1ull);
-            have = rel < P.n_ids;
-            id = P.id_begin + rel;
-            slot = (have && P.n_dump) ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
+    // a1: take the next trajectory id (atomic counter) and initialise it
+    auto start = [&]() -> bool {
+        rel = atomicAdd(P.work, 1ull);
+        if (rel >= P.n_ids) return false;
+        id = P.id_begin + rel;
+        slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
 #pragma unroll
-            for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
-            t = 0.0; s_next = 0.0; e = 0; k = 0; hash = SSA_FNV_OFFSET; ties = 0;
-            status = 0; absorbed = 0; err_r = -1;
-            need = false;
-        }
-        if (!have) break;   // no work left: this lane is done for good
+        for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
+        t = 0.0; s_next = 0.0; e = 0; k = 0; hash = SSA_FNV_OFFSET; ties = 0;
+        status = 0; absorbed = 0; err_r = -1;
+        return true;
+    };
+
+    bool live = start();
+    while (live) {
         // a2: one Philox block per candidate event, counter (e, id)
         const ssa_philox_out o = ssa_philox4x32_10_ks((ssa_u32)e, (ssa_u32)(e >> 32), (ssa_u32)id,
                                                       (ssa_u32)(id >> 32), P.ks);
         // a3 + a4 (the propensity prefix chain) and a5's logarithm are
-        // independent dependency chains: both are issued in one basic block
-        // so the scheduler interleaves them.
+        // independent dependency chains in one basic block, so the scheduler
+        // interleaves them.
         double c[SSA_R > 0 ? SSA_R : 1];
         const double a0 = ssa_prefix(x, c);
         // keep the prefix in registers: without this barrier the compiler
@@ -80,75 +78,81 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
                 : "+r"(jp[q & 3]) : "d"(c[q]), "d"(r));
         const int j = (jp[0] + jp[1]) + (jp[2] + jp[3]);
-        // a5: tau = E / a0 (fast in-range division; the rare cases branch)
-        bool fin = false;
-        double tn;
+        // a5: tau = E / a0 by the fast in-range IEEE division (speculative:
+        // replaced on the rare path when a0 is outside [2^-900, 2^901))
         const unsigned a0hi = (unsigned)__double2hiint(a0);
-        if (a0hi - (123u << 20) < ((1923u - 123u) << 20)) {   // a0 in [2^-900, 2^901)
-            tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
-        } else if (a0 > 0.0 && a0 < INF) {
-            tn = __dadd_rn(t, __ddiv_rn(E, a0));
-        } else if (a0 == 0.0) {
-            tn = INF;
-            absorbed = 1;
-        } else {
-            tn = INF;
-            status = 1;
-            err_r = ssa_first_bad(x);
-            fin = true;
-        }
-        // a6: grid alignment (selective memory on the grid)
-        if (!fin && tn > s_next) {
-            do {
-                const double tol = __dmul_rn(1e-9, s_next);
-                const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
-                                  (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
-                ties += near ? 1 : 0;
-                int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
-#pragma unroll
-                for (int s = 0; s < SSA_S; ++s) {
-                    if (x[s] > 2147483647.0) status = 2;
-                    dst[(ssa_u64)s * P.stride] = (int)x[s];
+        const bool fast = a0hi - (123u << 20) < ((1923u - 123u) << 20);
+        double tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
+        if (!fast || tn > s_next) {
+            // ---------------- rare path: a5 edge cases, a6, end + refill
+            bool fin = false;
+            if (!fast) {
+                if (a0 > 0.0 && a0 < INF) {
+                    tn = __dadd_rn(t, __ddiv_rn(E, a0));
+                } else if (a0 == 0.0) {
+                    tn = INF;            // absorbing: hold x to the end of the grid
+                    absorbed = 1;
+                } else {
+                    tn = INF;            // non-finite propensity: error (id, reaction)
+                    status = 1;
+                    err_r = ssa_first_bad(x);
+                    fin = true;
                 }
+            }
+            // a6: grid alignment (selective memory on the grid): x is the
+            // state just before the first event past s_k
+            if (!fin && tn > s_next) {
+                do {
+                    const double tol = __dmul_rn(1e-9, s_next);
+                    const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
+                                      (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
+                    ties += near ? 1 : 0;
+                    int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
+#pragma unroll
+                    for (int s = 0; s < SSA_S; ++s) {
+                        if (x[s] > 2147483647.0) status = 2;
+                        dst[(ssa_u64)s * P.stride] = (int)x[s];
+                    }
+                    if (slot >= 0) {
+                        const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
+#pragma unroll
+                        for (int s = 0; s < SSA_S; ++s) P.dump_states[base * SSA_S + s] = (int)x[s];
+                        P.dump_e[base] = e;
+                        P.dump_t[base] = (e > 0) ? t : 0.0;
+                    }
+                    ++k;
+                    s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+                } while (tn > s_next);
+                fin = (k > K);
+            }
+            if (fin) {
+                // trajectory done: per-trajectory records, then refill (a1)
+                my_events += e;
+                my_ties += ties;
                 if (slot >= 0) {
-                    const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
-#pragma unroll
-                    for (int s = 0; s < SSA_S; ++s) P.dump_states[base * SSA_S + s] = (int)x[s];
-                    P.dump_e[base] = e;
-                    P.dump_t[base] = (e > 0) ? t : 0.0;
+                    ssa_dev_summary sm;
+                    sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
+                    sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
+                    sm.err_reaction = err_r; sm.pad = 0;
+                    P.dump_sum[slot] = sm;
                 }
-                ++k;
-                s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
-            } while (tn > s_next);
-            fin = (k > K);
-        }
-        if (!fin) {
-            // a8
-            ssa_apply(j, x);
-            t = tn;
-            ++e;
-            hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
-        } else {
-            // trajectory done: per-trajectory records, then refill
-            my_events += e;
-            my_ties += ties;
-            if (slot >= 0) {
-                ssa_dev_summary sm;
-                sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
-                sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
-                sm.err_reaction = err_r; sm.pad = 0;
-                P.dump_sum[slot] = sm;
+                if (status) {
+                    const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
+                    atomicAdd(&P.stats->n_errors, 1ull);
+                    atomicOr(&P.stats->err_code, code);
+                    // smallest id wins; pack (id, code, reaction) so one atomicMin keeps them together
+                    const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
+                    atomicMin(&P.stats->first_err_id, packed);
+                }
+                live = start();
+                continue;
             }
-            if (status) {
-                const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
-                atomicAdd(&P.stats->n_errors, 1ull);
-                atomicOr(&P.stats->err_code, code);
-                // smallest id wins; pack (id, code, reaction) so one atomicMin keeps them together
-                const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
-                atomicMin(&P.stats->first_err_id, packed);
-            }
-            need = true;
         }
+        // a8: apply the selected reaction
+        ssa_apply(j, x);
+        t = tn;
+        ++e;
+        hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
     }
     // warp-level reduction of the counters, then one atomic per warp
 #pragma unroll

@@ -364,13 +364,105 @@ static __device__ __forceinline__ ssa_welford fold8(ssa_welford v[8])
     return ssa_welford_merge(v[0], v[4]);
 }
 
-// leaves: staging row r = blockIdx.y (+ 65535 * blockIdx.z), ids [0, count)
-__global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __restrict__ staging, ssa_u64 stride,
-                                                                ssa_u64 count, ssa_u64 rows, ssa_tree_out out)
+// Full tiles (no empty leaf): every merge joins two full subtrees of equal
+// size h (a power of two), where the divisions of the Chan merge are exact --
+// n_B / n = 1/2 and (n_A n_B) / n = h/2 -- so the merge reduces to
+//   d = m_B - m_A;  m = m_A + d * 0.5;  M2 = (M2_A + M2_B) + (d * d) * (h/2)
+// with bitwise the same result as ssa_welford_merge (R26), and no division.
+// This keeps K3 at HBM speed instead of FP64-division bound.
+static __device__ __forceinline__ void wf_merge_full(double& mA, double& m2A, double mB, double m2B, double half_h)
+{
+    const double d = __dadd_rn(mB, -mA);
+    mA = __dadd_rn(mA, __dmul_rn(d, 0.5));
+    m2A = __dadd_rn(__dadd_rn(m2A, m2B), __dmul_rn(__dmul_rn(d, d), half_h));
+}
+
+static __device__ __forceinline__ void tree_block_full(const int4 q0, const int4 q1, double& mean, double& m2)
+{
+    __shared__ double shm[SSA_TREE_BLOCK / 32], shq[SSA_TREE_BLOCK / 32];
+    // 8 adjacent leaves per thread: levels h = 1, 2, 4
+    double m[8] = {(double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w,
+                   (double)q1.x, (double)q1.y, (double)q1.z, (double)q1.w};
+    double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    wf_merge_full(m[0], v[0], m[1], v[1], 0.5);
+    wf_merge_full(m[2], v[2], m[3], v[3], 0.5);
+    wf_merge_full(m[4], v[4], m[5], v[5], 0.5);
+    wf_merge_full(m[6], v[6], m[7], v[7], 0.5);
+    wf_merge_full(m[0], v[0], m[2], v[2], 1.0);
+    wf_merge_full(m[4], v[4], m[6], v[6], 1.0);
+    wf_merge_full(m[0], v[0], m[4], v[4], 2.0);
+    double mm = m[0], vv = v[0];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // warp levels: subtrees of 8*o leaves, h/2 = 4*o
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double mb = __shfl_down_sync(0xffffffffu, mm, o);
+        const double vb = __shfl_down_sync(0xffffffffu, vv, o);
+        if ((lane & (2 * o - 1)) == 0) wf_merge_full(mm, vv, mb, vb, 4.0 * o);
+    }
+    if (lane == 0) { shm[warp] = mm; shq[warp] = vv; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a[SSA_TREE_BLOCK / 32], b[SSA_TREE_BLOCK / 32];
+#pragma unroll
+        for (int i = 0; i < SSA_TREE_BLOCK / 32; ++i) { a[i] = shm[i]; b[i] = shq[i]; }
+        // block levels: subtrees of 256*o leaves, h/2 = 128*o
+#pragma unroll
+        for (int o = 1; o < SSA_TREE_BLOCK / 32; o <<= 1)
+#pragma unroll
+            for (int i = 0; i + o < SSA_TREE_BLOCK / 32; i += 2 * o) wf_merge_full(a[i], b[i], a[i + o], b[i + o], 128.0 * o);
+        mean = a[0];
+        m2 = b[0];
+    }
+}
+
+// Full tiles only (launched over the first count / SPAN tiles of each row):
+// every thread issues the loads of its 8 leaves in TWO adjacent tiles before
+// reducing either, so each thread keeps 64 B in flight (the kernel is HBM
+// bound); no general-path code, so it stays small in registers.
+__global__ void __launch_bounds__(SSA_TREE_BLOCK, 4) ssa_tree_leaf_full(const int* __restrict__ staging,
+                                                                       ssa_u64 stride, ssa_u64 n_full,
+                                                                       ssa_u64 rows, ssa_tree_out out)
 {
     const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
     if (row >= rows) return;
-    const ssa_u64 base = (ssa_u64)blockIdx.x * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
+    const ssa_u64 t0 = 2ull * blockIdx.x;                 // first tile of this block
+    const int* src = staging + row * stride + (ssa_u64)threadIdx.x * 8;
+    const bool two = t0 + 1 < n_full;
+    const int4 a0 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN));
+    const int4 a1 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN + 4));
+    int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
+    if (two) {
+        b0 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN));
+        b1 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN + 4));
+    }
+    double mean = 0.0, m2 = 0.0;
+    tree_block_full(a0, a1, mean, m2);
+    if (threadIdx.x == 0) {
+        const ssa_u64 o = row * out.row_stride + t0 * out.elem_stride + out.offset;
+        out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
+    }
+    if (two) {
+        __syncthreads();                                   // shared scratch of tree_block_full reused
+        tree_block_full(b0, b1, mean, m2);
+        if (threadIdx.x == 0) {
+            const ssa_u64 o = row * out.row_stride + (t0 + 1) * out.elem_stride + out.offset;
+            out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
+        }
+    }
+}
+
+// leaves: staging row r = blockIdx.y (+ 65535 * blockIdx.z), ids [0, count);
+// blocks start at tile `first` (the tiles before it are full and reduced by
+// ssa_tree_leaf_full)
+__global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __restrict__ staging, ssa_u64 stride,
+                                                                ssa_u64 count, ssa_u64 rows, ssa_u64 first,
+                                                                ssa_tree_out out)
+{
+    const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    if (row >= rows) return;
+    const ssa_u64 tile = first + blockIdx.x;
+    const ssa_u64 base = tile * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
     const int* src = staging + row * stride;
     ssa_welford v[8];
     if (base + 8 <= count && (stride % 4) == 0) {
@@ -387,7 +479,7 @@ __global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __res
     }
     ssa_welford w = tree_block(fold8(v));
     if (threadIdx.x == 0) {
-        const ssa_u64 o = row * out.row_stride + (ssa_u64)blockIdx.x * out.elem_stride + out.offset;
+        const ssa_u64 o = row * out.row_stride + tile * out.elem_stride + out.offset;
         out.n[o] = w.n; out.mean[o] = w.mean; out.m2[o] = w.m2;
     }
 }
@@ -438,10 +530,23 @@ static dim3 tree_grid(ssa_u64 blocks_x, ssa_u64 rows)
 }
 
 cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 count, ssa_u64 rows,
-                                 const ssa_tree_out& out, cudaStream_t st)
+                                 const ssa_tree_out& out, cudaStream_t st, int* launches)
 {
     const ssa_u64 bx = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
-    ssa_tree_leaf<<<tree_grid(bx ? bx : 1, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, count, rows, out);
+    // full tiles through the division-free kernel (needs 16-byte aligned rows)
+    const ssa_u64 n_full = (stride % 4 == 0) ? count / SSA_TREE_SPAN : 0;
+    if (n_full) {
+        ssa_tree_leaf_full<<<tree_grid((n_full + 1) / 2, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, n_full,
+                                                                                          rows, out);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    if (bx > n_full || bx == 0) {
+        ++*launches;
+        ssa_tree_leaf<<<tree_grid(bx ? bx - n_full : 1, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, count, rows,
+                                                                                       n_full, out);
+    }
     return cudaGetLastError();
 }
 

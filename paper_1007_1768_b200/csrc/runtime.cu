@@ -70,7 +70,7 @@ struct K1Entry {
     cudaKernel_t fn = nullptr;
     int block = 0, minb = 0;
     int blocks_per_sm = 0;
-    void *c_rate = nullptr, *c_modc = nullptr, *c_x0 = nullptr;  // module constant memory
+    void *c_k = nullptr, *c_x0 = nullptr;  // module constant memory
     std::string log;
 };
 
@@ -98,25 +98,25 @@ struct ssa_model {
     std::vector<RxI> rx;
     mutable std::mutex mu;
     mutable std::map<int, DevCache> dev;
-    mutable double* pinned_const = nullptr;  // [rate R'][modc R'][x0 S], page-locked, for per-run uploads
+    mutable double* pinned_const = nullptr;  // [constant pool][x0 S], page-locked, for per-run uploads
 };
 
-// K1 constant-memory image of the model's numbers (rates, modifier
-// coefficients, initial counts), staged once in page-locked host memory and
-// copied to the device at the start of every run (the run's inputs).
-static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* bytes)
+static std::vector<double> const_pool(const ssa_model& m);
+
+// K1 constant-memory image of the model's numbers (the pool of distinct rate
+// and modifier constants, then the initial counts), staged once in
+// page-locked host memory and copied to the device at the start of every run
+// (the run's inputs).  *n_pool receives the pool size.
+static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* bytes, size_t* n_pool)
 {
-    const size_t R1 = (size_t)std::max(m.R, 1);
-    *bytes = sizeof(double) * (2 * R1 + (size_t)m.S);
+    const std::vector<double> pool = const_pool(m);
+    *n_pool = pool.size();
+    *bytes = sizeof(double) * (pool.size() + (size_t)m.S);
     if (!m.pinned_const) {
         CU(cudaMallocHost(&m.pinned_const, *bytes));
         double* p = m.pinned_const;
-        for (size_t j = 0; j < 2 * R1; ++j) p[j] = 0.0;
-        for (int j = 0; j < m.R; ++j) {
-            p[j] = m.rx[j].rate;
-            p[R1 + j] = m.rx[j].mod_coef;
-        }
-        for (int s = 0; s < m.S; ++s) p[2 * R1 + s] = (double)m.x0[s];
+        for (size_t i = 0; i < pool.size(); ++i) p[i] = pool[i];
+        for (int s = 0; s < m.S; ++s) p[pool.size() + s] = (double)m.x0[s];
     }
     *out = m.pinned_const;
     return SSA_OK;
@@ -232,13 +232,49 @@ static std::string factor_expr(int s, int m)
     return o.str();
 }
 
-static std::string prop_stmts(const RxI& q, int j)
+// Pool of the distinct rate / modifier constants of a model (bitwise
+// distinct values, first-appearance order); K1 reads them from the module's
+// __constant__ c_k[] (a uniform load fetches two), so equal constants are
+// loaded once per event.
+static std::vector<double> const_pool(const ssa_model& m)
+{
+    std::vector<double> pool;
+    auto add = [&](double v) {
+        for (double p : pool)
+            if (memcmp(&p, &v, sizeof v) == 0) return;
+        pool.push_back(v);
+    };
+    for (int j = 0; j < m.R; ++j) {
+        add(m.rx[j].rate);
+        if (m.rx[j].mod_sp >= 0) add(m.rx[j].mod_coef);
+    }
+    if (pool.empty()) pool.push_back(0.0);
+    return pool;
+}
+
+static int pool_index(const std::vector<double>& pool, double v)
+{
+    for (size_t i = 0; i < pool.size(); ++i)
+        if (memcmp(&pool[i], &v, sizeof v) == 0) return (int)i;
+    return -1;
+}
+
+// a3 for reaction j: k^ (rate, or the clamped linear modifier of P:93), then
+// a = k^ * h.  The model is immutable, so the sign of each modifier
+// coefficient is known when its kernel is generated: the clamp max(0, .) is
+// emitted only for d < 0 (k >= 0 and d >= 0 give k + d*x >= 0 for counts
+// x >= 0, so there it is a no-op).
+static std::string prop_stmts(const RxI& q, const std::vector<double>& pool)
 {
     std::ostringstream o;
-    if (q.mod_sp >= 0)
-        o << "k = __dadd_rn(c_rate[" << j << "], __dmul_rn(c_modc[" << j << "], x[" << q.mod_sp << "])); k = (k < 0.0) ? 0.0 : k; ";
-    else
-        o << "k = c_rate[" << j << "]; ";
+    const std::string rate = "c_k[" + std::to_string(pool_index(pool, q.rate)) + "]";
+    if (q.mod_sp >= 0) {
+        const std::string modc = "c_k[" + std::to_string(pool_index(pool, q.mod_coef)) + "]";
+        o << "k = __dadd_rn(" << rate << ", __dmul_rn(" << modc << ", x[" << q.mod_sp << "])); ";
+        if (!(q.mod_coef >= 0.0)) o << "k = (k < 0.0) ? 0.0 : k; ";
+    } else {
+        o << "k = " << rate << "; ";
+    }
     if (q.reac.empty()) {
         o << "a = k;";
     } else {
@@ -250,19 +286,41 @@ static std::string prop_stmts(const RxI& q, int j)
     return o.str();
 }
 
+// K1 code-generation variants (tuning; the arithmetic is identical in all of
+// them).  SSA_K1_GEN is read once per process:
+//   upd=brx|switch   a8 as one brx.idx jump table (default) or a C++ switch
+// (Measured and dropped: int64-pattern selection compares on the ALU pipe and
+// species counts in shared memory with a table update were both slower.)
+struct K1Gen {
+    bool flat_switch = true;
+};
+
+static K1Gen k1_gen()
+{
+    static const K1Gen g = [] {
+        K1Gen r;
+        const char* e = getenv("SSA_K1_GEN");
+        const std::string s = e ? e : "";
+        if (s.find("upd=switch") != std::string::npos) r.flat_switch = false;
+        return r;
+    }();
+    return g;
+}
+
 static std::string gen_k1_model(const ssa_model& m, int block, int minb)
 {
     const int S = m.S, R = m.R;
+    const K1Gen g = k1_gen();
     std::ostringstream o;
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
       << "\n#define SSA_K1_MINB " << minb << "\n";
-    o << "__constant__ double c_rate[" << std::max(R, 1) << "];\n__constant__ double c_modc[" << std::max(R, 1)
-      << "];\n__constant__ double c_x0[" << S << "];\n";
+    const std::vector<double> pool = const_pool(m);
+    o << "__constant__ double c_k[" << pool.size() << "];\n__constant__ double c_x0[" << S << "];\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
     o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], double (&c)[SSA_R > 0 ? SSA_R : 1]) {\n";
     o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)c;\n";
     for (int j = 0; j < R; ++j) {
-        o << "  { " << prop_stmts(m.rx[j], j) << " "
+        o << "  { " << prop_stmts(m.rx[j], pool) << " "
           << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
     }
     o << "  return acc;\n}\n";
@@ -273,19 +331,50 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb)
     o << "  const double* x = xs.v;\n";
     o << "  double a, h, k; (void)a; (void)h; (void)k; (void)x;\n";
     for (int j = 0; j < R; ++j)
-        o << "  { " << prop_stmts(m.rx[j], j) << " if (!(fabs(a) < __longlong_as_double(0x7FF0000000000000ll))) return " << j << "; }\n";
+        o << "  { " << prop_stmts(m.rx[j], pool) << " if (!(fabs(a) < __longlong_as_double(0x7FF0000000000000ll))) return " << j << "; }\n";
     o << "  return -1;\n}\n";
     o << "static __device__ __forceinline__ int ssa_first_bad(const double (&x)[SSA_S]) {\n";
     o << "  ssa_state_v xs;\n#pragma unroll\n  for (int s = 0; s < SSA_S; ++s) xs.v[s] = x[s];\n";
     o << "  return ssa_first_bad_v(xs);\n}\n";
-    o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n  switch (j) {\n";
-    for (int j = 0; j < R; ++j) {
-        if (m.rx[j].nu.empty()) continue;
-        o << "  case " << j << ":";
-        for (auto& d : m.rx[j].nu) o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
-        o << " break;\n";
+    bool any_nu = false;
+    for (int j = 0; j < R; ++j) any_nu = any_nu || !m.rx[j].nu.empty();
+    bool exact_imm = true;   // every delta is an exact fp64 immediate (|d| < 2^53)
+    for (int j = 0; j < R; ++j)
+        for (auto& d : m.rx[j].nu) exact_imm = exact_imm && std::llabs(d.second) < (1ll << 53);
+    o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
+    if (g.flat_switch && any_nu && exact_imm && S <= 28 && R <= 4096) {
+        // a8 as ONE indirect branch through a jump table (PTX brx.idx): the
+        // C++ switch compiles to a decision tree of small tables, several
+        // dependent branches deep.  Operands: %0..%(S-1) = x, %S = j.
+        o << "  asm volatile(\"{\\n\\t"
+          << "ssa_apply_tab: .branchtargets ";
+        for (int j = 0; j < R; ++j) o << (j ? ", " : "") << "ssa_apply_" << j;
+        o << ";\\n\\tbrx.idx %" << S << ", ssa_apply_tab;\\n\\t";
+        for (int j = 0; j < R; ++j) {
+            o << "ssa_apply_" << j << ":\\n\\t";
+            for (auto& d : m.rx[j].nu) {
+                double v = (double)d.second;
+                unsigned long long bits;
+                memcpy(&bits, &v, 8);
+                char hx[32];
+                snprintf(hx, sizeof hx, "0d%016llX", bits);
+                o << "add.rn.f64 %" << d.first << ", %" << d.first << ", " << hx << ";\\n\\t";
+            }
+            o << "bra ssa_apply_end;\\n\\t";
+        }
+        o << "ssa_apply_end:\\n\\t}\"\n    : ";
+        for (int s2 = 0; s2 < S; ++s2) o << (s2 ? ", " : "") << "\"+d\"(x[" << s2 << "])";
+        o << "\n    : \"r\"(j));\n}\n";
+    } else {
+        o << "  switch (j) {\n";
+        for (int j = 0; j < R; ++j) {
+            if (m.rx[j].nu.empty()) continue;
+            o << "  case " << j << ":";
+            for (auto& d : m.rx[j].nu) o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
+            o << " break;\n";
+        }
+        o << "  default: break;\n  }\n  (void)x;\n}\n";
     }
-    o << "  default: break;\n  }\n  (void)x;\n}\n";
     return o.str();
 }
 
@@ -357,20 +446,16 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, K1
     TRY(nvrtc_compile(k1_full_source(m, block, minb), cubin, e.log));
     CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
-    // rates, modifier coefficients and x0 into the module's constant memory
-    std::vector<double> rate(std::max(m.R, 1), 0.0), modc(std::max(m.R, 1), 0.0), x0(m.S);
-    for (int j = 0; j < m.R; ++j) {
-        rate[j] = m.rx[j].rate;
-        modc[j] = m.rx[j].mod_coef;
+    // constant pool and x0 into the module's constant memory
+    {
+        double* pc = nullptr;
+        size_t bytes = 0, n_pool = 0, got = 0;
+        TRY(pinned_constants(m, &pc, &bytes, &n_pool));
+        CU(cudaLibraryGetGlobal(&e.c_k, &got, e.lib, "c_k"));
+        CU(cudaMemcpy(e.c_k, pc, sizeof(double) * n_pool, cudaMemcpyHostToDevice));
+        CU(cudaLibraryGetGlobal(&e.c_x0, &got, e.lib, "c_x0"));
+        CU(cudaMemcpy(e.c_x0, pc + n_pool, sizeof(double) * m.S, cudaMemcpyHostToDevice));
     }
-    for (int s = 0; s < m.S; ++s) x0[s] = (double)m.x0[s];
-    size_t bytes = 0;
-    CU(cudaLibraryGetGlobal(&e.c_rate, &bytes, e.lib, "c_rate"));
-    CU(cudaMemcpy(e.c_rate, rate.data(), sizeof(double) * rate.size(), cudaMemcpyHostToDevice));
-    CU(cudaLibraryGetGlobal(&e.c_modc, &bytes, e.lib, "c_modc"));
-    CU(cudaMemcpy(e.c_modc, modc.data(), sizeof(double) * modc.size(), cudaMemcpyHostToDevice));
-    CU(cudaLibraryGetGlobal(&e.c_x0, &bytes, e.lib, "c_x0"));
-    CU(cudaMemcpy(e.c_x0, x0.data(), sizeof(double) * x0.size(), cudaMemcpyHostToDevice));
     int nb = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)e.fn, block, 0));
     e.blocks_per_sm = std::max(nb, 1);
@@ -549,8 +634,8 @@ struct RangeOut {
 struct RunInfo {
     ssa_dev_stats stats;
     int path = 0;
-    double device_ms = 0, ssa_ms = 0, jit_ms = 0;
-    uint64_t h2d = 0, d2h = 0;
+    double device_ms = 0, ssa_ms = 0, jit_ms = 0, reduce_ms = 0;
+    uint64_t h2d = 0, d2h = 0, reduce_bytes = 0;
     int launches = 0;
 };
 
@@ -639,15 +724,13 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     // the run's model inputs: one async copy from page-locked host memory
     if (path == SSA_PATH_THREAD) {
         double* pc = nullptr;
-        size_t bytes = 0;
+        size_t bytes = 0, n_pool = 0;
         {
             std::lock_guard<std::mutex> lk(m->mu);
-            TRY(pinned_constants(*m, &pc, &bytes));
+            TRY(pinned_constants(*m, &pc, &bytes, &n_pool));
         }
-        const size_t R1 = (size_t)std::max(m->R, 1);
-        CU(cudaMemcpyAsync(k1->c_rate, pc, 8 * R1, cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(k1->c_modc, pc + R1, 8 * R1, cudaMemcpyHostToDevice, st));
-        CU(cudaMemcpyAsync(k1->c_x0, pc + 2 * R1, 8 * (size_t)m->S, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(k1->c_k, pc, 8 * n_pool, cudaMemcpyHostToDevice, st));
+        CU(cudaMemcpyAsync(k1->c_x0, pc + n_pool, 8 * (size_t)m->S, cudaMemcpyHostToDevice, st));
         info.h2d += bytes;
     } else {
         CU(cudaMemcpyAsync(k2->dev_image, k2->host_image, k2->image_bytes, cudaMemcpyHostToDevice, st));
@@ -693,11 +776,15 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         if (!p_sum) { CU(dsum.alloc(sizeof(ssa_dev_summary) * n_dump, st)); p_sum = dsum.as<ssa_dev_summary>(); }
     }
 
-    cudaEvent_t ev0, ev1, evs0, evs1;
+    cudaEvent_t ev0, ev1, evs0, evs1, evr1;
     CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1)); CU(cudaEventCreate(&evs0)); CU(cudaEventCreate(&evs1));
-    struct EvGuard { cudaEvent_t a, b, c, d; ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c); cudaEventDestroy(d); } } eg{ev0, ev1, evs0, evs1};
+    CU(cudaEventCreate(&evr1));
+    struct EvGuard {
+        cudaEvent_t a, b, c, d, e;
+        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c); cudaEventDestroy(d); cudaEventDestroy(e); }
+    } eg{ev0, ev1, evs0, evs1, evr1};
     CU(cudaEventRecord(ev0, st));
-    float ssa_ms_total = 0.f;
+    float ssa_ms_total = 0.f, reduce_ms_total = 0.f;
 
     const ssa_u32 key0 = (ssa_u32)seed, key1 = (ssa_u32)(seed >> 32);
     for (ssa_u64 ch = 0; ch < n_chunks; ++ch) {
@@ -742,17 +829,20 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         if (n_tiles > 1) {
             double* b = tiles.as<double>();
             ssa_tree_out to{b, b + cells * n_tiles, b + 2 * cells * n_tiles, n_tiles, 1, 0};
-            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, to, st));
+            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, to, st, &info.launches));
             TRY(reduce_partials(ssa_tree_in{to.n, to.mean, to.m2, n_tiles, 1}, n_tiles, cells, chunk_out, st,
                                 &info.launches));
         } else {
-            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, chunk_out, st));
+            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, chunk_out, st, &info.launches));
         }
-        info.launches += 1;
-        CU(cudaEventSynchronize(evs1));
+        CU(cudaEventRecord(evr1, st));
+        CU(cudaEventSynchronize(evr1));
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, evs0, evs1));
         ssa_ms_total += ms;
+        CU(cudaEventElapsedTime(&ms, evs1, evr1));
+        reduce_ms_total += ms;
+        info.reduce_bytes += cn * cells * sizeof(int);
     }
     // a10 (per GPU): chunk roots -> range root
     if (n_chunks > 1) {
@@ -776,6 +866,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     CU(cudaEventElapsedTime(&ms, ev0, ev1));
     info.device_ms = ms;
     info.ssa_ms = ssa_ms_total;
+    info.reduce_ms = reduce_ms_total;
     return SSA_OK;
 }
 
@@ -789,6 +880,8 @@ static ssa_status fill_result(const RunInfo& info, ssa_result* r)
     r->path_used = info.path;
     r->device_ms = info.device_ms;
     r->ssa_ms = info.ssa_ms;
+    r->reduce_ms = info.reduce_ms;
+    r->reduce_bytes = info.reduce_bytes;
     r->jit_ms = info.jit_ms;
     r->h2d_bytes = info.h2d;
     r->d2h_bytes = info.d2h;
@@ -896,7 +989,8 @@ extern "C" ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, ui
     r->events = r->near_ties = r->n_errors = r->first_error_id = 0;
     r->first_error_reaction = -1;
     r->path_used = 0;
-    r->device_ms = r->ssa_ms = r->jit_ms = 0.0;
+    r->device_ms = r->ssa_ms = r->jit_ms = r->reduce_ms = 0.0;
+    r->reduce_bytes = 0;
     r->h2d_bytes = r->d2h_bytes = 0;
     r->kernel_launches = 0;
     // element (cell, rank) at d_roots[rank * 3 * cells + {0,1,2} * cells + cell]

@@ -63,7 +63,7 @@ cudaError_t ssa_k2_launch(const ssa_k2_params& p, int grid, int block, cudaStrea
 int ssa_k2_max_blocks_per_sm(int pmax, int block, size_t smem);
 
 cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 count, ssa_u64 rows,
-                                 const ssa_tree_out& out, cudaStream_t st);
+                                 const ssa_tree_out& out, cudaStream_t st, int* launches);
 cudaError_t ssa_tree_merge_launch(const ssa_tree_in& in, ssa_u64 count, ssa_u64 rows, const ssa_tree_out& out,
                                   cudaStream_t st);
 cudaError_t ssa_finalize_launch(const double* n, const double* mean, const double* m2, ssa_u64 cells,

@@ -69,7 +69,7 @@ class ssa_result(C.Structure):
                 ("first_error_id", C.c_uint64), ("first_error_reaction", C.c_int32), ("path_used", C.c_int32),
                 ("device_ms", C.c_double), ("ssa_ms", C.c_double), ("jit_ms", C.c_double),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("kernel_launches", C.c_int32),
-                ("pad2", C.c_int32)]
+                ("pad2", C.c_int32), ("reduce_ms", C.c_double), ("reduce_bytes", C.c_uint64)]
 
 
 _lib = None
@@ -198,6 +198,8 @@ class RunResult:
     kernel_launches: int
     status: int
     dump: Optional[Dump] = None
+    reduce_ms: float = 0.0           # device time of the chunk reductions (K3)
+    reduce_bytes: int = 0            # staged bytes they read
 
 
 def _options(path=SSA_PATH_AUTO, device=-1, stream=None, chunk=0, staging_budget_bytes=0, block=0,
@@ -225,7 +227,7 @@ def _make_dump(ids, G, S):
 def _result_from(r: ssa_result, st: int, mean, var, m2, count, dump=None) -> RunResult:
     return RunResult(mean, var, m2, count, r.events, r.near_ties, r.n_errors, r.first_error_id,
                      r.first_error_reaction, r.path_used, r.device_ms, r.ssa_ms, r.jit_ms, r.h2d_bytes,
-                     r.d2h_bytes, r.kernel_launches, st, dump)
+                     r.d2h_bytes, r.kernel_launches, st, dump, r.reduce_ms, r.reduce_bytes)
 
 
 def run(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed: int, *,

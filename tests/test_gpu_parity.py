@@ -101,6 +101,47 @@ def test_hiv_config2_full_size_sampled(S):
     assert np.all(r.mean[:, 0] == 1.0) and np.all(r.var[:, 0] == 0.0)
 
 
+def test_config4_shards_sampled(S):
+    """BASELINE configs[4] (HIV, 400 d, 2^24 ids over W = 8 shards, 65,536
+    dumped ids): in two of the eight shards (ranks 0 and 7) an aligned block of
+    4096 ids is run at the full horizon through ssa_run_shard with global ids
+    (so the Philox stream is the one the 8-GPU run uses).  Every config-4
+    dumped id in the blocks is replayed by the oracle bit-exactly, and the
+    shard root of one block is checked against the exact moments of all its
+    4096 trajectories (T2)."""
+    import torch
+    cfg = inputs.config(4)
+    n_total, W, blk = cfg.n_trajectories, 8, 4096
+    m = S.Model(cfg.network)
+    G = S.grid_size(cfg.t_end, cfg.dt)
+    cells = G * cfg.network.S
+    dumped = inputs.dump_ids(n_total, cfg.n_dump, cfg.seed)
+    for rank in (0, W - 1):
+        b, e = S.shard_bounds(n_total, W, rank)
+        lo = b + (e - b) // 2                        # aligned block in the middle of the shard
+        hi = lo + blk
+        assert lo % blk == 0
+        sel = dumped[(dumped >= lo) & (dumped < hi)]
+        assert len(sel) >= 4
+        ids = np.arange(lo, hi, dtype=np.uint64) if rank == 0 else sel
+        root = torch.zeros((1, 3, cells), dtype=torch.float64, device="cuda")
+        r = S.run_shard(m, lo, hi, cfg.t_end, cfg.dt, cfg.seed, root[0], path=THREAD, dump_ids=ids)
+        assert r.n_errors == 0
+        pos = np.searchsorted(ids, sel)
+        gx, ge, gt, sm = oracle_replay(cfg.network, sel, cfg.seed, cfg.t_end, cfg.dt, 0)
+        assert np.array_equal(r.dump.states[pos], gx)
+        assert np.array_equal(r.dump.events_at[pos], ge)
+        assert np.array_equal(r.dump.time_at[pos], gt)
+        assert np.array_equal(r.dump.summary["hash"][pos], sm["hash"])
+        assert np.array_equal(r.dump.summary["events"][pos], sm["events"])
+        if rank == 0:
+            mean, var, _, count = S.merge_roots(root, 1, cells)
+            ref_mean, ref_var = exact_moments(r.dump.states)
+            assert_moments_close(mean.reshape(G, -1), var.reshape(G, -1), ref_mean, ref_var)
+            assert np.all(count == blk)
+            assert r.events == int(r.dump.summary["events"].sum())
+
+
 # ------------------------------------------------------------ config 3 (warp path)
 def test_config3_warp_parity(S):
     cfg = inputs.config(3)
