@@ -74,9 +74,15 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
         int jp[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int q = 0; q < SSA_R - 1; ++q)   // compare + predicated increment
-            asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
-                : "+r"(jp[q & 3]) : "d"(c[q]), "d"(r));
+        for (int q = 0; q < SSA_R - 1; ++q) {   // compare + predicated increment
+            if (SSA_K1_SEL == 1 || (SSA_K1_SEL == 2 && (q & 1)))
+                // c_j, r >= +0 and not NaN: their bit patterns order as int64 (ALU pipe)
+                asm("{\n\t.reg .pred p;\n\tsetp.le.s64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                    : "+r"(jp[q & 3]) : "l"(__double_as_longlong(c[q])), "l"(__double_as_longlong(r)));
+            else
+                asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                    : "+r"(jp[q & 3]) : "d"(c[q]), "d"(r));
+        }
         const int j = (jp[0] + jp[1]) + (jp[2] + jp[3]);
         // a5: tau = E / a0 by the fast in-range IEEE division (speculative:
         // replaced on the rare path when a0 is outside [2^-900, 2^901))

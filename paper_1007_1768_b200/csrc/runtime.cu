@@ -293,6 +293,7 @@ static std::string prop_stmts(const RxI& q, const std::vector<double>& pool)
 // species counts in shared memory with a table update were both slower.)
 struct K1Gen {
     bool flat_switch = true;
+    int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
 };
 
 static K1Gen k1_gen()
@@ -302,6 +303,8 @@ static K1Gen k1_gen()
         const char* e = getenv("SSA_K1_GEN");
         const std::string s = e ? e : "";
         if (s.find("upd=switch") != std::string::npos) r.flat_switch = false;
+        if (s.find("sel=i64") != std::string::npos) r.sel = 1;
+        if (s.find("sel=mix") != std::string::npos) r.sel = 2;
         return r;
     }();
     return g;
@@ -313,7 +316,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb)
     const K1Gen g = k1_gen();
     std::ostringstream o;
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
-      << "\n#define SSA_K1_MINB " << minb << "\n";
+      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n";
     const std::vector<double> pool = const_pool(m);
     o << "__constant__ double c_k[" << pool.size() << "];\n__constant__ double c_x0[" << S << "];\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
