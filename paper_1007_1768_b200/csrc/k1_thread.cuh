@@ -18,6 +18,9 @@
 // as trajectories end.  Output is keyed by id, so results do not depend on
 // the schedule.
 //
+// SSA_K1_DUMP = 0 (runs without dumped ids) drops the raw-trajectory dump
+// and the firing hash, which only the dump exposes.
+//
 // Control flow: one loop iteration = one candidate event.  The common case
 // (a0 in the fast-division range, no grid point crossed) runs straight
 // through to the update with a single, rarely taken branch; everything else
@@ -45,7 +48,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         rel = atomicAdd(P.work, 1ull);
         if (rel >= P.n_ids) return false;
         id = P.id_begin + rel;
+#if SSA_K1_DUMP
         slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
+#endif
 #pragma unroll
         for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
         t = 0.0; s_next = 0.0; e = 0; k = 0; hash = SSA_FNV_OFFSET; ties = 0;
@@ -119,6 +124,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                         if (x[s] > 2147483647.0) status = 2;
                         dst[(ssa_u64)s * P.stride] = (int)x[s];
                     }
+#if SSA_K1_DUMP
                     if (slot >= 0) {
                         const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
 #pragma unroll
@@ -126,6 +132,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                         P.dump_e[base] = e;
                         P.dump_t[base] = (e > 0) ? t : 0.0;
                     }
+#endif
                     ++k;
                     s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
                 } while (tn > s_next);
@@ -135,6 +142,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 // trajectory done: per-trajectory records, then refill (a1)
                 my_events += e;
                 my_ties += ties;
+#if SSA_K1_DUMP
                 if (slot >= 0) {
                     ssa_dev_summary sm;
                     sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
@@ -142,6 +150,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     sm.err_reaction = err_r; sm.pad = 0;
                     P.dump_sum[slot] = sm;
                 }
+#endif
                 if (status) {
                     const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
                     atomicAdd(&P.stats->n_errors, 1ull);
@@ -158,7 +167,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         ssa_apply(j, x);
         t = tn;
         ++e;
-        hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
+#if SSA_K1_DUMP
+        hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;   // firing hash: observable only through the dump
+#endif
     }
     // warp-level reduction of the counters, then one atomic per warp
 #pragma unroll

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <sstream>
@@ -88,7 +89,7 @@ struct K2Dev {
 };
 
 struct DevCache {
-    std::map<std::pair<int, int>, K1Entry> k1;  // (block, minb)
+    std::map<std::tuple<int, int, int>, K1Entry> k1;  // (block, minb, dump)
     K2Dev k2;
 };
 
@@ -310,13 +311,14 @@ static K1Gen k1_gen()
     return g;
 }
 
-static std::string gen_k1_model(const ssa_model& m, int block, int minb)
+static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump)
 {
     const int S = m.S, R = m.R;
     const K1Gen g = k1_gen();
     std::ostringstream o;
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
-      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n";
+      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
+      << (dump ? 1 : 0) << "\n";
     const std::vector<double> pool = const_pool(m);
     o << "__constant__ double c_k[" << pool.size() << "];\n__constant__ double c_x0[" << S << "];\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
@@ -418,9 +420,11 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
     return SSA_OK;
 }
 
-static std::string k1_full_source(const ssa_model& m, int block, int minb)
+// dump: the variant that also records the raw-trajectory dump and the firing
+// hash (a11); runs without dumped ids use the variant without them.
+static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump)
 {
-    return std::string(kSsaDeviceSrc) + "\n" + gen_k1_model(m, block, minb) + "\n" + kK1ThreadSrc;
+    return std::string(kSsaDeviceSrc) + "\n" + gen_k1_model(m, block, minb, dump) + "\n" + kK1ThreadSrc;
 }
 
 static int default_minb(const ssa_model& m, int block)
@@ -432,10 +436,11 @@ static int default_minb(const ssa_model& m, int block)
 }
 
 // requires: current device == dev, m.mu held
-static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, K1Entry** out, double* jit_ms)
+static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, K1Entry** out,
+                            double* jit_ms)
 {
     DevCache& dc = m.dev[dev];
-    auto key = std::make_pair(block, minb);
+    auto key = std::make_tuple(block, minb, dump ? 1 : 0);
     auto it = dc.k1.find(key);
     if (it != dc.k1.end()) {
         *out = &it->second;
@@ -446,7 +451,7 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, K1
     e.block = block;
     e.minb = minb;
     std::vector<char> cubin;
-    TRY(nvrtc_compile(k1_full_source(m, block, minb), cubin, e.log));
+    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump), cubin, e.log));
     CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
     // constant pool and x0 into the module's constant memory
@@ -704,7 +709,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // blocks_per_sm > 0 also sets the K1 variant's __launch_bounds__ residency
             // target (its register budget is 64K / (block * blocks_per_sm))
             const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : default_minb(*m, block);
-            TRY(ensure_k1(*m, c.device, block, minb, &k1, &info.jit_ms));
+            TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, &k1, &info.jit_ms));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
@@ -1014,7 +1019,7 @@ extern "C" ssa_status ssa_model_prepare(const ssa_model* m, int32_t device, int3
     std::lock_guard<std::mutex> lk(m->mu);
     if (path == SSA_PATH_THREAD) {
         K1Entry* e = nullptr;
-        return ensure_k1(*m, c.device, 128, default_minb(*m, 128), &e, nullptr);
+        return ensure_k1(*m, c.device, 128, default_minb(*m, 128), false, &e, nullptr);
     }
     K2Dev* k = nullptr;
     return ensure_k2(*m, c.device, &k);
@@ -1042,21 +1047,21 @@ extern "C" int32_t ssa_abi_version(void) { return 1; }
 
 // Test/diagnostic hooks (not part of the stable ABI): the generated K1
 // source for a model, and compiling it without a device (NVRTC only).
-extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, int32_t minb)
+extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, int32_t minb, int32_t dump)
 {
     static thread_local std::string s;
     if (!m) return "";
-    s = k1_full_source(*m, block, minb);
+    s = k1_full_source(*m, block, minb, dump != 0);
     return s.c_str();
 }
 
-extern "C" ssa_status ssa_debug_k1_compile(const ssa_model* m, int32_t block, int32_t minb, char* log, uint64_t log_cap,
-                                           uint64_t* cubin_bytes)
+extern "C" ssa_status ssa_debug_k1_compile(const ssa_model* m, int32_t block, int32_t minb, int32_t dump, char* log,
+                                           uint64_t log_cap, uint64_t* cubin_bytes)
 {
     if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
     std::vector<char> cubin;
     std::string lg;
-    ssa_status st = nvrtc_compile(k1_full_source(*m, block, minb), cubin, lg);
+    ssa_status st = nvrtc_compile(k1_full_source(*m, block, minb, dump != 0), cubin, lg);
     if (log && log_cap) {
         std::string all = (st == SSA_OK) ? lg : g_err;
         strncpy(log, all.c_str(), (size_t)log_cap - 1);

@@ -106,9 +106,9 @@ def lib():
         L.ssa_last_error.argtypes = []
         L.ssa_last_error.restype = C.c_char_p
         L.ssa_abi_version.restype = C.c_int32
-        L.ssa_debug_k1_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        L.ssa_debug_k1_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]
         L.ssa_debug_k1_source.restype = C.c_char_p
-        L.ssa_debug_k1_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
+        L.ssa_debug_k1_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                            P(C.c_uint64)]
         L.ssa_debug_k1_compile.restype = C.c_int
         _lib = L
@@ -158,14 +158,15 @@ class Model:
     def prepare(self, device: int = -1, path: int = SSA_PATH_AUTO):
         _check(lib().ssa_model_prepare(self.handle, device, path))
 
-    def k1_source(self, block: int = 128, minb: int = 4) -> str:
-        return lib().ssa_debug_k1_source(self.handle, block, minb).decode()
+    def k1_source(self, block: int = 128, minb: int = 4, dump: bool = False) -> str:
+        """Generated K1 source (dump=True: the variant with raw-trajectory dump + hash)."""
+        return lib().ssa_debug_k1_source(self.handle, block, minb, int(dump)).decode()
 
-    def k1_compile(self, block: int = 128, minb: int = 4):
+    def k1_compile(self, block: int = 128, minb: int = 4, dump: bool = False):
         """NVRTC-compile the model's K1 kernel (no device needed); returns (status, log, cubin bytes)."""
         buf = C.create_string_buffer(1 << 16)
         nb = C.c_uint64()
-        st = lib().ssa_debug_k1_compile(self.handle, block, minb, buf, len(buf), C.byref(nb))
+        st = lib().ssa_debug_k1_compile(self.handle, block, minb, int(dump), buf, len(buf), C.byref(nb))
         return st, buf.value.decode(errors="replace"), nb.value
 
 
