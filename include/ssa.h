@@ -180,6 +180,25 @@ ssa_status ssa_run_shard(const ssa_model* model, uint64_t id_begin, uint64_t id_
                          double sample_dt, uint64_t seed, double* d_root, const ssa_run_options* opts,
                          ssa_result* result);
 
+/* Parameter sweep: StochRxn_ff's "set of parameter-swept simulations"
+ * (§3.2), e.g. the delta_t sensitivity analysis of Fig. 4 panels
+ * 2-4.  n_points parameter points, each a full vector of
+ * rate constants: rates[p*R + j] (HOST, finite, >= 0) and, optionally,
+ * modifier coefficients mod_coefs[p*R + j] (HOST, finite; NULL = the model's).
+ * The model supplies species, stoichiometry, modifier species and initial
+ * counts.  Every point simulates trajectories 0..n_per_point-1 with the same
+ * seed (common random numbers across points, R31), so point p's
+ * grids are bitwise those of ssa_run on the model with point p's constants.
+ * result->mean/var/m2/count are [n_points][G*S] (host, or device with
+ * opts->outputs_on_device); the counters are totals over all points.  Dump ids
+ * (opts->dump) are virtual ids p*n_per_point + i.  Thread path only
+ * (SSA_ERR_UNSUPPORTED for the warp path); the points whose staging fits the
+ * budget run in one kernel launch.  Errors as ssa_run (first_error_id is the
+ * virtual id). */
+ssa_status ssa_run_sweep(const ssa_model* model, int32_t n_points, const double* rates, const double* mod_coefs,
+                         uint64_t n_per_point, double t_end, double sample_dt, uint64_t seed, uint32_t reducers,
+                         const ssa_run_options* opts, ssa_result* result);
+
 /* Merge n_roots shard roots (DEVICE memory, contiguous [n_roots][3][cells],
  * in rank order, each an aligned subtree of equal span) as the top levels of
  * the canonical tree, then finalize into result->mean/var/m2/count (host or

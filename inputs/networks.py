@@ -200,6 +200,42 @@ def config(i: int) -> Config:
     return configs()[i]
 
 
+# --------------------------------------------------------------------------
+# Parameter sweeps ("a set of parameter-swept simulations";
+# Fig. 4 panels 2-4: delta_t = 5.0, 3.0, 0.5).
+# --------------------------------------------------------------------------
+def with_rates(net: Network, rates: Sequence[float]) -> Network:
+    """The same network with its rate constants replaced (one sweep point)."""
+    assert len(rates) == net.R
+    rx = tuple(Reaction(r.reactants, r.products, float(k), r.modifier_species, r.modifier_coef, r.name)
+               for r, k in zip(net.reactions, rates))
+    return Network(net.species, net.x0, rx, net.name)
+
+
+def rate_matrix(net: Network, reaction_index: Sequence[int], values: Sequence[float]) -> np.ndarray:
+    """[len(values), R] rate vectors: the network's rates with the listed
+    reactions' rate set to each value in turn."""
+    base = np.array([r.rate for r in net.reactions], dtype=np.float64)
+    out = np.tile(base, (len(values), 1))
+    for p, v in enumerate(values):
+        out[p, list(reaction_index)] = v
+    return out
+
+
+HIV_DELTA_T_SWEEP = (5.0, 3.0, 0.5)   # Fig. 4 panels 2-4 (PAPER.md:155)
+
+
+def hiv_delta_t_sweep(values: Sequence[float] = HIV_DELTA_T_SWEEP, param: str = "d_t"):
+    """(network, rates [P, R]) for the Fig. 4 sensitivity sweep.  param 'd_t'
+    sweeps the parameter the paper names (T clearance, reaction 6; SPEC.md's
+    reading); 'd_v' sweeps the virus clearance (reactions 26, 27), the
+    parameter the text describes as "regulating the lifespan of the virus"
+    (R32)."""
+    net = hiv()
+    idx = {"d_t": [5], "d_v": [25, 26]}[param]
+    return net, rate_matrix(net, idx, values)
+
+
 def dump_ids(n_total: int, n_dump: int, seed: int) -> np.ndarray:
     """Sorted, distinct trajectory ids to dump raw (R24)."""
     rng = np.random.Generator(np.random.PCG64(seed + 0x5EED))

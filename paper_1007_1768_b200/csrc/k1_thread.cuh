@@ -37,9 +37,18 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     const ssa_u64 G = (ssa_u64)K + 1;
     ssa_u64 my_events = 0, my_ties = 0;
 
+#if SSA_K1_SWEEP
+    // parameter sweep: the chunk's per-point constants in shared memory; kp
+    // points at the row of the current trajectory's sweep point
+    extern __shared__ double s_k[];
+    for (int q = threadIdx.x; q < P.n_pts * P.n_pool; q += blockDim.x) s_k[q] = P.pconst[q];
+    __syncthreads();
+    const double* kp = s_k;
+    const ssa_u64 pt0 = P.id_begin / P.n_per_point;
+#endif
     double x[SSA_S];
     double t = 0.0, s_next = 0.0;
-    ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0;
+    ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0, vid = 0;
     long long k = 0, slot = -1;
     int status = 0, absorbed = 0, err_r = -1;
 
@@ -47,9 +56,18 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     auto start = [&]() -> bool {
         rel = atomicAdd(P.work, 1ull);
         if (rel >= P.n_ids) return false;
-        id = P.id_begin + rel;
+        vid = P.id_begin + rel;
+#if SSA_K1_SWEEP
+        {
+            const ssa_u64 pt = vid / P.n_per_point;
+            id = vid - pt * P.n_per_point;       // trajectory id within its sweep point (RNG key)
+            kp = s_k + (pt - pt0) * (ssa_u64)P.n_pool;
+        }
+#else
+        id = vid;
+#endif
 #if SSA_K1_DUMP
-        slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
+        slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
 #endif
 #pragma unroll
         for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
@@ -67,7 +85,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // independent dependency chains in one basic block, so the scheduler
         // interleaves them.
         double c[SSA_R > 0 ? SSA_R : 1];
-        const double a0 = ssa_prefix(x, c);
+        const double a0 = ssa_prefix(x, c SSA_KP_ARG);
         // keep the prefix in registers: without this barrier the compiler
         // recomputes the whole propensity chain for the selection (a7)
 #pragma unroll
@@ -106,7 +124,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 } else {
                     tn = INF;            // non-finite propensity: error (id, reaction)
                     status = 1;
-                    err_r = ssa_first_bad(x);
+                    err_r = ssa_first_bad(x SSA_KP_ARG);
                     fin = true;
                 }
             }
@@ -156,7 +174,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     atomicAdd(&P.stats->n_errors, 1ull);
                     atomicOr(&P.stats->err_code, code);
                     // smallest id wins; pack (id, code, reaction) so one atomicMin keeps them together
-                    const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
+                    const ssa_u64 packed = (vid << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
                     atomicMin(&P.stats->first_err_id, packed);
                 }
                 live = start();

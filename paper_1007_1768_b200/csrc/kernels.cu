@@ -465,7 +465,7 @@ __global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __res
     const ssa_u64 base = tile * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
     const int* src = staging + row * stride;
     ssa_welford v[8];
-    if (base + 8 <= count && (stride % 4) == 0) {
+    if (base + 8 <= count && (((uintptr_t)(src + base)) & 15) == 0) {
         const int4 q0 = *reinterpret_cast<const int4*>(src + base);
         const int4 q1 = *reinterpret_cast<const int4*>(src + base + 4);
         v[0] = ssa_welford_leaf(q0.x); v[1] = ssa_welford_leaf(q0.y);
@@ -534,7 +534,8 @@ cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 cou
 {
     const ssa_u64 bx = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
     // full tiles through the division-free kernel (needs 16-byte aligned rows)
-    const ssa_u64 n_full = (stride % 4 == 0) ? count / SSA_TREE_SPAN : 0;
+    const bool aligned = stride % 4 == 0 && ((uintptr_t)staging % 16) == 0;
+    const ssa_u64 n_full = aligned ? count / SSA_TREE_SPAN : 0;
     if (n_full) {
         ssa_tree_leaf_full<<<tree_grid((n_full + 1) / 2, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, n_full,
                                                                                           rows, out);

@@ -89,7 +89,7 @@ struct K2Dev {
 };
 
 struct DevCache {
-    std::map<std::tuple<int, int, int>, K1Entry> k1;  // (block, minb, dump)
+    std::map<std::string, K1Entry> k1;  // k1_key(block, minb, dump, sweep layout)
     K2Dev k2;
 };
 
@@ -102,26 +102,14 @@ struct ssa_model {
     mutable double* pinned_const = nullptr;  // [constant pool][x0 S], page-locked, for per-run uploads
 };
 
-static std::vector<double> const_pool(const ssa_model& m);
+struct PoolLayout;
+static PoolLayout make_pool(const ssa_model& m, int points, const double* rates, const double* modcs);
 
-// K1 constant-memory image of the model's numbers (the pool of distinct rate
-// and modifier constants, then the initial counts), staged once in
-// page-locked host memory and copied to the device at the start of every run
-// (the run's inputs).  *n_pool receives the pool size.
-static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* bytes, size_t* n_pool)
-{
-    const std::vector<double> pool = const_pool(m);
-    *n_pool = pool.size();
-    *bytes = sizeof(double) * (pool.size() + (size_t)m.S);
-    if (!m.pinned_const) {
-        CU(cudaMallocHost(&m.pinned_const, *bytes));
-        double* p = m.pinned_const;
-        for (size_t i = 0; i < pool.size(); ++i) p[i] = pool[i];
-        for (int s = 0; s < m.S; ++s) p[pool.size() + s] = (double)m.x0[s];
-    }
-    *out = m.pinned_const;
-    return SSA_OK;
-}
+// K1 constant-memory image of the model's numbers (its constant pool, then
+// the initial counts), staged once in page-locked host memory and copied to
+// the device at the start of every run (the run's inputs).  *n_pool receives
+// the pool size.
+static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* bytes, size_t* n_pool);
 
 extern "C" ssa_status ssa_model_create(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
                                        const ssa_reaction* reactions, ssa_model** out)
@@ -233,46 +221,85 @@ static std::string factor_expr(int s, int m)
     return o.str();
 }
 
-// Pool of the distinct rate / modifier constants of a model (bitwise
-// distinct values, first-appearance order); K1 reads them from the module's
-// __constant__ c_k[] (a uniform load fetches two), so equal constants are
-// loaded once per event.
-static std::vector<double> const_pool(const ssa_model& m)
+// Layout of the K1 constants: the model's rate and modifier constants,
+// deduplicated into slots.  For a parameter sweep each reaction's constant
+// is a column over the sweep points and two reactions share a slot only if
+// their columns are bitwise equal at every point; a plain run is the
+// one-point case.  K1 reads slot i as SSA_K(i): c_k[i] from __constant__
+// memory (one uniform load fetches two), or kp[i] from the per-point rows in
+// shared memory in the sweep variant.  The clamp max(0, k + d*x) of P:93 is
+// emitted only if d < 0 at some point (k >= 0 and d >= 0 give k + d*x >= 0 for
+// counts x >= 0, so there it is a no-op).
+struct PoolLayout {
+    int n = 0;                       // slots
+    std::vector<int> rate_slot, mod_slot;
+    std::vector<char> clamp;
+    std::vector<double> values;      // [points][n]
+};
+
+static PoolLayout make_pool(const ssa_model& m, int points, const double* rates, const double* modcs)
 {
-    std::vector<double> pool;
-    auto add = [&](double v) {
-        for (double p : pool)
-            if (memcmp(&p, &v, sizeof v) == 0) return;
-        pool.push_back(v);
+    PoolLayout L;
+    const int R = m.R;
+    auto rate = [&](int p, int j) { return rates ? rates[(size_t)p * R + j] : m.rx[j].rate; };
+    auto modc = [&](int p, int j) { return modcs ? modcs[(size_t)p * R + j] : m.rx[j].mod_coef; };
+    std::vector<std::vector<double>> cols;
+    auto slot_of = [&](const std::vector<double>& col) {
+        for (size_t i = 0; i < cols.size(); ++i)
+            if (memcmp(cols[i].data(), col.data(), sizeof(double) * col.size()) == 0) return (int)i;
+        cols.push_back(col);
+        return (int)cols.size() - 1;
     };
-    for (int j = 0; j < m.R; ++j) {
-        add(m.rx[j].rate);
-        if (m.rx[j].mod_sp >= 0) add(m.rx[j].mod_coef);
+    L.rate_slot.assign(R, -1);
+    L.mod_slot.assign(R, -1);
+    L.clamp.assign(R, 0);
+    std::vector<double> col(points);
+    for (int j = 0; j < R; ++j) {
+        for (int p = 0; p < points; ++p) col[p] = rate(p, j);
+        L.rate_slot[j] = slot_of(col);
+        if (m.rx[j].mod_sp >= 0) {
+            bool neg = false;
+            for (int p = 0; p < points; ++p) {
+                col[p] = modc(p, j);
+                neg = neg || !(col[p] >= 0.0);
+            }
+            L.mod_slot[j] = slot_of(col);
+            L.clamp[j] = neg;
+        }
     }
-    if (pool.empty()) pool.push_back(0.0);
-    return pool;
+    if (cols.empty()) cols.push_back(std::vector<double>(points, 0.0));
+    L.n = (int)cols.size();
+    L.values.resize((size_t)points * L.n);
+    for (int p = 0; p < points; ++p)
+        for (int i = 0; i < L.n; ++i) L.values[(size_t)p * L.n + i] = cols[i][p];
+    return L;
 }
 
-static int pool_index(const std::vector<double>& pool, double v)
+static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* bytes, size_t* n_pool)
 {
-    for (size_t i = 0; i < pool.size(); ++i)
-        if (memcmp(&pool[i], &v, sizeof v) == 0) return (int)i;
-    return -1;
+    const PoolLayout L = make_pool(m, 1, nullptr, nullptr);
+    *n_pool = (size_t)L.n;
+    *bytes = sizeof(double) * ((size_t)L.n + (size_t)m.S);
+    if (!m.pinned_const) {
+        CU(cudaMallocHost(&m.pinned_const, *bytes));
+        double* p = m.pinned_const;
+        for (int i = 0; i < L.n; ++i) p[i] = L.values[i];
+        for (int s = 0; s < m.S; ++s) p[L.n + s] = (double)m.x0[s];
+    }
+    *out = m.pinned_const;
+    return SSA_OK;
 }
 
 // a3 for reaction j: k^ (rate, or the clamped linear modifier of P:93), then
-// a = k^ * h.  The model is immutable, so the sign of each modifier
-// coefficient is known when its kernel is generated: the clamp max(0, .) is
-// emitted only for d < 0 (k >= 0 and d >= 0 give k + d*x >= 0 for counts
-// x >= 0, so there it is a no-op).
-static std::string prop_stmts(const RxI& q, const std::vector<double>& pool)
+// a = k^ * h.
+static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L)
 {
     std::ostringstream o;
-    const std::string rate = "c_k[" + std::to_string(pool_index(pool, q.rate)) + "]";
+    const std::string rate = "SSA_K(" + std::to_string(L.rate_slot[j]) + ")";
     if (q.mod_sp >= 0) {
-        const std::string modc = "c_k[" + std::to_string(pool_index(pool, q.mod_coef)) + "]";
+        const std::string modc = "SSA_K(" + std::to_string(L.mod_slot[j]) + ")";
         o << "k = __dadd_rn(" << rate << ", __dmul_rn(" << modc << ", x[" << q.mod_sp << "])); ";
-        if (!(q.mod_coef >= 0.0)) o << "k = (k < 0.0) ? 0.0 : k; ";
+        if (L.clamp[j]) o << "k = (k < 0.0) ? 0.0 : k; ";
     } else {
         o << "k = " << rate << "; ";
     }
@@ -311,36 +338,43 @@ static K1Gen k1_gen()
     return g;
 }
 
-static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump)
+// sweep: the parameter-sweep variant (constants per sweep point, read from
+// shared memory through kp); L: the constant layout the code indexes.
+static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump, bool sweep, const PoolLayout& L)
 {
     const int S = m.S, R = m.R;
     const K1Gen g = k1_gen();
     std::ostringstream o;
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
       << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
-      << (dump ? 1 : 0) << "\n";
-    const std::vector<double> pool = const_pool(m);
-    o << "__constant__ double c_k[" << pool.size() << "];\n__constant__ double c_x0[" << S << "];\n";
+      << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
+    if (sweep) {
+        o << "#define SSA_K(i) kp[i]\n#define SSA_KP_PARAM , const double* __restrict__ kp\n#define SSA_KP_ARG , kp\n";
+    } else {
+        o << "__constant__ double c_k[" << L.n << "];\n";
+        o << "#define SSA_K(i) c_k[i]\n#define SSA_KP_PARAM\n#define SSA_KP_ARG\n";
+    }
+    o << "__constant__ double c_x0[" << S << "];\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
-    o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], double (&c)[SSA_R > 0 ? SSA_R : 1]) {\n";
+    o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], double (&c)[SSA_R > 0 ? SSA_R : 1] SSA_KP_PARAM) {\n";
     o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)c;\n";
     for (int j = 0; j < R; ++j) {
-        o << "  { " << prop_stmts(m.rx[j], pool) << " "
+        o << "  { " << prop_stmts(m.rx[j], j, L) << " "
           << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
     }
     o << "  return acc;\n}\n";
     // error path only: out of line, state passed by value so the caller's
     // counts never need an addressable (stack) copy
     o << "struct ssa_state_v { double v[SSA_S]; };\n";
-    o << "static __device__ __noinline__ int ssa_first_bad_v(const ssa_state_v xs) {\n";
+    o << "static __device__ __noinline__ int ssa_first_bad_v(const ssa_state_v xs SSA_KP_PARAM) {\n";
     o << "  const double* x = xs.v;\n";
     o << "  double a, h, k; (void)a; (void)h; (void)k; (void)x;\n";
     for (int j = 0; j < R; ++j)
-        o << "  { " << prop_stmts(m.rx[j], pool) << " if (!(fabs(a) < __longlong_as_double(0x7FF0000000000000ll))) return " << j << "; }\n";
+        o << "  { " << prop_stmts(m.rx[j], j, L) << " if (!(fabs(a) < __longlong_as_double(0x7FF0000000000000ll))) return " << j << "; }\n";
     o << "  return -1;\n}\n";
-    o << "static __device__ __forceinline__ int ssa_first_bad(const double (&x)[SSA_S]) {\n";
+    o << "static __device__ __forceinline__ int ssa_first_bad(const double (&x)[SSA_S] SSA_KP_PARAM) {\n";
     o << "  ssa_state_v xs;\n#pragma unroll\n  for (int s = 0; s < SSA_S; ++s) xs.v[s] = x[s];\n";
-    o << "  return ssa_first_bad_v(xs);\n}\n";
+    o << "  return ssa_first_bad_v(xs SSA_KP_ARG);\n}\n";
     bool any_nu = false;
     for (int j = 0; j < R; ++j) any_nu = any_nu || !m.rx[j].nu.empty();
     bool exact_imm = true;   // every delta is an exact fp64 immediate (|d| < 2^53)
@@ -422,9 +456,25 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
 
 // dump: the variant that also records the raw-trajectory dump and the firing
 // hash (a11); runs without dumped ids use the variant without them.
-static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump)
+// sweep: the parameter-sweep variant indexing the layout *sweep (else the
+// model's own constant pool).
+static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep)
 {
-    return std::string(kSsaDeviceSrc) + "\n" + gen_k1_model(m, block, minb, dump) + "\n" + kK1ThreadSrc;
+    const PoolLayout L = sweep ? *sweep : make_pool(m, 1, nullptr, nullptr);
+    return std::string(kSsaDeviceSrc) + "\n" + gen_k1_model(m, block, minb, dump, sweep != nullptr, L) + "\n" +
+           kK1ThreadSrc;
+}
+
+static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep)
+{
+    std::ostringstream o;
+    o << block << "/" << minb << "/" << (dump ? 1 : 0);
+    if (sweep) {
+        o << "/sweep:" << sweep->n;
+        for (size_t j = 0; j < sweep->rate_slot.size(); ++j)
+            o << "," << sweep->rate_slot[j] << ":" << sweep->mod_slot[j] << ":" << (int)sweep->clamp[j];
+    }
+    return o.str();
 }
 
 static int default_minb(const ssa_model& m, int block)
@@ -436,11 +486,11 @@ static int default_minb(const ssa_model& m, int block)
 }
 
 // requires: current device == dev, m.mu held
-static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, K1Entry** out,
-                            double* jit_ms)
+static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, const PoolLayout* sweep,
+                            K1Entry** out, double* jit_ms)
 {
     DevCache& dc = m.dev[dev];
-    auto key = std::make_tuple(block, minb, dump ? 1 : 0);
+    const std::string key = k1_key(block, minb, dump, sweep);
     auto it = dc.k1.find(key);
     if (it != dc.k1.end()) {
         *out = &it->second;
@@ -451,16 +501,18 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
     e.block = block;
     e.minb = minb;
     std::vector<char> cubin;
-    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump), cubin, e.log));
+    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep), cubin, e.log));
     CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
-    // constant pool and x0 into the module's constant memory
+    // constant pool (plain runs) and x0 into the module's constant memory
     {
         double* pc = nullptr;
         size_t bytes = 0, n_pool = 0, got = 0;
         TRY(pinned_constants(m, &pc, &bytes, &n_pool));
-        CU(cudaLibraryGetGlobal(&e.c_k, &got, e.lib, "c_k"));
-        CU(cudaMemcpy(e.c_k, pc, sizeof(double) * n_pool, cudaMemcpyHostToDevice));
+        if (!sweep) {
+            CU(cudaLibraryGetGlobal(&e.c_k, &got, e.lib, "c_k"));
+            CU(cudaMemcpy(e.c_k, pc, sizeof(double) * n_pool, cudaMemcpyHostToDevice));
+        }
         CU(cudaLibraryGetGlobal(&e.c_x0, &got, e.lib, "c_x0"));
         CU(cudaMemcpy(e.c_x0, pc + n_pool, sizeof(double) * m.S, cudaMemcpyHostToDevice));
     }
@@ -671,28 +723,50 @@ static ssa_status reduce_partials(ssa_tree_in in, ssa_u64 count, ssa_u64 rows, c
     return SSA_OK;
 }
 
+// Parameter sweep ("a set of parameter-swept simulations"):
+// P points of N trajectories each, point p's constants in row p of L.values.
+// The run covers virtual ids p * N + i; a chunk holds whole points.
+struct SweepSpec {
+    int P = 0;
+    ssa_u64 N = 0;
+    PoolLayout L;
+    std::vector<RangeOut> roots;   // per point
+};
+
 static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end, double t_end, double dt,
                             uint64_t seed, const ssa_run_options* o, Ctx& c, RangeOut root, RunInfo& info,
-                            const ssa_dump* dump, bool dump_on_device)
+                            const ssa_dump* dump, bool dump_on_device, const SweepSpec* sw = nullptr)
 {
     const long long K = grid_K(t_end, dt);
     const ssa_u64 G = (ssa_u64)K + 1, S = (ssa_u64)m->S, cells = G * S;
     const ssa_u64 n_ids = id_end - id_begin;
     const ssa_u64 span = next_pow2(n_ids);
-    // chunk size: a power of two (aligned subtree), staging within the budget
     const ssa_u64 budget = (o && o->staging_budget_bytes) ? o->staging_budget_bytes : (32ull << 30);
-    ssa_u64 C = span;
-    if (o && o->chunk) {
-        if (o->chunk & (o->chunk - 1)) return fail(SSA_ERR_INVALID_ARG, "chunk %llu is not a power of two", (unsigned long long)o->chunk);
-        C = std::min<ssa_u64>(span, o->chunk);
-    }
-    while (C > 1 && C * cells * 4ull > budget) C >>= 1;
-    const ssa_u64 n_chunks = (n_ids + C - 1) / C;
-
     int path = o ? o->path : SSA_PATH_AUTO;
     if (path == SSA_PATH_AUTO) path = (m->R <= 64) ? SSA_PATH_THREAD : SSA_PATH_WARP;
     if (path != SSA_PATH_THREAD && path != SSA_PATH_WARP) return fail(SSA_ERR_INVALID_ARG, "bad path %d", path);
     info.path = path;
+    ssa_u64 C = span;
+    if (sw) {
+        // chunk = as many whole sweep points as the staging budget and the
+        // shared-memory constant rows (<= 32 KiB) allow
+        if (path != SSA_PATH_THREAD) return fail(SSA_ERR_UNSUPPORTED, "parameter sweeps run on the thread path");
+        const ssa_u64 per_point = sw->N * cells * 4ull;
+        ssa_u64 pts = std::min<ssa_u64>((ssa_u64)sw->P, budget / per_point);
+        pts = std::min<ssa_u64>(pts, (32768 / 8) / (ssa_u64)sw->L.n);
+        if (pts == 0)
+            return fail(SSA_ERR_UNSUPPORTED, "sweep point staging (%llu B) exceeds the staging budget",
+                        (unsigned long long)per_point);
+        C = pts * sw->N;
+    } else {
+        // chunk size: a power of two (aligned subtree), staging within the budget
+        if (o && o->chunk) {
+            if (o->chunk & (o->chunk - 1)) return fail(SSA_ERR_INVALID_ARG, "chunk %llu is not a power of two", (unsigned long long)o->chunk);
+            C = std::min<ssa_u64>(span, o->chunk);
+        }
+        while (C > 1 && C * cells * 4ull > budget) C >>= 1;
+    }
+    const ssa_u64 n_chunks = (n_ids + C - 1) / C;
 
     int sms = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
@@ -709,7 +783,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // blocks_per_sm > 0 also sets the K1 variant's __launch_bounds__ residency
             // target (its register budget is 64K / (block * blocks_per_sm))
             const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : default_minb(*m, block);
-            TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, &k1, &info.jit_ms));
+            TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
@@ -737,21 +811,31 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             std::lock_guard<std::mutex> lk(m->mu);
             TRY(pinned_constants(*m, &pc, &bytes, &n_pool));
         }
-        CU(cudaMemcpyAsync(k1->c_k, pc, 8 * n_pool, cudaMemcpyHostToDevice, st));
+        if (!sw) {
+            CU(cudaMemcpyAsync(k1->c_k, pc, 8 * n_pool, cudaMemcpyHostToDevice, st));
+            info.h2d += 8 * n_pool;
+        }
         CU(cudaMemcpyAsync(k1->c_x0, pc + n_pool, 8 * (size_t)m->S, cudaMemcpyHostToDevice, st));
-        info.h2d += bytes;
+        info.h2d += 8 * (size_t)m->S;
     } else {
         CU(cudaMemcpyAsync(k2->dev_image, k2->host_image, k2->image_bytes, cudaMemcpyHostToDevice, st));
         info.h2d += k2->image_bytes;
     }
 
     // buffers
-    DevBuf staging, tiles, croots, statsb, work, dids, dstates, de, dt_, dsum;
-    const ssa_u64 stride = C;
-    CU(staging.alloc(sizeof(int) * C * cells, st));
-    const ssa_u64 n_tiles = (C + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
+    DevBuf staging, tiles, croots, statsb, work, dids, dstates, de, dt_, dsum, pconst;
+    const ssa_u64 stride = sw ? (C + 3) / 4 * 4 : C;     // rows 16-byte aligned for the vector loads of K3
+    CU(staging.alloc(sizeof(int) * stride * cells, st));
+    const ssa_u64 seg = sw ? sw->N : C;                   // ids per reduced segment (a point, or the chunk)
+    const ssa_u64 n_tiles = (seg + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
     if (n_tiles > 1) CU(tiles.alloc(sizeof(double) * 3 * cells * n_tiles, st));
-    if (n_chunks > 1) CU(croots.alloc(sizeof(double) * 3 * cells * n_chunks, st));
+    if (n_chunks > 1 && !sw) CU(croots.alloc(sizeof(double) * 3 * cells * n_chunks, st));
+    if (sw) {
+        CU(pconst.alloc(sizeof(double) * sw->L.values.size(), st));
+        CU(cudaMemcpyAsync(pconst.p, sw->L.values.data(), sizeof(double) * sw->L.values.size(),
+                           cudaMemcpyHostToDevice, st));
+        info.h2d += sizeof(double) * sw->L.values.size();
+    }
     CU(statsb.alloc(sizeof(ssa_dev_stats), st));
     CU(work.alloc(sizeof(ssa_u64) * n_chunks, st));
     CU(cudaMemsetAsync(statsb.p, 0, sizeof(ssa_dev_stats), st));
@@ -809,8 +893,16 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             }
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
             p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
+            size_t smem = 0;
+            if (sw) {
+                p.n_per_point = sw->N;
+                p.n_pts = (int)(cn / sw->N);
+                p.n_pool = sw->L.n;
+                p.pconst = pconst.as<double>() + (cb / sw->N) * (ssa_u64)sw->L.n;
+                smem = sizeof(double) * (size_t)p.n_pts * (size_t)p.n_pool;
+            }
             void* args[] = {&p};
-            CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(block), args, 0, st));
+            CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(block), args, smem, st));
             info.launches += 1;
         } else {
             ssa_k2_params p{};
@@ -826,22 +918,32 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         }
         CU(cudaGetLastError());
         CU(cudaEventRecord(evs1, st));
-        // a9: chunk reduce -> chunk root (or the range root when there is one chunk)
-        ssa_tree_out chunk_out;
-        if (n_chunks > 1) {
-            double* b = croots.as<double>();
-            chunk_out = ssa_tree_out{b, b + cells * n_chunks, b + 2 * cells * n_chunks, n_chunks, 0, ch};
-        } else {
-            chunk_out = ssa_tree_out{root.n, root.mean, root.m2, 1, 0, 0};
-        }
-        if (n_tiles > 1) {
-            double* b = tiles.as<double>();
-            ssa_tree_out to{b, b + cells * n_tiles, b + 2 * cells * n_tiles, n_tiles, 1, 0};
-            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, to, st, &info.launches));
-            TRY(reduce_partials(ssa_tree_in{to.n, to.mean, to.m2, n_tiles, 1}, n_tiles, cells, chunk_out, st,
-                                &info.launches));
-        } else {
-            CU(ssa_tree_leaf_launch(staging.as<int>(), stride, cn, cells, chunk_out, st, &info.launches));
+        // a9: reduce each segment (the chunk, or each sweep point in it) to its
+        // root: the chunk root, the range root when there is one chunk, or the
+        // point's root
+        const ssa_u64 n_seg = sw ? cn / sw->N : 1;
+        for (ssa_u64 q = 0; q < n_seg; ++q) {
+            const ssa_u64 sn = sw ? sw->N : cn;
+            const int* src = staging.as<int>() + q * seg;
+            ssa_tree_out seg_out;
+            if (sw) {
+                const RangeOut& pr = sw->roots[(size_t)(cb / sw->N + q)];
+                seg_out = ssa_tree_out{pr.n, pr.mean, pr.m2, 1, 0, 0};
+            } else if (n_chunks > 1) {
+                double* b = croots.as<double>();
+                seg_out = ssa_tree_out{b, b + cells * n_chunks, b + 2 * cells * n_chunks, n_chunks, 0, ch};
+            } else {
+                seg_out = ssa_tree_out{root.n, root.mean, root.m2, 1, 0, 0};
+            }
+            if (n_tiles > 1) {
+                double* b = tiles.as<double>();
+                ssa_tree_out to{b, b + cells * n_tiles, b + 2 * cells * n_tiles, n_tiles, 1, 0};
+                CU(ssa_tree_leaf_launch(src, stride, sn, cells, to, st, &info.launches));
+                TRY(reduce_partials(ssa_tree_in{to.n, to.mean, to.m2, n_tiles, 1}, n_tiles, cells, seg_out, st,
+                                    &info.launches));
+            } else {
+                CU(ssa_tree_leaf_launch(src, stride, sn, cells, seg_out, st, &info.launches));
+            }
         }
         CU(cudaEventRecord(evr1, st));
         CU(cudaEventSynchronize(evr1));
@@ -853,7 +955,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         info.reduce_bytes += cn * cells * sizeof(int);
     }
     // a10 (per GPU): chunk roots -> range root
-    if (n_chunks > 1) {
+    if (n_chunks > 1 && !sw) {
         double* b = croots.as<double>();
         TRY(reduce_partials(ssa_tree_in{b, b + cells * n_chunks, b + 2 * cells * n_chunks, n_chunks, 1}, n_chunks, cells,
                             ssa_tree_out{root.n, root.mean, root.m2, 1, 0, 0}, st, &info.launches));
@@ -985,6 +1087,61 @@ extern "C" ssa_status ssa_run_shard(const ssa_model* m, uint64_t id_begin, uint6
     return fill_result(info, r);
 }
 
+extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const double* rates, const double* mod_coefs,
+                                    uint64_t n_per_point, double t_end, double sample_dt, uint64_t seed,
+                                    uint32_t reducers, const ssa_run_options* o, ssa_result* r)
+{
+    TRY(check_common(m, t_end, sample_dt, r));
+    if (n_points < 1 || n_points > 65536) return fail(SSA_ERR_INVALID_ARG, "n_points must be in [1, 65536]");
+    if (!rates) return fail(SSA_ERR_INVALID_ARG, "rates is null");
+    if (n_per_point == 0) return fail(SSA_ERR_INVALID_ARG, "n_per_point must be >= 1");
+    if ((ssa_u64)n_points * n_per_point > (1ull << 40)) return fail(SSA_ERR_INVALID_ARG, "n_points * n_per_point > 2^40");
+    if (o && o->path == SSA_PATH_WARP) return fail(SSA_ERR_UNSUPPORTED, "parameter sweeps run on the thread path");
+    const size_t R = (size_t)m->R;
+    for (size_t i = 0; i < (size_t)n_points * R; ++i) {
+        if (!std::isfinite(rates[i]) || rates[i] < 0.0)
+            return fail(SSA_ERR_MODEL, "sweep point %zu, reaction %zu: rate must be finite and >= 0", i / R, i % R);
+        if (mod_coefs && !std::isfinite(mod_coefs[i]))
+            return fail(SSA_ERR_MODEL, "sweep point %zu, reaction %zu: non-finite modifier coefficient", i / R, i % R);
+    }
+    Ctx c;
+    TRY(setup_ctx(o, c));
+    const ssa_u64 cells = ssa_grid_size(t_end, sample_dt) * (ssa_u64)m->S;
+    SweepSpec sw;
+    sw.P = n_points;
+    sw.N = n_per_point;
+    sw.L = make_pool(*m, n_points, rates, mod_coefs);
+    DevBuf rootb;
+    CU(rootb.alloc(sizeof(double) * 3 * cells * (size_t)n_points, c.st));
+    double* rb = rootb.as<double>();
+    for (int p = 0; p < n_points; ++p) {
+        double* b = rb + (size_t)p * 3 * cells;
+        sw.roots.push_back(RangeOut{b, b + cells, b + 2 * cells});
+    }
+    RunInfo info;
+    const bool on_dev = o && o->outputs_on_device;
+    TRY(run_range(m, 0, (ssa_u64)n_points * n_per_point, t_end, sample_dt, seed, o, c, sw.roots[0], info,
+                  o ? o->dump : nullptr, on_dev, &sw));
+    ssa_status st = fill_result(info, r);
+    // finalize every point into its [G*S] slab of the caller's arrays
+    for (int p = 0; p < n_points; ++p) {
+        ssa_result rp = *r;
+        const size_t off = (size_t)p * cells;
+        rp.mean = r->mean ? r->mean + off : nullptr;
+        rp.var = r->var ? r->var + off : nullptr;
+        rp.m2 = r->m2 ? r->m2 + off : nullptr;
+        rp.count = r->count ? r->count + off : nullptr;
+        rp.kernel_launches = 0;
+        rp.d2h_bytes = 0;
+        const RangeOut& pr = sw.roots[p];
+        TRY(finalize_to(pr.n, pr.mean, pr.m2, cells, reducers ? reducers : (SSA_REDUCE_MEAN | SSA_REDUCE_VAR), &rp,
+                        on_dev, c.st));
+        r->kernel_launches += rp.kernel_launches;
+        r->d2h_bytes += rp.d2h_bytes;
+    }
+    return st;
+}
+
 extern "C" ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, uint64_t cells,
                                       const ssa_run_options* o, ssa_result* r)
 {
@@ -1019,7 +1176,7 @@ extern "C" ssa_status ssa_model_prepare(const ssa_model* m, int32_t device, int3
     std::lock_guard<std::mutex> lk(m->mu);
     if (path == SSA_PATH_THREAD) {
         K1Entry* e = nullptr;
-        return ensure_k1(*m, c.device, 128, default_minb(*m, 128), false, &e, nullptr);
+        return ensure_k1(*m, c.device, 128, default_minb(*m, 128), false, nullptr, &e, nullptr);
     }
     K2Dev* k = nullptr;
     return ensure_k2(*m, c.device, &k);
@@ -1051,7 +1208,7 @@ extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, in
 {
     static thread_local std::string s;
     if (!m) return "";
-    s = k1_full_source(*m, block, minb, dump != 0);
+    s = k1_full_source(*m, block, minb, dump != 0, nullptr);
     return s.c_str();
 }
 
@@ -1061,7 +1218,7 @@ extern "C" ssa_status ssa_debug_k1_compile(const ssa_model* m, int32_t block, in
     if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
     std::vector<char> cubin;
     std::string lg;
-    ssa_status st = nvrtc_compile(k1_full_source(*m, block, minb, dump != 0), cubin, lg);
+    ssa_status st = nvrtc_compile(k1_full_source(*m, block, minb, dump != 0, nullptr), cubin, lg);
     if (log && log_cap) {
         std::string all = (st == SSA_OK) ? lg : g_err;
         strncpy(log, all.c_str(), (size_t)log_cap - 1);

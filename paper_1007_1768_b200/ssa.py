@@ -97,6 +97,9 @@ def lib():
         L.ssa_run_shard.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_double, C.c_double, C.c_uint64,
                                     C.c_void_p, P(ssa_run_options), P(ssa_result)]
         L.ssa_run_shard.restype = C.c_int
+        L.ssa_run_sweep.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_double), C.c_uint64, C.c_double,
+                                    C.c_double, C.c_uint64, C.c_uint32, P(ssa_run_options), P(ssa_result)]
+        L.ssa_run_sweep.restype = C.c_int
         L.ssa_merge_roots.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, P(ssa_run_options), P(ssa_result)]
         L.ssa_merge_roots.restype = C.c_int
         L.ssa_model_prepare.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
@@ -245,6 +248,36 @@ def run(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed:
     r = ssa_result()
     r.mean, r.var, r.m2, r.count = mean.ctypes.data, var.ctypes.data, m2.ctypes.data, count.ctypes.data
     st = lib().ssa_run(model.handle, n_trajectories, t_end, sample_dt, seed, reducers, C.byref(o), C.byref(r))
+    if st != SSA_OK and (raise_on_error or st not in (3, 4)):
+        _check(st)
+    return _result_from(r, st, mean, var, m2, count, dump)
+
+
+def run_sweep(model: Model, rates, n_per_point: int, t_end: float, sample_dt: float, seed: int, *,
+              mod_coefs=None, reducers: int = SSA_REDUCE_MEAN | SSA_REDUCE_VAR, dump_ids=None,
+              raise_on_error: bool = True, **opts) -> RunResult:
+    """ssa_run_sweep: `rates` is [n_points, R] (and `mod_coefs`, if given);
+    returns mean/var/m2/count as [n_points, G, S] numpy arrays.  Dump ids are
+    virtual ids p * n_per_point + i."""
+    rates = np.ascontiguousarray(np.asarray(rates, dtype=np.float64))
+    assert rates.ndim == 2 and rates.shape[1] == model.R
+    P = rates.shape[0]
+    mc = None
+    if mod_coefs is not None:
+        mc = np.ascontiguousarray(np.asarray(mod_coefs, dtype=np.float64))
+        assert mc.shape == rates.shape
+    G = grid_size(t_end, sample_dt)
+    S = model.S
+    mean, var, m2, count = (np.zeros((P, G, S)) for _ in range(4))
+    dump = cdump = None
+    if dump_ids is not None and len(dump_ids):
+        dump, cdump = _make_dump(dump_ids, G, S)
+    o = _options(dump=cdump, **opts)
+    r = ssa_result()
+    r.mean, r.var, r.m2, r.count = mean.ctypes.data, var.ctypes.data, m2.ctypes.data, count.ctypes.data
+    dp = C.POINTER(C.c_double)
+    st = lib().ssa_run_sweep(model.handle, P, rates.ctypes.data_as(dp), mc.ctypes.data_as(dp) if mc is not None else None,
+                             n_per_point, t_end, sample_dt, seed, reducers, C.byref(o), C.byref(r))
     if st != SSA_OK and (raise_on_error or st not in (3, 4)):
         _check(st)
     return _result_from(r, st, mean, var, m2, count, dump)

@@ -33,7 +33,7 @@ def _declared_functions():
 
 def test_header_symbols_exported(ssa):
     names = _declared_functions()
-    assert {"ssa_model_create", "ssa_run", "ssa_run_shard", "ssa_merge_roots", "ssa_grid_size",
+    assert {"ssa_model_create", "ssa_run", "ssa_run_shard", "ssa_run_sweep", "ssa_merge_roots", "ssa_grid_size",
             "ssa_status_string", "ssa_last_error"} <= set(names)
     out = subprocess.run(["nm", "-D", "--defined-only", ssa.LIB_PATH], stdout=subprocess.PIPE, text=True,
                          check=True).stdout
@@ -126,3 +126,17 @@ def test_shard_bounds_are_aligned_subtrees(ssa):
                     assert b % span == 0
                     covered.extend(range(b, e))
             assert covered == list(range(n))
+
+
+def test_sweep_validation_without_device(ssa):
+    """ssa_run_sweep validates its parameter points before touching a device."""
+    net = inputs.immigration_death()
+    m = ssa.Model(net)
+    bad = inputs.rate_matrix(net, [1], [0.1, -1.0])
+    with pytest.raises(ssa.SSAError) as ei:
+        ssa.run_sweep(m, bad, 10, 5.0, 1.0, 1)
+    assert ei.value.status == 2
+    nan = inputs.rate_matrix(net, [0], [float("nan")])
+    with pytest.raises(ssa.SSAError) as ei:
+        ssa.run_sweep(m, nan, 10, 5.0, 1.0, 1)
+    assert ei.value.status == 2
