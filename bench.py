@@ -177,6 +177,55 @@ def run_reference(args, rank, world):
     return 0
 
 
+# ---------------------------------------------------------------- sweep workload
+def run_sweep_bench(args, rank, world):
+    """The paper's delta_t sensitivity sweep (Fig. 4 panels 2-4)
+    as one ssa_run_sweep: 3 points x (config-2 trajectories / 3) over config 2's
+    horizon, on one GPU.  Device time by CUDA events on the run's stream."""
+    if world != 1:
+        print(json.dumps({"error": "the sweep workload runs on one GPU"}))
+        return 1
+    import torch
+
+    import inputs
+    from paper_1007_1768_b200 import build as B
+    B.build()
+    from paper_1007_1768_b200 import ssa as S
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    net, rates = inputs.hiv_delta_t_sweep()
+    cfg = inputs.config(2)
+    n_per = (args.n_per_gpu or cfg.n_trajectories) // len(rates)
+    t_end = args.t_end or cfg.t_end
+    m = S.Model(net)
+    l2 = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        S.run_sweep(m, rates, n_per, t_end, cfg.dt, cfg.seed, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    events, launches = 0, 0
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            l2.zero_()
+            r = S.run_sweep(m, rates, n_per, t_end, cfg.dt, cfg.seed, stream=stream.cuda_stream)
+            events += r.events
+            launches += r.kernel_launches
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    line = {"metric": "ssa_events_per_s", "value": events / (ms / 1e3), "unit": "events/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "fig4-delta-t-sweep", "model": net.name, "points": [float(v) for v in rates[:, 5]],
+                       "swept_reaction": 6, "n_trajectories_per_point": n_per, "t_end": t_end, "sample_dt": cfg.dt,
+                       "seed": cfg.seed, "path": "thread", "l2": "flushed between steps (256 MiB write)"},
+            "trajectories_per_s": len(rates) * n_per * args.steps / (ms / 1e3),
+            "events_per_step": events / args.steps, "gpu_launches": launches, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -192,6 +241,8 @@ def main():
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="config", choices=["config", "sweep"],
+                    help="sweep: the Fig. 4 delta_t sensitivity sweep (ssa_run_sweep, 1 GPU)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -199,6 +250,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.workload == "sweep":
+        return run_sweep_bench(args, rank, world)
 
     import numpy as np
     import torch
