@@ -1,320 +1,16 @@
 // kernels.cu -- nvcc-compiled kernels of the ensemble-SSA hot path (sm_100a):
-//   K2  ssa_k2<P>      one trajectory per warp (networks with hundreds of
-//                      reactions): lane-contiguous propensity blocks, a
-//                      Hillis-Steele warp scan, ballot/ffs selection, state in
-//                      shared memory, RNG amortised 32 events per lane
-//                      (north_star (a)), order R13.
 //   K3  ssa_tree_leaf  canonical-tree Welford reduction of a chunk's staged
 //                      grid samples (a9, no atomics: north_star (d)).
 //   K4  ssa_tree_merge merge of partial roots (tiles -> chunk -> shard -> GPUs)
 //       ssa_finalize   mean, population variance = M2/n (a10).
-// K1 (thread path) is model-specialised and compiled by NVRTC (jit.cpp).
+// K1 (thread path, k1_thread.cuh) and K2 (warp path, k2_warp.cuh) are
+// model-specialised and compiled by NVRTC at run time (runtime.cu).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "ssa_device.cuh"
 #include "ssa_kernels.h"
 
-__constant__ double k2_plog[14] = SSA_PLOG_COEF_INIT;
-
-// =========================================================================
-// K2: warp per trajectory
-// =========================================================================
-// Propensities live in shared memory, laid out [q][lane] for the lane-
-// contiguous blocks j = lane*P + q (conflict-free), and after each event only
-// the reactions that read a changed species are recomputed (dependency graph,
-// a_j is a pure function of x, so the cached values are
-// bit-identical to a full recompute).  The summation order is the warp32
-// order of DESIGN.md §2.
-//
-// Packed reaction word (see ensure_k2 in runtime.cu):
-//   bits [0,2) n_reac; term q: species [2+16q, 16+16q), coef [16+16q, 18+16q);
-//   bits [50,64) modifier species (0x3FFF = none).
-struct k2_rx {
-    ssa_u64 pk;
-    double rate;
-    double modc;
-};
-
-// C(x, m) for m in {1, 2}; m == 3 is rare and branches.
-static __device__ __forceinline__ double k2_factor(double x, int m)
-{
-    const double x1 = __dmul_rn(x, __dadd_rn(x, -1.0));
-    double f = (m == 1) ? x : __dmul_rn(x1, 0.5);
-    if (m == 3) f = __ddiv_rn(__dmul_rn(x1, __dadd_rn(x, -2.0)), 6.0);
-    return f;
-}
-
-static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const double* __restrict__ x)
-{
-    const ssa_u64 pk = q.pk;
-    const int n = (int)(pk & 3ull);
-    double h = 1.0;
-    if (n >= 1) h = k2_factor(x[(int)((pk >> 2) & 0x3FFF)], (int)((pk >> 16) & 3));
-    if (n >= 2) h = __dmul_rn(h, k2_factor(x[(int)((pk >> 18) & 0x3FFF)], (int)((pk >> 32) & 3)));
-    if (n >= 3) h = __dmul_rn(h, k2_factor(x[(int)((pk >> 34) & 0x3FFF)], (int)((pk >> 48) & 3)));
-    double k = q.rate;
-    const int ms = (int)(pk >> 50);
-    if (ms != 0x3FFF) {
-        k = __dadd_rn(k, __dmul_rn(q.modc, x[ms]));
-        k = (k < 0.0) ? 0.0 : k;
-    }
-    return (n == 0) ? k : __dmul_rn(k, h);
-}
-
-size_t ssa_k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
-{
-    const size_t warps = (size_t)(block / 32);
-    return sizeof(k2_rx) * (size_t)R + sizeof(double) * (size_t)S                    // tables, x0
-           + warps * sizeof(double) * ((size_t)S + 32 * (size_t)P)                    // x, a per warp
-           + sizeof(int) * ((size_t)R + 1 + n_ent + (size_t)S + 1 + n_dep);           // nu, dep CSR
-}
-
-template <int PMAX>
-__global__ void __launch_bounds__(SSA_K2_BLOCK, 4) ssa_k2(const ssa_k2_params P)
-{
-    extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    const int S = P.S, R = P.R, Pl = P.P;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const int nwarps = blockDim.x >> 5;
-    const unsigned FULL = 0xffffffffu;
-    // shared layout: rx[R] | x0[S] | (x[S] | a[32 P]) per warp | nu_off[R+1] | nu_ent | dep_off[S+1] | dep_ent
-    k2_rx* rx = (k2_rx*)k2_smem_raw;
-    double* x0 = (double*)(rx + R);
-    double* wbase = x0 + S;
-    double* x = wbase + (size_t)warp * (S + 32 * Pl);
-    double* a = x + S;                                   // a[q*32 + l] = propensity of j = l*P + q
-    int* nu_off = (int*)(wbase + (size_t)nwarps * (S + 32 * Pl));
-    int* nu_ent = nu_off + (R + 1);
-    int* dep_off = nu_ent + P.n_ent;
-    int* dep_ent = dep_off + (S + 1);
-    for (int i = threadIdx.x; i < R; i += blockDim.x) {
-        k2_rx q;
-        q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i];
-        rx[i] = q;
-    }
-    for (int i = threadIdx.x; i < S; i += blockDim.x) x0[i] = P.x0[i];
-    for (int i = threadIdx.x; i <= R; i += blockDim.x) nu_off[i] = P.nu_off[i];
-    for (int i = threadIdx.x; i < P.n_ent; i += blockDim.x) nu_ent[i] = P.nu_ent[i];
-    for (int i = threadIdx.x; i <= S; i += blockDim.x) dep_off[i] = P.dep_off[i];
-    for (int i = threadIdx.x; i < P.n_dep; i += blockDim.x) dep_ent[i] = P.dep_ent[i];
-    __syncthreads();
-
-    const double INF = __longlong_as_double(0x7FF0000000000000ll);
-    const double dt = P.dt;
-    const long long K = P.K;
-    const ssa_u64 G = (ssa_u64)K + 1;
-    ssa_u64 my_events = 0, my_ties = 0;
-
-    for (;;) {
-        ssa_u64 rel = 0;
-        if (lane == 0) rel = atomicAdd(P.work, 1ull);
-        rel = __shfl_sync(FULL, rel, 0);
-        if (rel >= P.n_ids) break;
-        const ssa_u64 id = P.id_begin + rel;
-        const long long slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
-        for (int s = lane; s < S; s += 32) x[s] = x0[s];
-        __syncwarp();
-        // a3 at the initial state: every propensity of this lane's block
-#pragma unroll
-        for (int q = 0; q < PMAX; ++q) {
-            if (q < Pl) {
-                const int j = lane * Pl + q;
-                a[q * 32 + lane] = (j < R) ? k2_propensity(rx[j], x) : 0.0;
-            }
-        }
-        __syncwarp();
-
-        double t = 0.0, s_next = 0.0;
-        ssa_u64 e = 0, hash = SSA_FNV_OFFSET, ties = 0;
-        long long k = 0;
-        int status = 0, absorbed = 0, err_r = -1;
-        const ssa_u32 idlo = (ssa_u32)id, idhi = (ssa_u32)(id >> 32);
-        double Ec = 0.0, U2c = 0.0;
-
-        for (;;) {
-            // a2, amortised: lane l draws event e0 + l for the next 32 events
-            if ((e & 31ull) == 0) {
-                const ssa_u64 ee = e + (ssa_u64)lane;
-                const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)ee, (ssa_u32)(ee >> 32), idlo, idhi,
-                                                           P.key0, P.key1);
-                Ec = -ssa_plog(ssa_u53(o.o1, o.o0), k2_plog);
-                U2c = ssa_u53(o.o3, o.o2);
-            }
-            // a4: lane sum (sequential over the lane's block), then warp scan
-            double L = 0.0;
-#pragma unroll
-            for (int q = 0; q < PMAX; ++q)
-                if (q < Pl) L = __dadd_rn(L, a[q * 32 + lane]);
-            double v = L;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(FULL, v, o);
-                if (lane >= o) v = __dadd_rn(y, v);
-            }
-            const double a0 = __shfl_sync(FULL, v, 31);
-            // a5
-            const int src = (int)(e & 31ull);
-            const double E = __shfl_sync(FULL, Ec, src);
-            const double u2 = __shfl_sync(FULL, U2c, src);
-            double tn;
-            if (a0 > 0.0 && a0 < INF) {
-                tn = __dadd_rn(t, ssa_div_tau(E, a0));
-            } else if (a0 == 0.0) {
-                tn = INF;
-                absorbed = 1;
-            } else {
-                status = 1;
-                int bad = R;   // first reaction with a non-finite propensity
-#pragma unroll
-                for (int q = PMAX - 1; q >= 0; --q)
-                    if (q < Pl && lane * Pl + q < R && !(fabs(a[q * 32 + lane]) < INF)) bad = lane * Pl + q;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(FULL, bad, o));
-                err_r = bad < R ? bad : -1;
-                break;
-            }
-            // a6 (warp-uniform)
-            if (tn > s_next) {
-                do {
-                    const double tol = __dmul_rn(1e-9, s_next);
-                    const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
-                                      (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
-                    ties += near ? 1 : 0;
-                    int ovf = 0;
-                    for (int s = lane; s < S; s += 32) {
-                        const double xv = x[s];
-                        ovf |= (xv > 2147483647.0) ? 1 : 0;
-                        P.staging[((ssa_u64)k * S + s) * P.stride + rel] = (int)xv;
-                        if (slot >= 0) P.dump_states[((ssa_u64)slot * G + (ssa_u64)k) * S + s] = (int)xv;
-                    }
-                    if (__any_sync(FULL, ovf)) status = 2;
-                    if (slot >= 0 && lane == 0) {
-                        P.dump_e[(ssa_u64)slot * G + (ssa_u64)k] = e;
-                        P.dump_t[(ssa_u64)slot * G + (ssa_u64)k] = (e > 0) ? t : 0.0;
-                    }
-                    ++k;
-                    s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
-                } while (tn > s_next);
-                if (k > K) break;
-            }
-            // a7: lane* = first lane whose inclusive prefix exceeds r
-            const double r = __dmul_rn(u2, a0);
-            const unsigned mask = __ballot_sync(FULL, v > r);
-            const int ls = __ffs(mask) - 1;
-            const double vprev = __shfl_up_sync(FULL, v, 1);
-            int j = -1;
-            if (lane == ls) {
-                double p = (lane > 0) ? vprev : 0.0;
-                for (int q = 0; q < Pl; ++q) {
-                    p = __dadd_rn(p, a[q * 32 + lane]);
-                    if (p > r) { j = lane * Pl + q; break; }
-                }
-                if (j < 0)
-                    for (int q = Pl - 1; q >= 0; --q)
-                        if (a[q * 32 + lane] > 0.0) { j = lane * Pl + q; break; }
-            }
-            j = __shfl_sync(FULL, j, ls);
-            if (j < 0) {
-                // rounding fallback: last positive propensity in an earlier lane
-                int lp = -1;
-                for (int q = 0; q < Pl; ++q)
-                    if (a[q * 32 + lane] > 0.0) lp = lane * Pl + q;
-                const unsigned m2 = __ballot_sync(FULL, lp >= 0 && lane < ls);
-                j = __shfl_sync(FULL, lp, 31 - __clz(m2));
-            }
-            // a8: state update
-            const int nb = nu_off[j], ne = nu_off[j + 1];
-            for (int q = nb + lane; q < ne; q += 32) {
-                const int ent = nu_ent[q];
-                const int sp = ent & 0xFFFF;
-                x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));   // arithmetic shift: signed delta
-            }
-            __syncwarp();
-            // a3 for the reactions that read a changed species (lane t takes
-            // the t-th entry of the concatenated dependency lists)
-            int T = 0;
-            for (int q = nb; q < ne; ++q) {
-                const int sp = nu_ent[q] & 0xFFFF;
-                T += dep_off[sp + 1] - dep_off[sp];
-            }
-            for (int base = 0; base < T; base += 32) {
-                int rem = base + lane, jj = -1;
-                for (int q = nb; q < ne; ++q) {
-                    const int sp = nu_ent[q] & 0xFFFF;
-                    const int o = dep_off[sp], len = dep_off[sp + 1] - o;
-                    if (rem >= 0 && rem < len) jj = dep_ent[o + rem];
-                    rem -= len;
-                }
-                if (jj >= 0) {
-                    const int l = jj / Pl, q = jj - l * Pl;
-                    a[q * 32 + l] = k2_propensity(rx[jj], x);
-                }
-            }
-            __syncwarp();
-            t = tn;
-            ++e;
-            hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            my_events += e;
-            my_ties += ties;
-            if (slot >= 0) {
-                ssa_dev_summary sm;
-                sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
-                sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
-                sm.err_reaction = err_r; sm.pad = 0;
-                P.dump_sum[slot] = sm;
-            }
-            if (status) {
-                const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
-                atomicAdd(&P.stats->n_errors, 1ull);
-                atomicOr(&P.stats->err_code, code);
-                const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
-                atomicMin(&P.stats->first_err_id, packed);
-            }
-        }
-    }
-    if (lane == 0) {
-        atomicAdd(&P.stats->events, my_events);
-        if (my_ties) atomicAdd(&P.stats->near_ties, my_ties);
-    }
-}
-
-static const void* k2_fn(int pmax)
-{
-    switch (pmax) {
-    case 1: return (const void*)ssa_k2<1>;
-    case 2: return (const void*)ssa_k2<2>;
-    case 4: return (const void*)ssa_k2<4>;
-    case 8: return (const void*)ssa_k2<8>;
-    case 16: return (const void*)ssa_k2<16>;
-    default: return nullptr;
-    }
-}
-
-cudaError_t ssa_k2_launch(const ssa_k2_params& p, int grid, int block, cudaStream_t st)
-{
-    const size_t smem = ssa_k2_smem_bytes(p.S, p.R, p.P, p.n_ent, p.n_dep, block);
-    const void* fn = k2_fn(p.PMAX);
-    if (!fn) return cudaErrorInvalidValue;
-    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    void* args[] = {(void*)&p};
-    return cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, st);
-}
-
-int ssa_k2_max_blocks_per_sm(int pmax, int block, size_t smem)
-{
-    int n = 0;
-    const void* fn = k2_fn(pmax);
-    if (!fn) return 0;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, block, smem) != cudaSuccess) return 0;
-    return n;
-}
 
 // =========================================================================
 // K3/K4: canonical-tree Welford reduction (no atomics)

@@ -75,9 +75,16 @@ struct K1Entry {
     std::string log;
 };
 
+struct K2Kernel {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t fn = nullptr;
+    size_t smem = 0;
+    int blocks_per_sm = 0;
+};
+
 struct K2Dev {
     bool ready = false;
-    int P = 0, PMAX = 0, n_ent = 0;
+    int P = 0, n_ent = 0, n_dep = 0;
     void* dev_image = nullptr;   // one device block holding the tables below
     void* host_image = nullptr;  // its page-locked host image
     size_t image_bytes = 0;
@@ -85,7 +92,7 @@ struct K2Dev {
     double *rate = nullptr, *modc = nullptr, *x0 = nullptr;
     int *nu_off = nullptr, *nu_ent = nullptr;
     int *dep_off = nullptr, *dep_ent = nullptr;
-    int n_dep = 0;
+    std::map<std::string, K2Kernel> kern;   // "block/dump" -> NVRTC-compiled K2
 };
 
 struct DevCache {
@@ -189,6 +196,8 @@ extern "C" void ssa_model_destroy(ssa_model* m)
             K2Dev& k = kv.second.k2;
             if (k.dev_image) cudaFree(k.dev_image);
             if (k.host_image) cudaFreeHost(k.host_image);
+            for (auto& e : k.kern)
+                if (e.second.lib) cudaLibraryUnload(e.second.lib);
             for (auto& e : kv.second.k1)
                 if (e.second.lib) cudaLibraryUnload(e.second.lib);
         }
@@ -528,95 +537,144 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
 
 // requires: current device == dev, m.mu held.  The K2 tables live in one
 // device block whose image is kept in page-locked host memory; every run
-// re-uploads it (the run's model inputs) with one async copy.
-static ssa_status ensure_k2(const ssa_model& m, int dev, K2Dev** out)
+// re-uploads it (the run's model inputs) with one async copy.  The kernel
+// itself is NVRTC-compiled per (block, dump) with S, R and P baked in.
+static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
+{
+    const size_t warps = (size_t)(block / 32);
+    return 24 * (size_t)R + 8 * (size_t)S + warps * 8 * ((size_t)S + 32 * (size_t)P) +
+           4 * ((size_t)R + 1 + (size_t)n_ent + (size_t)R + 1 + (size_t)n_dep);
+}
+
+static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump)
+{
+    std::ostringstream o;
+    o << "#define SSA_S " << m.S << "\n#define SSA_R " << m.R << "\n#define SSA_P " << P << "\n#define SSA_K2_BLOCK "
+      << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0) << "\n";
+    o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
+    return o.str();
+}
+
+static std::string k2_full_source(const ssa_model& m, int P, int block, int minb, bool dump)
+{
+    return std::string(kSsaDeviceSrc) + "\n" + gen_k2_model(m, P, block, minb, dump) + "\n" + kK2WarpSrc;
+}
+
+// minb: the __launch_bounds__ residency target (1 = let the compiler use the
+// registers it wants)
+static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bool dump, K2Dev** out,
+                            K2Kernel** kout, double* jit_ms)
 {
     K2Dev& k = m.dev[dev].k2;
-    if (k.ready) {
-        *out = &k;
-        return SSA_OK;
-    }
     const int R = m.R, S = m.S;
-    const int P = std::max(1, (R + 31) / 32);
-    int PMAX = 1;
-    while (PMAX < P) PMAX <<= 1;
-    if (PMAX > 16) return fail(SSA_ERR_UNSUPPORTED, "warp path supports at most 512 reactions (got %d)", R);
-    const size_t R1 = (size_t)std::max(R, 1);
-    std::vector<ssa_u64> pk(R1, 0);
-    std::vector<double> rate(R1, 0.0), modc(R1, 0.0), x0(S);
-    std::vector<int> nu_off(R + 1, 0), nu_ent;
-    for (int j = 0; j < R; ++j) {
-        const RxI& q = m.rx[j];
-        ssa_u64 w = (ssa_u64)q.reac.size();
-        for (size_t t = 0; t < q.reac.size(); ++t) {
-            w |= (ssa_u64)(q.reac[t].first & 0x3FFF) << (2 + 16 * t);
-            w |= (ssa_u64)(q.reac[t].second & 3) << (16 + 16 * t);
+    if (!k.ready) {
+        const int P = std::max(1, (R + 31) / 32);
+        if (P > 16) return fail(SSA_ERR_UNSUPPORTED, "warp path supports at most 512 reactions (got %d)", R);
+        if (S > 16383) return fail(SSA_ERR_UNSUPPORTED, "warp path supports at most 16383 species (got %d)", S);
+        const size_t R1 = (size_t)std::max(R, 1);
+        std::vector<ssa_u64> pk(R1, 0);
+        std::vector<double> rate(R1, 0.0), modc(R1, 0.0), x0(S);
+        std::vector<int> nu_off(R + 1, 0), nu_ent;
+        for (int j = 0; j < R; ++j) {
+            const RxI& q = m.rx[j];
+            ssa_u64 w = (ssa_u64)q.reac.size();
+            for (size_t t = 0; t < q.reac.size(); ++t) {
+                w |= (ssa_u64)(q.reac[t].first & 0x3FFF) << (2 + 16 * t);
+                w |= (ssa_u64)(q.reac[t].second & 3) << (16 + 16 * t);
+            }
+            w |= (ssa_u64)(q.mod_sp >= 0 ? q.mod_sp : 0x3FFF) << 50;
+            pk[j] = w;
+            rate[j] = q.rate;
+            modc[j] = q.mod_coef;
+            for (auto& d : q.nu) {
+                if (d.second < -32768 || d.second > 32767)
+                    return fail(SSA_ERR_UNSUPPORTED, "warp path: reaction %d changes species %d by %lld (|delta| > 32767)",
+                                j, d.first, d.second);
+                nu_ent.push_back((int)(d.first & 0xFFFF) | (int)((unsigned)(int)d.second << 16));
+            }
+            nu_off[j + 1] = (int)nu_ent.size();
         }
-        w |= (ssa_u64)(q.mod_sp >= 0 ? q.mod_sp : 0x3FFF) << 50;
-        pk[j] = w;
-        rate[j] = q.rate;
-        modc[j] = q.mod_coef;
-        for (auto& d : q.nu) {
-            if (d.second < -32768 || d.second > 32767)
-                return fail(SSA_ERR_UNSUPPORTED, "warp path: reaction %d changes species %d by %lld (|delta| > 32767)", j,
-                            d.first, d.second);
-            nu_ent.push_back((int)(d.first & 0xFFFF) | (int)((unsigned)(int)d.second << 16));
+        for (int s2 = 0; s2 < S; ++s2) x0[s2] = (double)m.x0[s2];
+        const int n_ent_real = (int)nu_ent.size();
+        if (nu_ent.empty()) nu_ent.push_back(0);
+        // dependency graph: reaction j -> the reactions whose propensity reads a
+        // species j changes (as a reactant or as the modifier species), unique,
+        // ascending
+        std::vector<std::vector<int>> readers(S);
+        for (int j = 0; j < R; ++j) {
+            const RxI& q = m.rx[j];
+            for (auto& t : q.reac) readers[t.first].push_back(j);
+            if (q.mod_sp >= 0) readers[q.mod_sp].push_back(j);
         }
-        nu_off[j + 1] = (int)nu_ent.size();
+        std::vector<int> dep_off(R + 1, 0), dep_ent;
+        for (int j = 0; j < R; ++j) {
+            std::vector<int> d;
+            for (auto& c : m.rx[j].nu) d.insert(d.end(), readers[c.first].begin(), readers[c.first].end());
+            std::sort(d.begin(), d.end());
+            d.erase(std::unique(d.begin(), d.end()), d.end());
+            dep_ent.insert(dep_ent.end(), d.begin(), d.end());
+            dep_off[j + 1] = (int)dep_ent.size();
+        }
+        const int n_dep_real = (int)dep_ent.size();
+        if (dep_ent.empty()) dep_ent.push_back(0);
+        // image layout (8-byte aligned sections): pk | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
+        const size_t o_pk = 0, o_rate = o_pk + 8 * R1, o_modc = o_rate + 8 * R1, o_x0 = o_modc + 8 * R1;
+        const size_t o_off = o_x0 + 8 * (size_t)std::max(S, 1);
+        const size_t o_ent = o_off + ((4 * nu_off.size() + 7) & ~(size_t)7);
+        const size_t o_doff = o_ent + ((4 * nu_ent.size() + 7) & ~(size_t)7);
+        const size_t o_dent = o_doff + ((4 * dep_off.size() + 7) & ~(size_t)7);
+        const size_t bytes = o_dent + 4 * dep_ent.size();
+        CU(cudaMallocHost(&k.host_image, bytes));
+        char* h = (char*)k.host_image;
+        memcpy(h + o_pk, pk.data(), 8 * R1);
+        memcpy(h + o_rate, rate.data(), 8 * R1);
+        memcpy(h + o_modc, modc.data(), 8 * R1);
+        memcpy(h + o_x0, x0.data(), 8 * (size_t)S);
+        memcpy(h + o_off, nu_off.data(), 4 * nu_off.size());
+        memcpy(h + o_ent, nu_ent.data(), 4 * nu_ent.size());
+        memcpy(h + o_doff, dep_off.data(), 4 * dep_off.size());
+        memcpy(h + o_dent, dep_ent.data(), 4 * dep_ent.size());
+        CU(cudaMalloc(&k.dev_image, bytes));
+        CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
+        char* d = (char*)k.dev_image;
+        k.pk = (ssa_u64*)(d + o_pk);
+        k.rate = (double*)(d + o_rate);
+        k.modc = (double*)(d + o_modc);
+        k.x0 = (double*)(d + o_x0);
+        k.nu_off = (int*)(d + o_off);
+        k.nu_ent = (int*)(d + o_ent);
+        k.dep_off = (int*)(d + o_doff);
+        k.dep_ent = (int*)(d + o_dent);
+        k.image_bytes = bytes;
+        k.P = P;
+        k.n_ent = n_ent_real;
+        k.n_dep = n_dep_real;
+        k.ready = true;
     }
-    for (int s = 0; s < S; ++s) x0[s] = (double)m.x0[s];
-    const int n_ent_real = (int)nu_ent.size();
-    if (nu_ent.empty()) nu_ent.push_back(0);
-    // dependency graph: species -> reactions whose propensity reads it (as a
-    // reactant or as the modifier species), ascending reaction index
-    std::vector<std::vector<int>> deps(S);
-    for (int j = 0; j < R; ++j) {
-        const RxI& q = m.rx[j];
-        for (auto& t : q.reac) deps[t.first].push_back(j);
-        if (q.mod_sp >= 0 && (deps[q.mod_sp].empty() || deps[q.mod_sp].back() != j)) deps[q.mod_sp].push_back(j);
-    }
-    std::vector<int> dep_off(S + 1, 0), dep_ent;
-    for (int s = 0; s < S; ++s) {
-        for (int j : deps[s]) dep_ent.push_back(j);
-        dep_off[s + 1] = (int)dep_ent.size();
-    }
-    const int n_dep_real = (int)dep_ent.size();
-    if (dep_ent.empty()) dep_ent.push_back(0);
-    // image layout (8-byte aligned sections): pk | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
-    const size_t o_pk = 0, o_rate = o_pk + 8 * R1, o_modc = o_rate + 8 * R1, o_x0 = o_modc + 8 * R1;
-    const size_t o_off = o_x0 + 8 * (size_t)S;
-    const size_t o_ent = o_off + ((4 * nu_off.size() + 7) & ~(size_t)7);
-    const size_t o_doff = o_ent + ((4 * nu_ent.size() + 7) & ~(size_t)7);
-    const size_t o_dent = o_doff + ((4 * dep_off.size() + 7) & ~(size_t)7);
-    const size_t bytes = o_dent + 4 * dep_ent.size();
-    CU(cudaMallocHost(&k.host_image, bytes));
-    char* h = (char*)k.host_image;
-    memcpy(h + o_pk, pk.data(), 8 * R1);
-    memcpy(h + o_rate, rate.data(), 8 * R1);
-    memcpy(h + o_modc, modc.data(), 8 * R1);
-    memcpy(h + o_x0, x0.data(), 8 * (size_t)S);
-    memcpy(h + o_off, nu_off.data(), 4 * nu_off.size());
-    memcpy(h + o_ent, nu_ent.data(), 4 * nu_ent.size());
-    memcpy(h + o_doff, dep_off.data(), 4 * dep_off.size());
-    memcpy(h + o_dent, dep_ent.data(), 4 * dep_ent.size());
-    CU(cudaMalloc(&k.dev_image, bytes));
-    CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
-    char* d = (char*)k.dev_image;
-    k.pk = (ssa_u64*)(d + o_pk);
-    k.rate = (double*)(d + o_rate);
-    k.modc = (double*)(d + o_modc);
-    k.x0 = (double*)(d + o_x0);
-    k.nu_off = (int*)(d + o_off);
-    k.nu_ent = (int*)(d + o_ent);
-    k.dep_off = (int*)(d + o_doff);
-    k.dep_ent = (int*)(d + o_dent);
-    k.image_bytes = bytes;
-    k.P = P;
-    k.PMAX = PMAX;
-    k.n_ent = n_ent_real;
-    k.n_dep = n_dep_real;
-    k.ready = true;
     *out = &k;
+    const std::string key = std::to_string(block) + "/" + std::to_string(minb) + "/" + (dump ? "1" : "0");
+    auto it = k.kern.find(key);
+    if (it == k.kern.end()) {
+        auto t0 = std::chrono::steady_clock::now();
+        K2Kernel kk;
+        std::vector<char> cubin;
+        std::string log;
+        TRY(nvrtc_compile(k2_full_source(m, k.P, block, minb, dump), cubin, log));
+        CU(cudaLibraryLoadData(&kk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+        CU(cudaLibraryGetKernel(&kk.fn, kk.lib, "ssa_k2"));
+        kk.smem = k2_smem_bytes(S, R, k.P, k.n_ent, k.n_dep, block);
+        if (kk.smem > 227 * 1024)
+            return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", kk.smem);
+        CU(cudaFuncSetAttribute((const void*)kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kk.smem));
+        int nb = 0;
+        CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)kk.fn, block, kk.smem));
+        if (nb <= 0) return fail(SSA_ERR_CUDA, "warp path: kernel cannot be resident (block %d, smem %zu)", block, kk.smem);
+        kk.blocks_per_sm = nb;
+        auto t1 = std::chrono::steady_clock::now();
+        if (jit_ms) *jit_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        it = k.kern.emplace(key, kk).first;
+    }
+    *kout = &it->second;
     return SSA_OK;
 }
 
@@ -774,6 +832,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     // kernels for this model on this device (JIT on first use)
     K1Entry* k1 = nullptr;
     K2Dev* k2 = nullptr;
+    K2Kernel* k2k = nullptr;
     int block = (o && o->block > 0) ? o->block : (path == SSA_PATH_THREAD ? 128 : SSA_K2_BLOCK);
     if (block % 32 || block > 1024) return fail(SSA_ERR_INVALID_ARG, "block %d must be a multiple of 32 <= 1024", block);
     int grid = 0;
@@ -789,11 +848,9 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             grid = sms * bps;
             grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + block - 1) / block);
         } else {
-            TRY(ensure_k2(*m, c.device, &k2));
-            const size_t smem = ssa_k2_smem_bytes(m->S, m->R, k2->P, k2->n_ent, k2->n_dep, block);
-            if (smem > 227 * 1024) return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", smem);
-            int bps = ssa_k2_max_blocks_per_sm(k2->PMAX, block, smem);
-            if (bps <= 0) return fail(SSA_ERR_CUDA, "warp path: kernel cannot be resident (block %d, smem %zu)", block, smem);
+            const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : 1;
+            TRY(ensure_k2(*m, c.device, block, minb, dump && dump->n > 0, &k2, &k2k, &info.jit_ms));
+            int bps = k2k->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             const int wpb = block / 32;
             grid = sms * bps;
@@ -906,14 +963,15 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             info.launches += 1;
         } else {
             ssa_k2_params p{};
-            p.S = m->S; p.R = m->R; p.P = k2->P; p.PMAX = k2->PMAX; p.n_ent = k2->n_ent;
+            p.n_ent = k2->n_ent; p.n_dep = k2->n_dep;
             p.pk = k2->pk; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
-            p.n_dep = k2->n_dep; p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
+            p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
             p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
-            CU(ssa_k2_launch(p, grid, block, st));
+            void* args[] = {&p};
+            CU(cudaLaunchKernel((const void*)k2k->fn, dim3(grid), dim3(block), args, k2k->smem, st));
             info.launches += 1;
         }
         CU(cudaGetLastError());
@@ -1179,7 +1237,8 @@ extern "C" ssa_status ssa_model_prepare(const ssa_model* m, int32_t device, int3
         return ensure_k1(*m, c.device, 128, default_minb(*m, 128), false, nullptr, &e, nullptr);
     }
     K2Dev* k = nullptr;
-    return ensure_k2(*m, c.device, &k);
+    K2Kernel* kk = nullptr;
+    return ensure_k2(*m, c.device, SSA_K2_BLOCK, 1, false, &k, &kk, nullptr);
 }
 
 // ------------------------------------------------------------------ misc
@@ -1227,3 +1286,28 @@ extern "C" ssa_status ssa_debug_k1_compile(const ssa_model* m, int32_t block, in
     if (cubin_bytes) *cubin_bytes = cubin.size();
     return st;
 }
+
+extern "C" const char* ssa_debug_k2_source(const ssa_model* m, int32_t block, int32_t dump)
+{
+    static thread_local std::string s;
+    if (!m) return "";
+    s = k2_full_source(*m, std::max(1, (m->R + 31) / 32), block, 1, dump != 0);
+    return s.c_str();
+}
+
+extern "C" ssa_status ssa_debug_k2_compile(const ssa_model* m, int32_t block, int32_t dump, char* log, uint64_t log_cap,
+                                           uint64_t* cubin_bytes)
+{
+    if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
+    std::vector<char> cubin;
+    std::string lg;
+    ssa_status st = nvrtc_compile(k2_full_source(*m, std::max(1, (m->R + 31) / 32), block, 1, dump != 0), cubin, lg);
+    if (log && log_cap) {
+        std::string all = (st == SSA_OK) ? lg : g_err;
+        strncpy(log, all.c_str(), (size_t)log_cap - 1);
+        log[log_cap - 1] = 0;
+    }
+    if (cubin_bytes) *cubin_bytes = cubin.size();
+    return st;
+}
+

@@ -114,6 +114,10 @@ def lib():
         L.ssa_debug_k1_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                            P(C.c_uint64)]
         L.ssa_debug_k1_compile.restype = C.c_int
+        L.ssa_debug_k2_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
+        L.ssa_debug_k2_source.restype = C.c_char_p
+        L.ssa_debug_k2_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64, P(C.c_uint64)]
+        L.ssa_debug_k2_compile.restype = C.c_int
         _lib = L
     return _lib
 
@@ -165,12 +169,31 @@ class Model:
         """Generated K1 source (dump=True: the variant with raw-trajectory dump + hash)."""
         return lib().ssa_debug_k1_source(self.handle, block, minb, int(dump)).decode()
 
+    def k2_source(self, block: int = 256, dump: bool = False) -> str:
+        """Generated K2 (warp path) source."""
+        return _k2_source(self, block, dump)
+
+    def k2_compile(self, block: int = 256, dump: bool = False):
+        """NVRTC-compile the model's K2 kernel (no device needed); returns (status, log, cubin bytes)."""
+        return _k2_compile(self, block, dump)
+
     def k1_compile(self, block: int = 128, minb: int = 4, dump: bool = False):
         """NVRTC-compile the model's K1 kernel (no device needed); returns (status, log, cubin bytes)."""
         buf = C.create_string_buffer(1 << 16)
         nb = C.c_uint64()
         st = lib().ssa_debug_k1_compile(self.handle, block, minb, int(dump), buf, len(buf), C.byref(nb))
         return st, buf.value.decode(errors="replace"), nb.value
+
+
+def _k2_source(model, block: int = 256, dump: bool = False) -> str:
+    return lib().ssa_debug_k2_source(model.handle, block, int(dump)).decode()
+
+
+def _k2_compile(model, block: int = 256, dump: bool = False):
+    buf = C.create_string_buffer(1 << 16)
+    nb = C.c_uint64()
+    st = lib().ssa_debug_k2_compile(model.handle, block, int(dump), buf, len(buf), C.byref(nb))
+    return st, buf.value.decode(errors="replace"), nb.value
 
 
 @dataclass
