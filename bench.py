@@ -57,6 +57,18 @@ def alg_instr_per_event(net, path: int) -> float:
     return philox + u53 + plog + tau + props + prefix + select + update + rest
 
 
+def alg_warp_instr_per_event(net) -> float:
+    """Algorithmic WARP-instructions per applied event of the warp path (K2,
+    DESIGN.md §7): one trajectory per warp, P = ceil(R/32) propensities per
+    lane.  Lane sum (P loads + P adds), 5-step scan (2 shuffles + add), 3
+    broadcasts, tau (IEEE divide 9 + add), grid check, r, selection (P adds +
+    P compares + vprev shuffle + ballot/ffs/broadcast), update and dependency
+    recompute (one lane-parallel pass each), Philox + u53 + plog amortised
+    over 32 events, loop."""
+    P = max(1, -(-net.R // 32))
+    return 2 * P + 15 + 6 + 10 + 2 + (2 * P + 5) + 5 + 15 + 78 / 32 + 3
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -367,14 +379,18 @@ def main():
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     props = torch.cuda.get_device_properties(dev)
     n_sm = props.multi_processor_count
-    I = alg_instr_per_event(net, path)
     per_rank_events = events / world / args.steps
     k1_ms = statistics.mean(ssa_ms) if ssa_ms else float("nan")
-    achieved = per_rank_events * I / 32.0 / (k1_ms / 1e3) / 1e9          # G warp-instr/s
+    if path == 1:
+        I = alg_instr_per_event(net, path)                                # thread-instructions per event
+        achieved = per_rank_events * I / 32.0 / (k1_ms / 1e3) / 1e9      # G warp-instr/s
+    else:
+        I = alg_warp_instr_per_event(net)                                 # warp-instructions per event
+        achieved = per_rank_events * I / (k1_ms / 1e3) / 1e9
     peak = n_sm * 4 * sm_max * 1e6 / 1e9                                  # G warp-instr/s
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
                 "traffic": None, "kernel": "ssa_k1" if path == 1 else "ssa_k2",
-                "alg_thread_instr_per_event": I, "kernel_ms": k1_ms,
+                ("alg_thread_instr_per_event" if path == 1 else "alg_warp_instr_per_event"): I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
 
     # secondary: the chunk reduction (K3) reads the staged grid samples once -- HBM bound
