@@ -3,7 +3,9 @@
 // The warp path of north_star (a) for networks with hundreds of reactions.
 // Compiled by NVRTC at run time after ssa_device.cuh and a generated section
 // (runtime.cu: gen_k2_model) that defines SSA_S, SSA_R, SSA_P = ceil(R/32),
-// SSA_K2_BLOCK, SSA_K2_MINB (residency target) and SSA_K2_DUMP.  The model
+// SSA_K2_BLOCK, SSA_K2_MINB (residency target), SSA_K2_DUMP, SSA_HAS_M3 (a
+// reactant with coefficient 3), SSA_NU_MAX and SSA_DEP_MAX (longest net-change
+// and dependency lists).  The model
 // tables (packed reactant words, rates, modifier coefficients, x0, net
 // changes, and per-reaction dependency lists) come from the run's device
 // image (ssa_k2_params) and are staged in shared memory once per block.
@@ -42,6 +44,35 @@ static __device__ __forceinline__ double k2_factor(double x, int m)
     return __ddiv_rn(__dmul_rn(x1, __dadd_rn(x, -2.0)), 6.0);
 }
 
+#if !SSA_HAS_M3
+// Branch-free form (the 32 lanes evaluate different reactions, so branches
+// would diverge): missing reactant terms contribute the exact factor 1.0 and
+// a missing modifier the exact term +0 (0 * x), so every case reduces to the
+// definition's operations: h = f1 * f2 (f2 = 1 for n <= 1, f1 = 1 for n = 0),
+// a = k^ * h, k^ = max(0, k + d x_m).  Up to the sign of a zero propensity
+// (a -0 rate), which changes no sum, comparison or selection.
+static __device__ __forceinline__ double k2_factor_bf(double x, int m)
+{
+    const double x2 = __dmul_rn(__dmul_rn(x, __dadd_rn(x, -1.0)), 0.5);
+    return (m == 2) ? x2 : x;
+}
+
+static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const double* __restrict__ x)
+{
+    const ssa_u64 pk = q.pk;
+    const int n = (int)(pk & 3ull);
+    const double xa = x[(int)((pk >> 2) & 0x3FFF)];
+    const double xb = x[(int)((pk >> 18) & 0x3FFF)];
+    const int ms = (int)(pk >> 50);
+    const double xm = x[ms == 0x3FFF ? 0 : ms];
+    const double f1 = (n >= 1) ? k2_factor_bf(xa, (int)((pk >> 16) & 3)) : 1.0;
+    const double f2 = (n >= 2) ? k2_factor_bf(xb, (int)((pk >> 32) & 3)) : 1.0;
+    const double h = __dmul_rn(f1, f2);
+    double k = __dadd_rn(q.rate, __dmul_rn(ms == 0x3FFF ? 0.0 : q.modc, xm));
+    k = (k < 0.0) ? 0.0 : k;
+    return __dmul_rn(k, h);
+}
+#else
 static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const double* __restrict__ x)
 {
     const ssa_u64 pk = q.pk;
@@ -58,6 +89,7 @@ static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const dou
     }
     return (n == 0) ? k : __dmul_rn(k, h);
 }
+#endif
 
 #define SSA_K2_WARPS (SSA_K2_BLOCK / 32)
 
@@ -144,7 +176,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const double y = __shfl_up_sync(FULL, v, o);
-                if (lane >= o) v = __dadd_rn(y, v);
+                // v = y + v on lanes >= o: one predicated add (no selects)
+                asm("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %2, %3;\n\t@p add.rn.f64 %0, %1, %0;\n\t}"
+                    : "+d"(v) : "d"(y), "r"(lane), "r"(o));
             }
             const double a0 = __shfl_sync(FULL, v, 31);
             // a5
@@ -207,12 +241,16 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             const double r = __dmul_rn(u2, a0);
             const double vprev = __shfl_up_sync(FULL, v, 1);
             double p = (lane > 0) ? vprev : 0.0;
-            int jl = -1;
+            // p is nondecreasing over the lane's reactions: the first q with
+            // p > r is P - #{q : p_q > r} (none: -1)
+            int over = 0;
 #pragma unroll
             for (int q = 0; q < SSA_P; ++q) {
                 p = __dadd_rn(p, aq[q]);
-                jl = (jl < 0 && p > r) ? q : jl;
+                asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                    : "+r"(over) : "d"(p), "d"(r));
             }
+            const int jl = over ? SSA_P - over : -1;
             const int ls = __ffs(__ballot_sync(FULL, v > r)) - 1;
             int jq = __shfl_sync(FULL, jl, ls);
             int j;
@@ -229,7 +267,12 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             }
             // a8: state update, lane t takes the t-th net change of j
             const int nb = nu_off[j], ne = nu_off[j + 1];
+#if SSA_NU_MAX <= 32
+            if (nb + lane < ne) {
+                const int q = nb + lane;
+#else
             for (int q = nb + lane; q < ne; q += 32) {
+#endif
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
                 x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));   // arithmetic shift: signed delta
@@ -237,7 +280,12 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             __syncwarp();
             // a3: lane t recomputes the t-th reaction of dep(j)
             const int db = dep_off[j], de = dep_off[j + 1];
+#if SSA_DEP_MAX <= 32
+            if (db + lane < de) {
+                const int q = db + lane;
+#else
             for (int q = db + lane; q < de; q += 32) {
+#endif
                 const int jj = dep_ent[q];
                 const int l = jj / SSA_P, qq = jj - l * SSA_P;
                 a[qq * 32 + l] = k2_propensity(rx[jj], x);

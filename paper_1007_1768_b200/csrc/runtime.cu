@@ -548,9 +548,30 @@ static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block
 
 static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump)
 {
+    // longest net-change list and longest per-reaction dependency list (as
+    // built by ensure_k2), and whether any reactant has coefficient 3
+    int nu_max = 0, dep_max = 0, m3 = 0;
+    std::vector<std::vector<int>> readers(m.S);
+    for (int j = 0; j < m.R; ++j) {
+        nu_max = std::max(nu_max, (int)m.rx[j].nu.size());
+        for (auto& t : m.rx[j].reac) {
+            readers[t.first].push_back(j);
+            m3 |= (t.second == 3);
+        }
+        if (m.rx[j].mod_sp >= 0) readers[m.rx[j].mod_sp].push_back(j);
+    }
+    for (int j = 0; j < m.R; ++j) {
+        std::vector<int> d;
+        for (auto& c : m.rx[j].nu) d.insert(d.end(), readers[c.first].begin(), readers[c.first].end());
+        std::sort(d.begin(), d.end());
+        d.erase(std::unique(d.begin(), d.end()), d.end());
+        dep_max = std::max(dep_max, (int)d.size());
+    }
     std::ostringstream o;
     o << "#define SSA_S " << m.S << "\n#define SSA_R " << m.R << "\n#define SSA_P " << P << "\n#define SSA_K2_BLOCK "
-      << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0) << "\n";
+      << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0)
+      << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
+      << "\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
     return o.str();
 }
