@@ -79,8 +79,13 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     bool live = start();
     while (live) {
         // a2: one Philox block per candidate event, counter (e, id)
+#if SSA_KS_IMM
+        // key schedule compiled in: the round keys are instruction immediates
+        const ssa_philox_out o = ssa_philox_seeded((ssa_u32)e, (ssa_u32)(e >> 32), (ssa_u32)id, (ssa_u32)(id >> 32));
+#else
         const ssa_philox_out o = ssa_philox4x32_10_ks((ssa_u32)e, (ssa_u32)(e >> 32), (ssa_u32)id,
                                                       (ssa_u32)(id >> 32), P.ks);
+#endif
         // a3 + a4 (the propensity prefix chain) and a5's logarithm are
         // independent dependency chains in one basic block, so the scheduler
         // interleaves them.

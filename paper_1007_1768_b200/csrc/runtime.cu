@@ -330,6 +330,7 @@ static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L)
 // species counts in shared memory with a table update were both slower.)
 struct K1Gen {
     bool flat_switch = true;
+    bool seed_imm = true;   // keys=imm|param: Philox round keys as instruction immediates (kernel per seed)
     int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
 };
 
@@ -340,6 +341,7 @@ static K1Gen k1_gen()
         const char* e = getenv("SSA_K1_GEN");
         const std::string s = e ? e : "";
         if (s.find("upd=switch") != std::string::npos) r.flat_switch = false;
+        if (s.find("keys=param") != std::string::npos) r.seed_imm = false;
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
         return r;
@@ -349,7 +351,9 @@ static K1Gen k1_gen()
 
 // sweep: the parameter-sweep variant (constants per sweep point, read from
 // shared memory through kp); L: the constant layout the code indexes.
-static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump, bool sweep, const PoolLayout& L)
+// seed >= 0: the run's Philox key schedule is compiled in as immediates.
+static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump, bool sweep, const PoolLayout& L,
+                                long long seed_bits, bool use_seed)
 {
     const int S = m.S, R = m.R;
     const K1Gen g = k1_gen();
@@ -357,6 +361,22 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
       << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
       << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
+    if (use_seed) {
+        const ssa_u32 k0 = (ssa_u32)(unsigned long long)seed_bits, k1 = (ssa_u32)((unsigned long long)seed_bits >> 32);
+        // Philox4x32-10 (a2) with this seed's round keys as literals
+        o << "#define SSA_KS_IMM 1\n"
+          << "static __device__ __forceinline__ ssa_philox_out ssa_philox_seeded(ssa_u32 c0, ssa_u32 c1, ssa_u32 c2, "
+             "ssa_u32 c3) {\n  ssa_u32 lo0, hi0, lo1, hi1;\n";
+        for (int r = 0; r < 10; ++r) {
+            const ssa_u32 rk0 = k0 + (ssa_u32)r * 0x9E3779B9u, rk1 = k1 + (ssa_u32)r * 0xBB67AE85u;
+            o << "  lo0 = 0xD2511F53u * c0; hi0 = __umulhi(0xD2511F53u, c0); lo1 = 0xCD9E8D57u * c2; "
+                 "hi1 = __umulhi(0xCD9E8D57u, c2);\n"
+              << "  c0 = hi1 ^ c1 ^ " << rk0 << "u; c1 = lo1; c2 = hi0 ^ c3 ^ " << rk1 << "u; c3 = lo0;\n";
+        }
+        o << "  ssa_philox_out o; o.o0 = c0; o.o1 = c1; o.o2 = c2; o.o3 = c3; return o;\n}\n";
+    } else {
+        o << "#define SSA_KS_IMM 0\n";
+    }
     if (sweep) {
         o << "#define SSA_K(i) kp[i]\n#define SSA_KP_PARAM , const double* __restrict__ kp\n#define SSA_KP_ARG , kp\n";
     } else {
@@ -467,17 +487,20 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
 // hash (a11); runs without dumped ids use the variant without them.
 // sweep: the parameter-sweep variant indexing the layout *sweep (else the
 // model's own constant pool).
-static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep)
+// seed: the run's seed when the key schedule is compiled in (K1Gen::seed_imm),
+// else -1 (keys from the launch parameters).
+static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep,
+                                  long long seed = -1)
 {
     const PoolLayout L = sweep ? *sweep : make_pool(m, 1, nullptr, nullptr);
-    return std::string(kSsaDeviceSrc) + "\n" + gen_k1_model(m, block, minb, dump, sweep != nullptr, L) + "\n" +
-           kK1ThreadSrc;
+    return std::string(kSsaDeviceSrc) + "\n" +
+           gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1) + "\n" + kK1ThreadSrc;
 }
 
-static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep)
+static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed)
 {
     std::ostringstream o;
-    o << block << "/" << minb << "/" << (dump ? 1 : 0);
+    o << block << "/" << minb << "/" << (dump ? 1 : 0) << "/" << seed;
     if (sweep) {
         o << "/sweep:" << sweep->n;
         for (size_t j = 0; j < sweep->rate_slot.size(); ++j)
@@ -496,10 +519,10 @@ static int default_minb(const ssa_model& m, int block)
 
 // requires: current device == dev, m.mu held
 static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, const PoolLayout* sweep,
-                            K1Entry** out, double* jit_ms)
+                            K1Entry** out, double* jit_ms, long long seed = -1)
 {
     DevCache& dc = m.dev[dev];
-    const std::string key = k1_key(block, minb, dump, sweep);
+    const std::string key = k1_key(block, minb, dump, sweep, seed);
     auto it = dc.k1.find(key);
     if (it != dc.k1.end()) {
         *out = &it->second;
@@ -510,7 +533,7 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
     e.block = block;
     e.minb = minb;
     std::vector<char> cubin;
-    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep), cubin, e.log));
+    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep, seed), cubin, e.log));
     CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
     // constant pool (plain runs) and x0 into the module's constant memory
@@ -863,7 +886,10 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // blocks_per_sm > 0 also sets the K1 variant's __launch_bounds__ residency
             // target (its register budget is 64K / (block * blocks_per_sm))
             const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : default_minb(*m, block);
-            TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms));
+            // seed -1 is reserved for "keys from the parameters" (a seed of 2^64-1 takes that path)
+            const long long kseed = k1_gen().seed_imm ? (long long)seed : -1;
+            TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms,
+                          kseed));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
@@ -1285,11 +1311,11 @@ extern "C" int32_t ssa_abi_version(void) { return 1; }
 
 // Test/diagnostic hooks (not part of the stable ABI): the generated K1
 // source for a model, and compiling it without a device (NVRTC only).
-extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, int32_t minb, int32_t dump)
+extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, int32_t minb, int32_t dump, int64_t seed)
 {
     static thread_local std::string s;
     if (!m) return "";
-    s = k1_full_source(*m, block, minb, dump != 0, nullptr);
+    s = k1_full_source(*m, block, minb, dump != 0, nullptr, seed);
     return s.c_str();
 }
 

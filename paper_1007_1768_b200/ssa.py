@@ -109,7 +109,7 @@ def lib():
         L.ssa_last_error.argtypes = []
         L.ssa_last_error.restype = C.c_char_p
         L.ssa_abi_version.restype = C.c_int32
-        L.ssa_debug_k1_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32]
+        L.ssa_debug_k1_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64]
         L.ssa_debug_k1_source.restype = C.c_char_p
         L.ssa_debug_k1_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                            P(C.c_uint64)]
@@ -165,9 +165,10 @@ class Model:
     def prepare(self, device: int = -1, path: int = SSA_PATH_AUTO):
         _check(lib().ssa_model_prepare(self.handle, device, path))
 
-    def k1_source(self, block: int = 128, minb: int = 4, dump: bool = False) -> str:
-        """Generated K1 source (dump=True: the variant with raw-trajectory dump + hash)."""
-        return lib().ssa_debug_k1_source(self.handle, block, minb, int(dump)).decode()
+    def k1_source(self, block: int = 128, minb: int = 4, dump: bool = False, seed: int = -1) -> str:
+        """Generated K1 source (dump=True: the variant with raw-trajectory dump + hash;
+        seed >= 0: the variant with that seed's Philox key schedule compiled in)."""
+        return lib().ssa_debug_k1_source(self.handle, block, minb, int(dump), seed).decode()
 
     def k2_source(self, block: int = 256, dump: bool = False) -> str:
         """Generated K2 (warp path) source."""
