@@ -45,34 +45,43 @@ static __device__ __forceinline__ double k2_factor(double x, int m)
 }
 
 #if !SSA_HAS_M3
-// Branch-free form (the 32 lanes evaluate different reactions, so branches
-// would diverge): missing reactant terms contribute the exact factor 1.0 and
-// a missing modifier the exact term +0 (0 * x), so every case reduces to the
-// definition's operations: h = f1 * f2 (f2 = 1 for n <= 1, f1 = 1 for n = 0),
-// a = k^ * h, k^ = max(0, k + d x_m).  Up to the sign of a zero propensity
-// (a -0 rate), which changes no sum, comparison or selection.
+// Decoded reaction descriptor (built in shared memory from the packed tables
+// at block start): at most two reactant terms (no coefficient 3 in this
+// model), absent terms/modifier encoded so that they contribute exact
+// neutral operands.
+struct k2_rxd {
+    double rate;     // k
+    double modc;     // d, 0.0 when the reaction has no modifier
+    int sab;         // reactant species a | b << 16 (absent: 0)
+    int sms;         // modifier species (none: 0) | propensity slot (q*32 + l) << 16
+    int mab;         // coefficient of a | of b << 8 (0 = absent factor)
+    int pad;
+};
+
 static __device__ __forceinline__ double k2_factor_bf(double x, int m)
 {
-    const double x2 = __dmul_rn(__dmul_rn(x, __dadd_rn(x, -1.0)), 0.5);
-    return (m == 2) ? x2 : x;
+    const double x2 = __dmul_rn(__dmul_rn(x, __dadd_rn(x, -1.0)), 0.5);   // C(x,2)
+    return (m == 2) ? x2 : ((m == 1) ? x : 1.0);
 }
 
-static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const double* __restrict__ x)
+// Branch-free form (the 32 lanes evaluate different reactions, so branches
+// would diverge): absent reactant terms contribute the exact factor 1.0 and
+// an absent modifier the exact term +0 (0 * x), so every case performs the
+// definition's operations: h = f1 * f2, k^ = max(0, k + d x_m), a = k^ * h --
+// up to the sign of a zero propensity (a -0 rate), which changes no sum,
+// comparison or selection.
+static __device__ __forceinline__ double k2_propensity_d(const k2_rxd& d, const double* __restrict__ x)
 {
-    const ssa_u64 pk = q.pk;
-    const int n = (int)(pk & 3ull);
-    const double xa = x[(int)((pk >> 2) & 0x3FFF)];
-    const double xb = x[(int)((pk >> 18) & 0x3FFF)];
-    const int ms = (int)(pk >> 50);
-    const double xm = x[ms == 0x3FFF ? 0 : ms];
-    const double f1 = (n >= 1) ? k2_factor_bf(xa, (int)((pk >> 16) & 3)) : 1.0;
-    const double f2 = (n >= 2) ? k2_factor_bf(xb, (int)((pk >> 32) & 3)) : 1.0;
+    const double f1 = k2_factor_bf(x[d.sab & 0xFFFF], d.mab & 0xFF);
+    const double f2 = k2_factor_bf(x[(unsigned)d.sab >> 16], d.mab >> 8);
     const double h = __dmul_rn(f1, f2);
-    double k = __dadd_rn(q.rate, __dmul_rn(ms == 0x3FFF ? 0.0 : q.modc, xm));
+    double k = __dadd_rn(d.rate, __dmul_rn(d.modc, x[d.sms & 0xFFFF]));
     k = (k < 0.0) ? 0.0 : k;
     return __dmul_rn(k, h);
 }
-#else
+#endif
+
+// General form (any model, e.g. with coefficient-3 reactants).
 static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const double* __restrict__ x)
 {
     const ssa_u64 pk = q.pk;
@@ -89,7 +98,6 @@ static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const dou
     }
     return (n == 0) ? k : __dmul_rn(k, h);
 }
-#endif
 
 #define SSA_K2_WARPS (SSA_K2_BLOCK / 32)
 
@@ -108,6 +116,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     int* nu_ent = nu_off + (SSA_R + 1);
     int* dep_off = nu_ent + P.n_ent;
     int* dep_ent = dep_off + (SSA_R + 1);
+#if !SSA_HAS_M3
+    k2_rxd* rxd = (k2_rxd*)(k2_smem_raw + P.rxd_offset);   // 16-byte aligned, after dep_ent
+#endif
     for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
         k2_rx q;
         q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i];
@@ -117,6 +128,24 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     for (int i = threadIdx.x; i <= SSA_R; i += SSA_K2_BLOCK) { nu_off[i] = P.nu_off[i]; dep_off[i] = P.dep_off[i]; }
     for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_ent[i] = P.nu_ent[i];
     for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dep_ent[i] = P.dep_ent[i];
+#if !SSA_HAS_M3
+    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
+        const ssa_u64 pk = P.pk[i];
+        const int n = (int)(pk & 3ull);
+        const int ms = (int)(pk >> 50);
+        k2_rxd d;
+        d.rate = P.rate[i];
+        d.modc = (ms != 0x3FFF) ? P.modc[i] : 0.0;
+        const int sa = n >= 1 ? (int)((pk >> 2) & 0x3FFF) : 0, sb = n >= 2 ? (int)((pk >> 18) & 0x3FFF) : 0;
+        const int ma = n >= 1 ? (int)((pk >> 16) & 3) : 0, mb = n >= 2 ? (int)((pk >> 32) & 3) : 0;
+        const int slot = (i % SSA_P) * 32 + i / SSA_P;
+        d.sab = sa | (sb << 16);
+        d.sms = (ms != 0x3FFF ? ms : 0) | (slot << 16);
+        d.mab = ma | (mb << 8);
+        d.pad = 0;
+        rxd[i] = d;
+    }
+#endif
     __syncthreads();
 
     const double INF = __longlong_as_double(0x7FF0000000000000ll);
@@ -287,8 +316,13 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             for (int q = db + lane; q < de; q += 32) {
 #endif
                 const int jj = dep_ent[q];
+#if !SSA_HAS_M3
+                const k2_rxd d = rxd[jj];
+                a[(unsigned)d.sms >> 16] = k2_propensity_d(d, x);
+#else
                 const int l = jj / SSA_P, qq = jj - l * SSA_P;
                 a[qq * 32 + l] = k2_propensity(rx[jj], x);
+#endif
             }
             __syncwarp();
             t = tn;

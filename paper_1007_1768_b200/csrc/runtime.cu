@@ -562,11 +562,19 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
 // device block whose image is kept in page-locked host memory; every run
 // re-uploads it (the run's model inputs) with one async copy.  The kernel
 // itself is NVRTC-compiled per (block, dump) with S, R and P baked in.
-static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
+// dynamic shared memory of K2: rx[R] (24 B) | x0[S] | per warp (x[S] | a[32P]) |
+// nu_off | nu_ent | dep_off | dep_ent | (16-byte aligned) decoded descriptors [R] (32 B)
+static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block)
 {
     const size_t warps = (size_t)(block / 32);
-    return 24 * (size_t)R + 8 * (size_t)S + warps * 8 * ((size_t)S + 32 * (size_t)P) +
-           4 * ((size_t)R + 1 + (size_t)n_ent + (size_t)R + 1 + (size_t)n_dep);
+    const size_t b = 24 * (size_t)R + 8 * (size_t)S + warps * 8 * ((size_t)S + 32 * (size_t)P) +
+                     4 * ((size_t)R + 1 + (size_t)n_ent + (size_t)R + 1 + (size_t)n_dep);
+    return (b + 15) & ~(size_t)15;
+}
+
+static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
+{
+    return k2_rxd_offset(S, R, P, n_ent, n_dep, block) + 32 * (size_t)R;
 }
 
 static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump)
@@ -1014,6 +1022,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             p.n_ent = k2->n_ent; p.n_dep = k2->n_dep;
             p.pk = k2->pk; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
             p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
+            p.rxd_offset = k2_rxd_offset(m->S, m->R, k2->P, k2->n_ent, k2->n_dep, block);
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;

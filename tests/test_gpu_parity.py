@@ -240,6 +240,21 @@ def test_edge_cases(S):
         _parity(S, inputs.pure_death(1.0, 5), 257, 10.0, 0.5, 3, path)
 
 
+@pytest.mark.parametrize("path", [THREAD, WARP])
+def test_trimolecular_and_modifier_network(S, path):
+    """Reactant coefficient 3 (C(x,3)), a bimolecular 2A term, a catalyst and a
+    negative rate modifier on a small network, both paths (the warp path then
+    takes its general propensity evaluator)."""
+    net = Network(("A", "B", "C"), (60, 5, 3), (
+        _rx([(0, 3)], [(1, 1)], 2e-4),                 # 3A -> B       C(A,3)
+        _rx([(1, 1)], [(0, 3)], 0.3),                  # B -> 3A
+        _rx([(0, 2)], [(2, 1)], 1e-3),                 # 2A -> C       C(A,2)
+        _rx([(2, 1)], [(0, 2)], 0.2),                  # C -> 2A
+        _rx([(1, 1), (2, 1)], [(1, 1)], 0.05, mod=(0, -1e-3)),   # B + C -> B, k^ = max(0, k - 1e-3 A)
+    ))
+    _parity(S, net, 700, 6.0, 0.25, 17, path)
+
+
 def test_numeric_error_reported(S):
     """A propensity that overflows to inf (SPEC.md:85 'NaN/inf -> hard error
     naming the reaction'): SSA_ERR_NUMERIC with the id and reaction."""
