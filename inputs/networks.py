@@ -30,6 +30,15 @@ class Reaction:
     modifier_species: int = -1
     modifier_coef: float = 0.0
     name: str = ""
+    # Gated propensities ("mu*step(V5)*(1-step(V4))"):
+    # mass_action False makes h = 1 (the reactants then only set the stoichiometry);
+    # each gate (species, kind) multiplies the propensity by [x > 0] (kind 0,
+    # step(x)) or [x == 0] (kind 1, 1 - step(x)).
+    mass_action: bool = True
+    gates: Tuple[Tuple[int, int], ...] = ()
+
+
+GATE_POSITIVE, GATE_ZERO = 0, 1
 
 
 @dataclass(frozen=True)
@@ -49,9 +58,11 @@ class Network:
 
 
 def _rx(reac: Sequence[Term], prod: Sequence[Term], rate: float, name: str = "",
-        mod: Optional[Tuple[int, float]] = None) -> Reaction:
+        mod: Optional[Tuple[int, float]] = None, mass_action: bool = True,
+        gates: Sequence[Tuple[int, int]] = ()) -> Reaction:
     ms, mc = (-1, 0.0) if mod is None else mod
-    return Reaction(tuple(reac), tuple(prod), float(rate), ms, float(mc), name)
+    return Reaction(tuple(reac), tuple(prod), float(rate), ms, float(mc), name, bool(mass_action),
+                    tuple((int(a), int(b)) for a, b in gates))
 
 
 # --------------------------------------------------------------------------
@@ -99,7 +110,13 @@ HIV_PARAMS = dict(lam=200.0, d_uf=1e-5, d_ut=0.129, d_uz=0.005, d_t=0.01, d_tf=1
                   pi=200.0, s3=1e-4, d_i=0.33, d_z=0.01, d_v=2.0)
 
 
-def hiv(**overrides) -> Network:
+def hiv(variant: str = "A", **overrides) -> Network:
+    """The paper's HIV network (Table 1).  variant "A": the
+    mutation V5 -> V4 is Table 1's mass action mu*V5 (R2); "B": the
+    time-triggered mutation of PAPER.md:95 ("a stochastic event expected to
+    occur at about a given time") as SPEC.md:424's gated propensity
+    mu*step(V5)*(1-step(V4)) -- one mutation at rate mu while V5 > 0 and no V4
+    exists (NEXT 3, R33)."""
     p = dict(HIV_PARAMS)
     p.update(overrides)
     U0, U, T, Z4, Z5, I4, I5, V4, V5, F = range(10)
@@ -122,7 +139,9 @@ def hiv(**overrides) -> Network:
         _rx([(I4, 1), (Z4, 1)], [(U, 1), (I4, 1), (Z4, 1)], p["s1"], "15 I4+Z4 -> U+I4+Z4"),
         _rx([(I5, 1), (Z5, 1)], [(Z5, 1)], p["d_iz"], "16 I5+Z5 -> Z5"),
         _rx([(I4, 1), (Z4, 1)], [(Z4, 1)], p["d_iz"], "17 I4+Z4 -> Z4"),
-        _rx([(V5, 1)], [(V4, 1)], p["mu"], "18 V5 -> V4"),
+        (_rx([(V5, 1)], [(V4, 1)], p["mu"], "18 V5 -> V4") if variant == "A" else
+         _rx([(V5, 1)], [(V4, 1)], p["mu"], "18 V5 -> V4 (mu step(V5) (1-step(V4)))", mass_action=False,
+             gates=[(V5, GATE_POSITIVE), (V4, GATE_ZERO)])),
         _rx([(I5, 1)], [(V5, 200)], p["pi"], "19 I5 -> 200 V5"),
         _rx([(I4, 1)], [(V4, 200)], p["pi"], "20 I4 -> 200 V4"),
         _rx([(V4, 1)], [(F, 1), (V4, 1)], p["s3"], "21 V4 -> F+V4"),
@@ -133,7 +152,8 @@ def hiv(**overrides) -> Network:
         _rx([(V5, 1)], [], p["d_v"], "26 V5 -> 0"),
         _rx([(V4, 1)], [], p["d_v"], "27 V4 -> 0"),
     ]
-    return Network(HIV_SPECIES, HIV_X0, tuple(R), "hiv")
+    assert variant in ("A", "B")
+    return Network(HIV_SPECIES, HIV_X0, tuple(R), "hiv" if variant == "A" else "hiv-B")
 
 
 # --------------------------------------------------------------------------
@@ -207,8 +227,8 @@ def config(i: int) -> Config:
 def with_rates(net: Network, rates: Sequence[float]) -> Network:
     """The same network with its rate constants replaced (one sweep point)."""
     assert len(rates) == net.R
-    rx = tuple(Reaction(r.reactants, r.products, float(k), r.modifier_species, r.modifier_coef, r.name)
-               for r, k in zip(net.reactions, rates))
+    rx = tuple(Reaction(r.reactants, r.products, float(k), r.modifier_species, r.modifier_coef, r.name,
+                        r.mass_action, r.gates) for r, k in zip(net.reactions, rates))
     return Network(net.species, net.x0, rx, net.name)
 
 

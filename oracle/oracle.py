@@ -40,7 +40,9 @@ class _Model(C.Structure):
                 ("x0", C.POINTER(C.c_int64)), ("n_reac", C.POINTER(C.c_int32)),
                 ("reac_sp", C.POINTER(C.c_int32)), ("reac_coef", C.POINTER(C.c_int32)),
                 ("nu", C.POINTER(C.c_int64)), ("rate", C.POINTER(C.c_double)),
-                ("mod_sp", C.POINTER(C.c_int32)), ("mod_coef", C.POINTER(C.c_double))]
+                ("mod_sp", C.POINTER(C.c_int32)), ("mod_coef", C.POINTER(C.c_double)),
+                ("mass_action", C.POINTER(C.c_int32)), ("n_gates", C.POINTER(C.c_int32)),
+                ("gate_sp", C.POINTER(C.c_int32)), ("gate_kind", C.POINTER(C.c_int32))]
 
 
 class Summary(C.Structure):
@@ -112,6 +114,10 @@ class OracleModel:
         self.rate = np.zeros(max(R, 1), np.float64)
         self.mod_sp = np.full(max(R, 1), -1, np.int32)
         self.mod_coef = np.zeros(max(R, 1), np.float64)
+        self.mass_action = np.ones(max(R, 1), np.int32)
+        self.n_gates = np.zeros(max(R, 1), np.int32)
+        self.gate_sp = np.zeros(4 * max(R, 1), np.int32)
+        self.gate_kind = np.zeros(4 * max(R, 1), np.int32)
         for j, rx in enumerate(net.reactions):
             assert len(rx.reactants) <= 3
             self.n_reac[j] = len(rx.reactants)
@@ -124,10 +130,19 @@ class OracleModel:
             self.rate[j] = rx.rate
             self.mod_sp[j] = rx.modifier_species
             self.mod_coef[j] = rx.modifier_coef
+            self.mass_action[j] = 1 if getattr(rx, "mass_action", True) else 0
+            gates = getattr(rx, "gates", ())
+            assert len(gates) <= 4
+            self.n_gates[j] = len(gates)
+            for g, (sp, kind) in enumerate(gates):
+                self.gate_sp[4 * j + g] = sp
+                self.gate_kind[4 * j + g] = kind
         self._c = _Model(S, R, _ptr(self.x0, C.c_int64), _ptr(self.n_reac, C.c_int32),
                          _ptr(self.reac_sp, C.c_int32), _ptr(self.reac_coef, C.c_int32),
                          _ptr(self.nu, C.c_int64), _ptr(self.rate, C.c_double),
-                         _ptr(self.mod_sp, C.c_int32), _ptr(self.mod_coef, C.c_double))
+                         _ptr(self.mod_sp, C.c_int32), _ptr(self.mod_coef, C.c_double),
+                         _ptr(self.mass_action, C.c_int32), _ptr(self.n_gates, C.c_int32),
+                         _ptr(self.gate_sp, C.c_int32), _ptr(self.gate_kind, C.c_int32))
 
     @property
     def c(self):

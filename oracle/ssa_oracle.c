@@ -67,6 +67,11 @@ typedef struct {
     const double *rate;      /* [R] rate constant k_j                      */
     const int32_t *mod_sp;   /* [R] modifier species or -1   */
     const double *mod_coef;  /* [R] modifier coefficient d_j               */
+    /* gated propensities (NEXT 3; SPEC.md:424 mu*step(V5)*(1-step(V4))):   */
+    const int32_t *mass_action; /* [R] 1: h = prod C(x,m); 0: h = 1        */
+    const int32_t *n_gates;  /* [R] number of gates (0..4)                 */
+    const int32_t *gate_sp;  /* [R*4] gate species                         */
+    const int32_t *gate_kind;/* [R*4] 0: [x > 0] (step), 1: [x == 0]       */
 } oracle_model;
 
 typedef struct {
@@ -195,6 +200,7 @@ int oracle_propensities(const oracle_model *M, const int64_t *x, double *a, int3
             double fct = binom_factor(x[M->reac_sp[3 * j + q]], M->reac_coef[3 * j + q]);
             h = (q == 0) ? fct : h * fct;
         }
+        if (M->mass_action && !M->mass_action[j]) h = 1.0;   /* reactants only consume */
         double k = M->rate[j];
         if (M->mod_sp[j] >= 0) {
             double xm = (double)x[M->mod_sp[j]];
@@ -202,6 +208,13 @@ int oracle_propensities(const oracle_model *M, const int64_t *x, double *a, int3
             if (k < 0.0) k = 0.0;            /* "0 <= beta_R5" */
         }
         a[j] = k * h;
+        /* gates: a closed gate makes the propensity exactly 0 */
+        int open = 1;
+        for (int g = 0; M->n_gates && g < M->n_gates[j]; ++g) {
+            int64_t xg = x[M->gate_sp[4 * j + g]];
+            if (M->gate_kind[4 * j + g] == 0 ? !(xg > 0) : !(xg == 0)) open = 0;
+        }
+        if (!open) a[j] = 0.0;
         if (!isfinite(a[j])) {
             if (bad) *bad = j;
             return OR_ERR_NUMERIC;

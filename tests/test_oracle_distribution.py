@@ -227,3 +227,57 @@ def test_determinism_and_independence(oracle_lib):
     # the grid times of the last applied event are bounded by the grid
     G = a.grid_t.shape[0]
     assert np.all(a.grid_t <= np.arange(G) * 0.1 + 1e-15)
+
+
+# ---------------------------------------------------------------- gated propensities (NEXT 3)
+def test_gate_zero_one_shot_event_closed_form(oracle_lib):
+    """0 -> M at rate mu with the gate [M == 0] (SPEC.md:424's 1-step(x)):
+    exactly one event, at an Exp(mu) time, so M(t) is Bernoulli with
+    p(t) = 1 - exp(-mu t) and never exceeds 1."""
+    O = oracle_lib
+    mu, n = 0.3, 4000
+    net = Network(("M",), (0,), (_rx([], [(0, 1)], mu, gates=[(0, inputs.GATE_ZERO)]),))
+    res = O.run(O.OracleModel(net), np.arange(n), 21, 10.0, 0.5)
+    assert res.status == 0
+    assert set(np.unique(res.grid_x)) <= {0, 1}
+    assert np.all(res.summaries["events"] <= 1)
+    for k in range(res.mean.shape[0]):
+        p = 1.0 - math.exp(-mu * 0.5 * k)
+        assert _zmean(res.mean[k, 0], p, p * (1 - p), n) < Z
+        assert abs(res.var[k, 0] - res.mean[k, 0] * (1 - res.mean[k, 0])) < 1e-12
+
+
+def test_gate_positive_constant_rate_closed_form(oracle_lib):
+    """A -> 0 with mass_action off (h = 1) and the gate [A > 0] (step(A)):
+    A falls by one at constant rate k while positive, so A(t) =
+    max(0, A0 - N_t) with N_t ~ Poisson(k t)."""
+    O = oracle_lib
+    k, A0, n = 2.0, 10, 3000
+    net = Network(("A",), (A0,), (_rx([(0, 1)], [], k, mass_action=False, gates=[(0, inputs.GATE_POSITIVE)]),))
+    res = O.run(O.OracleModel(net), np.arange(n), 22, 8.0, 0.5)
+    assert res.status == 0 and np.all(res.grid_x >= 0)
+    for kk in range(res.mean.shape[0]):
+        lam = k * 0.5 * kk
+        pm = [math.exp(-lam) * lam ** i / math.factorial(i) for i in range(A0)]
+        m1 = sum((A0 - i) * p for i, p in enumerate(pm))
+        m2 = sum((A0 - i) ** 2 * p for i, p in enumerate(pm))
+        assert _zmean(res.mean[kk, 0], m1, m2 - m1 * m1, n) < Z
+    # absorbing once A = 0 (the only reaction's gate closes)
+    assert np.all(res.summaries["events"] <= A0)
+
+
+def test_hiv_variant_b_structure(oracle_lib):
+    """HIV Variant B (PAPER.md:95 time-triggered mutation): the
+    gated reaction 18 can fire only while V5 > 0 and no V4 exists (it re-arms
+    if V4 dies out), at rate mu, whatever the V5 count.  With mu = 0 no V4 ever
+    appears; with mu raised to 0.5/day mutations happen; Table 1's structural
+    invariants hold in both."""
+    O = oracle_lib
+    for mu, expect_v4 in ((0.0, False), (0.5, True)):
+        res = O.run(O.OracleModel(inputs.hiv("B", mu=mu)), np.arange(64), 23, 2.0, 0.25)
+        assert res.status == 0
+        gx = res.grid_x
+        assert np.all(gx[:, :, 0] == 1) and np.all(gx >= 0)
+        assert np.all(np.diff(gx[:, :, 9], axis=1) >= 0)
+        assert np.all(gx[:, 0, 7] == 0)
+        assert bool(np.any(gx[:, :, 7] > 0)) == expect_v4

@@ -42,6 +42,22 @@ def test_propensity_printed_values(oracle_lib):
     assert O.propensities(m, x)[1][8] > 4e-5
 
 
+def test_propensity_gated_variant_b(oracle_lib):
+    """SPEC.md:424 Variant B: a_18 = mu * step(V5) * (1 - step(V4)) -- exactly mu
+    while V5 > 0 and V4 == 0, whatever V5, else exactly 0; every other
+    reaction is unchanged from Variant A."""
+    O = oracle_lib
+    mb, ma = O.OracleModel(inputs.hiv("B")), O.OracleModel(inputs.hiv("A"))
+    x = np.array(mb.x0)
+    for v5, v4, want in ((100, 0, 2.5e-3), (1, 0, 2.5e-3), (7, 1, 0.0), (0, 0, 0.0), (0, 3, 0.0)):
+        x[8], x[7] = v5, v4
+        st, a, _ = O.propensities(mb, x)
+        assert st == 0 and a[17] == want
+        _, aa, _ = O.propensities(ma, x)
+        assert aa[17] == 2.5e-3 * v5                        # Variant A: mass action mu * V5
+        assert np.array_equal(np.delete(a, 17), np.delete(aa, 17))
+
+
 def test_propensity_combinatorial_factor(oracle_lib):
     """C(x,2) (unordered pairs, R1): 2 S1 -> S2 at S1=1000 has
     h = 499500; with c2 = 0.002 the product is 999 up to one rounding."""
