@@ -81,6 +81,32 @@ typedef struct ssa_model ssa_model;
  * is immutable and may be used from several threads at once. */
 ssa_status ssa_model_create(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
                             const ssa_reaction* reactions, ssa_model** out);
+/* Gated propensities (the paper's time-triggered
+ * mutation, "a stochastic event expected to occur at about a
+ * given time", as SPEC.md:424's mu*step(V5)*(1-step(V4)); R33).
+ * Per reaction: mass_action = 1 keeps h = prod C(x_s, m_s) over the
+ * reactants; 0 makes h = 1 (the reactants then only set the stoichiometry).
+ * Each gate multiplies the propensity by an indicator: SSA_GATE_POSITIVE is
+ * [x_species > 0] (step), SSA_GATE_ZERO is [x_species == 0] (1 - step).  A
+ * closed gate makes a_j exactly 0; an open one leaves k^ * h unchanged. */
+enum { SSA_GATE_POSITIVE = 0, SSA_GATE_ZERO = 1 };
+typedef struct {
+    int32_t species;
+    int32_t kind;          /* SSA_GATE_POSITIVE or SSA_GATE_ZERO */
+} ssa_gate;
+typedef struct {
+    int32_t mass_action;   /* 1 (default) or 0 */
+    int32_t n_gates;       /* 0..4 */
+    const ssa_gate* gates; /* [n_gates], may be NULL when n_gates == 0 */
+} ssa_reaction_ext;
+
+/* ssa_model_create with optional per-reaction extensions: ext is NULL (every
+ * reaction mass action, no gates: the same as ssa_model_create) or an array
+ * of n_reactions entries (deep-copied).  Errors as ssa_model_create, plus
+ * SSA_ERR_MODEL for a gate species out of range, an unknown gate kind or more
+ * than 4 gates. */
+ssa_status ssa_model_create_ex(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
+                               const ssa_reaction* reactions, const ssa_reaction_ext* ext, ssa_model** out);
 void ssa_model_destroy(ssa_model* model);
 int32_t ssa_model_n_species(const ssa_model* model);
 int32_t ssa_model_n_reactions(const ssa_model* model);

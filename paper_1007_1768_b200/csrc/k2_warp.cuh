@@ -4,7 +4,8 @@
 // Compiled by NVRTC at run time after ssa_device.cuh and a generated section
 // (runtime.cu: gen_k2_model) that defines SSA_S, SSA_R, SSA_P = ceil(R/32),
 // SSA_K2_BLOCK, SSA_K2_MINB (residency target), SSA_K2_DUMP, SSA_HAS_M3 (a
-// reactant with coefficient 3), SSA_NU_MAX and SSA_DEP_MAX (longest net-change
+// reactant with coefficient 3), SSA_HAS_GATES (gated propensities, NEXT 3),
+// SSA_NU_MAX and SSA_DEP_MAX (longest net-change
 // and dependency lists).  The model
 // tables (packed reactant words, rates, modifier coefficients, x0, net
 // changes, and per-reaction dependency lists) come from the run's device
@@ -33,7 +34,28 @@ struct k2_rx {
     ssa_u64 pk;      // n_reac | 3 x (14-bit species, 2-bit coef) | 14-bit modifier species
     double rate;
     double modc;
+    ssa_u64 gw;      // gates: count (3 bits) | 4 x (14-bit species, 1-bit kind: 0 [x>0], 1 [x==0])
 };
+
+// NEXT 3: a closed gate makes the propensity exactly 0 (R33)
+static __device__ __forceinline__ double k2_gated(double a, ssa_u64 gw, const double* __restrict__ x)
+{
+#if SSA_HAS_GATES
+    const int ng = (int)(gw & 7ull);
+    bool open = true;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const ssa_u64 w = gw >> (3 + 15 * g);
+        const double xg = x[(int)(w & 0x3FFF)];
+        const bool ok = ((w >> 14) & 1ull) ? (xg == 0.0) : (xg > 0.0);
+        open = open && (g >= ng || ok);
+    }
+    return open ? a : 0.0;
+#else
+    (void)gw; (void)x;
+    return a;
+#endif
+}
 
 // C(x, m) for m in {1, 2, 3}, exact for counts < 2^26.
 static __device__ __forceinline__ double k2_factor(double x, int m)
@@ -56,6 +78,7 @@ struct k2_rxd {
     int sms;         // modifier species (none: 0) | propensity slot (q*32 + l) << 16
     int mab;         // coefficient of a | of b << 8 (0 = absent factor)
     int pad;
+    ssa_u64 gw;      // gate word (as k2_rx)
 };
 
 static __device__ __forceinline__ double k2_factor_bf(double x, int m)
@@ -77,7 +100,7 @@ static __device__ __forceinline__ double k2_propensity_d(const k2_rxd& d, const 
     const double h = __dmul_rn(f1, f2);
     double k = __dadd_rn(d.rate, __dmul_rn(d.modc, x[d.sms & 0xFFFF]));
     k = (k < 0.0) ? 0.0 : k;
-    return __dmul_rn(k, h);
+    return k2_gated(__dmul_rn(k, h), d.gw, x);
 }
 #endif
 
@@ -96,7 +119,7 @@ static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const dou
         k = __dadd_rn(k, __dmul_rn(q.modc, x[ms]));
         k = (k < 0.0) ? 0.0 : k;
     }
-    return (n == 0) ? k : __dmul_rn(k, h);
+    return k2_gated((n == 0) ? k : __dmul_rn(k, h), q.gw, x);
 }
 
 #define SSA_K2_WARPS (SSA_K2_BLOCK / 32)
@@ -121,7 +144,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #endif
     for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
         k2_rx q;
-        q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i];
+        q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i]; q.gw = P.gw[i];
         rx[i] = q;
     }
     for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
@@ -143,6 +166,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         d.sms = (ms != 0x3FFF ? ms : 0) | (slot << 16);
         d.mab = ma | (mb << 8);
         d.pad = 0;
+        d.gw = P.gw[i];
         rxd[i] = d;
     }
 #endif

@@ -64,6 +64,8 @@ struct RxI {
     double rate = 0.0;
     int mod_sp = -1;
     double mod_coef = 0.0;
+    bool mass_action = true;                   // false: h = 1 (gated propensities, NEXT 3)
+    std::vector<std::pair<int, int>> gates;    // (species, SSA_GATE_POSITIVE | SSA_GATE_ZERO)
 };
 
 struct K1Entry {
@@ -89,6 +91,7 @@ struct K2Dev {
     void* host_image = nullptr;  // its page-locked host image
     size_t image_bytes = 0;
     ssa_u64* pk = nullptr;
+    ssa_u64* gw = nullptr;
     double *rate = nullptr, *modc = nullptr, *x0 = nullptr;
     int *nu_off = nullptr, *nu_ent = nullptr;
     int *dep_off = nullptr, *dep_ent = nullptr;
@@ -120,6 +123,12 @@ static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* byt
 
 extern "C" ssa_status ssa_model_create(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
                                        const ssa_reaction* reactions, ssa_model** out)
+{
+    return ssa_model_create_ex(n_species, initial_counts, n_reactions, reactions, nullptr, out);
+}
+
+extern "C" ssa_status ssa_model_create_ex(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
+                                          const ssa_reaction* reactions, const ssa_reaction_ext* ext, ssa_model** out)
 {
     if (!out) return fail(SSA_ERR_INVALID_ARG, "out is null");
     *out = nullptr;
@@ -179,6 +188,22 @@ extern "C" ssa_status ssa_model_create(int32_t n_species, const int64_t* initial
             if (!std::isfinite(q.mod_coef)) return fail(SSA_ERR_MODEL, "reaction %d: non-finite modifier coefficient", j);
         } else {
             q.mod_coef = 0.0;
+        }
+        if (ext) {
+            const ssa_reaction_ext& x = ext[j];
+            if (x.mass_action != 0 && x.mass_action != 1)
+                return fail(SSA_ERR_MODEL, "reaction %d: mass_action must be 0 or 1", j);
+            q.mass_action = x.mass_action == 1;
+            if (x.n_gates < 0 || x.n_gates > 4) return fail(SSA_ERR_MODEL, "reaction %d: %d gates (0..4)", j, x.n_gates);
+            if (x.n_gates > 0 && !x.gates) return fail(SSA_ERR_INVALID_ARG, "reaction %d: gates is null", j);
+            for (int g = 0; g < x.n_gates; ++g) {
+                const ssa_gate& gt = x.gates[g];
+                if (gt.species < 0 || gt.species >= n_species)
+                    return fail(SSA_ERR_MODEL, "reaction %d: unknown gate species %d", j, gt.species);
+                if (gt.kind != SSA_GATE_POSITIVE && gt.kind != SSA_GATE_ZERO)
+                    return fail(SSA_ERR_MODEL, "reaction %d: unknown gate kind %d", j, gt.kind);
+                q.gates.push_back({gt.species, gt.kind});
+            }
         }
         m->rx.push_back(q);
     }
@@ -312,13 +337,19 @@ static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L)
     } else {
         o << "k = " << rate << "; ";
     }
-    if (q.reac.empty()) {
+    if (q.reac.empty() || !q.mass_action) {
         o << "a = k;";
     } else {
         o << "h = " << factor_expr(q.reac[0].first, q.reac[0].second) << "; ";
         for (size_t t = 1; t < q.reac.size(); ++t)
             o << "h = __dmul_rn(h, " << factor_expr(q.reac[t].first, q.reac[t].second) << "); ";
         o << "a = __dmul_rn(k, h);";
+    }
+    if (!q.gates.empty()) {   // a closed gate makes the propensity exactly 0
+        o << " a = (";
+        for (size_t g = 0; g < q.gates.size(); ++g)
+            o << (g ? " && " : "") << "x[" << q.gates[g].first << "]" << (q.gates[g].second == SSA_GATE_ZERO ? " == 0.0" : " > 0.0");
+        o << ") ? a : 0.0;";
     }
     return o.str();
 }
@@ -562,34 +593,36 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
 // device block whose image is kept in page-locked host memory; every run
 // re-uploads it (the run's model inputs) with one async copy.  The kernel
 // itself is NVRTC-compiled per (block, dump) with S, R and P baked in.
-// dynamic shared memory of K2: rx[R] (24 B) | x0[S] | per warp (x[S] | a[32P]) |
-// nu_off | nu_ent | dep_off | dep_ent | (16-byte aligned) decoded descriptors [R] (32 B)
+// dynamic shared memory of K2: rx[R] (32 B) | x0[S] | per warp (x[S] | a[32P]) |
+// nu_off | nu_ent | dep_off | dep_ent | (16-byte aligned) decoded descriptors [R] (40 B)
 static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block)
 {
     const size_t warps = (size_t)(block / 32);
-    const size_t b = 24 * (size_t)R + 8 * (size_t)S + warps * 8 * ((size_t)S + 32 * (size_t)P) +
+    const size_t b = 32 * (size_t)R + 8 * (size_t)S + warps * 8 * ((size_t)S + 32 * (size_t)P) +
                      4 * ((size_t)R + 1 + (size_t)n_ent + (size_t)R + 1 + (size_t)n_dep);
     return (b + 15) & ~(size_t)15;
 }
 
 static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
 {
-    return k2_rxd_offset(S, R, P, n_ent, n_dep, block) + 32 * (size_t)R;
+    return k2_rxd_offset(S, R, P, n_ent, n_dep, block) + 40 * (size_t)R;
 }
 
 static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump)
 {
     // longest net-change list and longest per-reaction dependency list (as
     // built by ensure_k2), and whether any reactant has coefficient 3
-    int nu_max = 0, dep_max = 0, m3 = 0;
+    int nu_max = 0, dep_max = 0, m3 = 0, gates = 0;
     std::vector<std::vector<int>> readers(m.S);
     for (int j = 0; j < m.R; ++j) {
         nu_max = std::max(nu_max, (int)m.rx[j].nu.size());
+        gates |= !m.rx[j].gates.empty();
         for (auto& t : m.rx[j].reac) {
             readers[t.first].push_back(j);
             m3 |= (t.second == 3);
         }
         if (m.rx[j].mod_sp >= 0) readers[m.rx[j].mod_sp].push_back(j);
+        for (auto& g : m.rx[j].gates) readers[g.first].push_back(j);
     }
     for (int j = 0; j < m.R; ++j) {
         std::vector<int> d;
@@ -601,7 +634,7 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
     std::ostringstream o;
     o << "#define SSA_S " << m.S << "\n#define SSA_R " << m.R << "\n#define SSA_P " << P << "\n#define SSA_K2_BLOCK "
       << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0)
-      << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
+      << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
     return o.str();
@@ -624,13 +657,20 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         if (P > 16) return fail(SSA_ERR_UNSUPPORTED, "warp path supports at most 512 reactions (got %d)", R);
         if (S > 16383) return fail(SSA_ERR_UNSUPPORTED, "warp path supports at most 16383 species (got %d)", S);
         const size_t R1 = (size_t)std::max(R, 1);
-        std::vector<ssa_u64> pk(R1, 0);
+        std::vector<ssa_u64> pk(R1, 0), gw(R1, 0);
         std::vector<double> rate(R1, 0.0), modc(R1, 0.0), x0(S);
         std::vector<int> nu_off(R + 1, 0), nu_ent;
         for (int j = 0; j < R; ++j) {
             const RxI& q = m.rx[j];
-            ssa_u64 w = (ssa_u64)q.reac.size();
-            for (size_t t = 0; t < q.reac.size(); ++t) {
+            // gate word: count (3 bits) | per gate 14-bit species, 1-bit kind
+            ssa_u64 g = (ssa_u64)q.gates.size();
+            for (size_t t = 0; t < q.gates.size(); ++t)
+                g |= ((ssa_u64)(q.gates[t].first & 0x3FFF) | ((ssa_u64)q.gates[t].second << 14)) << (3 + 15 * t);
+            gw[j] = g;
+            // packed reactant word of the PROPENSITY (no terms when h = 1)
+            const size_t nr = q.mass_action ? q.reac.size() : 0;
+            ssa_u64 w = (ssa_u64)nr;
+            for (size_t t = 0; t < nr; ++t) {
                 w |= (ssa_u64)(q.reac[t].first & 0x3FFF) << (2 + 16 * t);
                 w |= (ssa_u64)(q.reac[t].second & 3) << (16 + 16 * t);
             }
@@ -650,13 +690,14 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         const int n_ent_real = (int)nu_ent.size();
         if (nu_ent.empty()) nu_ent.push_back(0);
         // dependency graph: reaction j -> the reactions whose propensity reads a
-        // species j changes (as a reactant or as the modifier species), unique,
-        // ascending
+        // species j changes (as a reactant, the modifier species or a gate
+        // species), unique, ascending
         std::vector<std::vector<int>> readers(S);
         for (int j = 0; j < R; ++j) {
             const RxI& q = m.rx[j];
             for (auto& t : q.reac) readers[t.first].push_back(j);
             if (q.mod_sp >= 0) readers[q.mod_sp].push_back(j);
+            for (auto& g : q.gates) readers[g.first].push_back(j);
         }
         std::vector<int> dep_off(R + 1, 0), dep_ent;
         for (int j = 0; j < R; ++j) {
@@ -669,8 +710,9 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         }
         const int n_dep_real = (int)dep_ent.size();
         if (dep_ent.empty()) dep_ent.push_back(0);
-        // image layout (8-byte aligned sections): pk | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
-        const size_t o_pk = 0, o_rate = o_pk + 8 * R1, o_modc = o_rate + 8 * R1, o_x0 = o_modc + 8 * R1;
+        // image layout (8-byte aligned sections): pk | gw | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
+        const size_t o_pk = 0, o_gw = o_pk + 8 * R1, o_rate = o_gw + 8 * R1, o_modc = o_rate + 8 * R1,
+                     o_x0 = o_modc + 8 * R1;
         const size_t o_off = o_x0 + 8 * (size_t)std::max(S, 1);
         const size_t o_ent = o_off + ((4 * nu_off.size() + 7) & ~(size_t)7);
         const size_t o_doff = o_ent + ((4 * nu_ent.size() + 7) & ~(size_t)7);
@@ -679,6 +721,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         CU(cudaMallocHost(&k.host_image, bytes));
         char* h = (char*)k.host_image;
         memcpy(h + o_pk, pk.data(), 8 * R1);
+        memcpy(h + o_gw, gw.data(), 8 * R1);
         memcpy(h + o_rate, rate.data(), 8 * R1);
         memcpy(h + o_modc, modc.data(), 8 * R1);
         memcpy(h + o_x0, x0.data(), 8 * (size_t)S);
@@ -690,6 +733,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
         char* d = (char*)k.dev_image;
         k.pk = (ssa_u64*)(d + o_pk);
+        k.gw = (ssa_u64*)(d + o_gw);
         k.rate = (double*)(d + o_rate);
         k.modc = (double*)(d + o_modc);
         k.x0 = (double*)(d + o_x0);
@@ -1020,7 +1064,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         } else {
             ssa_k2_params p{};
             p.n_ent = k2->n_ent; p.n_dep = k2->n_dep;
-            p.pk = k2->pk; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
+            p.pk = k2->pk; p.gw = k2->gw; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
             p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
             p.rxd_offset = k2_rxd_offset(m->S, m->R, k2->P, k2->n_ent, k2->n_dep, block);
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;

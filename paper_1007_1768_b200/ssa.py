@@ -42,6 +42,14 @@ class ssa_reaction(C.Structure):
                 ("rate", C.c_double), ("modifier_species", C.c_int32), ("modifier_coef", C.c_double)]
 
 
+class ssa_gate(C.Structure):
+    _fields_ = [("species", C.c_int32), ("kind", C.c_int32)]
+
+
+class ssa_reaction_ext(C.Structure):
+    _fields_ = [("mass_action", C.c_int32), ("n_gates", C.c_int32), ("gates", C.POINTER(ssa_gate))]
+
+
 class ssa_traj_summary(C.Structure):
     _fields_ = [("events", C.c_uint64), ("hash", C.c_uint64), ("t_last", C.c_double),
                 ("near_ties", C.c_uint64), ("absorbed", C.c_int32), ("status", C.c_int32),
@@ -85,6 +93,9 @@ def lib():
         P = C.POINTER
         L.ssa_model_create.argtypes = [C.c_int32, P(C.c_int64), C.c_int32, P(ssa_reaction), P(C.c_void_p)]
         L.ssa_model_create.restype = C.c_int
+        L.ssa_model_create_ex.argtypes = [C.c_int32, P(C.c_int64), C.c_int32, P(ssa_reaction), P(ssa_reaction_ext),
+                                          P(C.c_void_p)]
+        L.ssa_model_create_ex.restype = C.c_int
         L.ssa_model_destroy.argtypes = [C.c_void_p]
         L.ssa_model_destroy.restype = None
         L.ssa_model_n_species.argtypes = [C.c_void_p]
@@ -148,7 +159,17 @@ class Model:
                                  r.modifier_species, r.modifier_coef)
         x0 = np.ascontiguousarray(np.array(network.x0, dtype=np.int64))
         h = C.c_void_p()
-        _check(lib().ssa_model_create(self.S, x0.ctypes.data_as(C.POINTER(C.c_int64)), self.R, rx, C.byref(h)))
+        # gated propensities (NEXT 3): per-reaction extensions only when used
+        ext = None
+        if any((not getattr(r, "mass_action", True)) or getattr(r, "gates", ()) for r in network.reactions):
+            ext = (ssa_reaction_ext * max(self.R, 1))()
+            for j, r in enumerate(network.reactions):
+                gates = getattr(r, "gates", ())
+                garr = (ssa_gate * max(len(gates), 1))(*[ssa_gate(sp, kind) for sp, kind in gates])
+                keep.append(garr)
+                ext[j] = ssa_reaction_ext(1 if getattr(r, "mass_action", True) else 0, len(gates), garr)
+        _check(lib().ssa_model_create_ex(self.S, x0.ctypes.data_as(C.POINTER(C.c_int64)), self.R, rx, ext,
+                                         C.byref(h)))
         self.handle = h
 
     def close(self):

@@ -292,3 +292,18 @@ def test_device_outputs_and_determinism(S):
     assert np.array_equal(out[0].cpu().numpy(), h.mean) and np.array_equal(out[1].cpu().numpy(), h.var)
     h2 = S.run(m, 2048, cfg.t_end, cfg.dt, cfg.seed, path=THREAD)
     assert np.array_equal(h.mean, h2.mean) and h.events == h2.events
+
+
+# ------------------------------------------------------------ gated propensities (NEXT 3)
+@pytest.mark.parametrize("path", [THREAD, WARP])
+def test_gated_networks_parity(S, path):
+    """SPEC.md:424-style gates and the mass-action switch on both paths,
+    bit-exact against the oracle: the one-shot event, constant-rate depletion,
+    and the HIV Variant B time-triggered mutation (mu raised so that it fires
+    inside the short horizon)."""
+    one_shot = Network(("M",), (0,), (_rx([], [(0, 1)], 0.3, gates=[(0, inputs.GATE_ZERO)]),))
+    deplete = Network(("A",), (10,), (_rx([(0, 1)], [], 2.0, mass_action=False,
+                                           gates=[(0, inputs.GATE_POSITIVE)]),))
+    _parity(S, one_shot, 1000, 10.0, 0.5, 21, path)
+    _parity(S, deplete, 1000, 8.0, 0.5, 22, path)
+    _parity(S, inputs.hiv("B", mu=0.5), 200, 2.0, 0.25, 23, path)

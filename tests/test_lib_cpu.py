@@ -140,3 +140,16 @@ def test_sweep_validation_without_device(ssa):
     with pytest.raises(ssa.SSAError) as ei:
         ssa.run_sweep(m, nan, 10, 5.0, 1.0, 1)
     assert ei.value.status == 2
+
+
+def test_gate_validation(ssa):
+    """ssa_model_create_ex rejects bad gates (species, kind, count)."""
+    from inputs.networks import Network, _rx
+    for gates in ([(3, 0)], [(0, 2)], [(0, 0)] * 5):
+        net = Network(("A",), (1,), (_rx([], [(0, 1)], 1.0, gates=gates),))
+        with pytest.raises(ssa.SSAError) as ei:
+            ssa.Model(net)
+        assert ei.value.status == 2
+    ok = ssa.Model(Network(("A",), (1,), (_rx([(0, 1)], [], 1.0, mass_action=False, gates=[(0, 0)]),)))
+    st, log, _ = ok.k1_compile()
+    assert st == 0, log
