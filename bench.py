@@ -253,6 +253,8 @@ def main():
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--variant", default="A", choices=["A", "B"],
+                    help="HIV configs: B = the gated time-triggered mutation (SPEC.md:424, NEXT 3)")
     ap.add_argument("--workload", default="config", choices=["config", "sweep"],
                     help="sweep: the Fig. 4 delta_t sensitivity sweep (ssa_run_sweep, 1 GPU)")
     args = ap.parse_args()
@@ -282,6 +284,10 @@ def main():
 
     cfg = inputs.config(args.config)
     net = cfg.network
+    if args.variant == "B":
+        if net.name != "hiv":
+            raise SystemExit("--variant B applies to the HIV configs (2, 4)")
+        net = inputs.hiv("B")
     n_per = args.n_per_gpu or cfg.n_trajectories
     n_total = n_per * world
     t_end = args.t_end or cfg.t_end
@@ -416,7 +422,8 @@ def main():
         "metric": "ssa_events_per_s", "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config{args.config}-{cfg.name}", "model": net.name, "species": net.S,
+        "config": {"workload": f"config{args.config}-{cfg.name}" + ("-variantB" if args.variant == "B" else ""),
+                   "model": net.name, "species": net.S,
                    "reactions": net.R, "n_trajectories_per_gpu": n_per, "global_batch": n_total, "t_end": t_end,
                    "sample_dt": dt, "grid_points": G, "seed": cfg.seed, "path": "thread" if path == 1 else "warp",
                    "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
