@@ -89,6 +89,10 @@ def lib():
         L.oracle_run.argtypes = [P(_Model), C.c_int64, P(C.c_uint64), C.c_uint64, C.c_double,
                                  C.c_double, C.c_int32, P(C.c_double), P(C.c_double),
                                  P(C.c_int32), P(C.c_uint64), P(C.c_double), C.c_void_p]
+        L.oracle_trajectory_events.argtypes = [P(_Model), C.c_uint64, C.c_uint64, C.c_double, C.c_double,
+                                               C.c_int32, P(C.c_int32), P(C.c_uint64), P(C.c_double),
+                                               P(Summary), C.c_int64, P(C.c_double), P(C.c_int32),
+                                               P(C.c_int64)]
         _lib = L
     return _lib
 
@@ -294,3 +298,83 @@ def run(model: OracleModel, ids, seed: int, t_end: float, dt: float, mode: int =
                           None if sums is None else sums.ctypes.data)
     return RunResult(mean[:, :S], var[:, :S], st,
                      None if gx is None else gx[:, :, :S], ge, gt, sums)
+
+
+# --------------------------------------------------------------------------
+# Union-time selective memory (PAPER.md:143-149
+# §3.2.1, Fig. 3), written out as the offline brute-force
+# definition of: collect every stream, take the union of their
+# point times, hold each stream's value (zero-order hold, right-continuous),
+# reduce across streams (Y), then reduce k_x successive Y-points (X).
+# --------------------------------------------------------------------------
+def events(model: OracleModel, tid: int, seed: int, t_end: float, mode: int = 0):
+    """Applied events of trajectory `tid` on [0, t_end]: (times [E], reactions [E])."""
+    n = C.c_int64()
+    s = Summary()
+    lib().oracle_trajectory_events(model.c, tid, seed, t_end, t_end, mode, None, None, None, C.byref(s),
+                                   0, None, None, C.byref(n))
+    E = n.value
+    t = np.zeros(max(E, 1), np.float64)
+    j = np.zeros(max(E, 1), np.int32)
+    lib().oracle_trajectory_events(model.c, tid, seed, t_end, t_end, mode, None, None, None, C.byref(s),
+                                   E, _ptr(t, C.c_double), _ptr(j, C.c_int32), C.byref(n))
+    return t[:E], j[:E]
+
+
+def stream(model: OracleModel, tid: int, seed: int, t_end: float, mode: int = 0):
+    """The trajectory as a point stream: (0, x0), one point
+    per applied event (time, state after it), and the horizon point (t_end,
+    final state) unless an event lies exactly at t_end."""
+    t, j = events(model, tid, seed, t_end, mode)
+    S = model.S
+    nu = model.nu.reshape(-1, max(S, 1))[:, :S] if model.R else np.zeros((0, S), np.int64)
+    x = np.array(model.x0, np.int64)
+    times = [0.0]
+    states = [x.copy()]
+    for tt, jj in zip(t, j):
+        x = x + nu[jj]
+        times.append(float(tt))
+        states.append(x.copy())
+    if times[-1] < t_end:
+        times.append(float(t_end))
+        states.append(x.copy())
+    return np.array(times), np.array(states, np.int64).reshape(len(times), S)
+
+
+def union_reduce(streams, kx: int):
+    """Y-then-X reduction of k point streams.  Returns (times [P], mean [P,S],
+    var [P,S], n [P]): Y-points at every distinct union time u (each stream's
+    held value, summed exactly), grouped kx at a time in time order; a group's
+    time is the IEEE left-to-right sum of its Y-times divided by its size, its
+    moments are exact (n = k * size, mean = S1/n, population variance
+    (n S2 - S1^2)/n^2, each rounded once)."""
+    from fractions import Fraction
+    k = len(streams)
+    U = np.unique(np.concatenate([np.asarray(t, np.float64) for t, _ in streams]))
+    S = streams[0][1].shape[1]
+    S1 = [[0] * S for _ in U]
+    S2 = [[0] * S for _ in U]
+    for t, x in streams:
+        idx = np.searchsorted(t, U, side="right") - 1          # zero-order hold
+        assert np.all(idx >= 0)
+        held = x[idx]
+        for m in range(len(U)):
+            for s_ in range(S):
+                v = int(held[m, s_])
+                S1[m][s_] += v
+                S2[m][s_] += v * v
+    times, means, vars_, ns = [], [], [], []
+    for g0 in range(0, len(U), kx):
+        grp = range(g0, min(g0 + kx, len(U)))
+        tsum = 0.0
+        for m in grp:
+            tsum = tsum + float(U[m])
+        times.append(tsum / len(grp))
+        n = k * len(grp)
+        a1 = [sum(S1[m][s_] for m in grp) for s_ in range(S)]
+        a2 = [sum(S2[m][s_] for m in grp) for s_ in range(S)]
+        means.append([float(Fraction(a1[s_], n)) for s_ in range(S)])
+        vars_.append([float(Fraction(n * a2[s_] - a1[s_] * a1[s_], n * n)) for s_ in range(S)])
+        ns.append(n)
+    return np.array(times), np.array(means).reshape(-1, S), np.array(vars_).reshape(-1, S), np.array(ns)
+

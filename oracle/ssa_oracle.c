@@ -418,9 +418,25 @@ int oracle_align_events(int32_t S, const int64_t *x0, int64_t n_events, const do
 #define FNV_OFFSET 0xcbf29ce484222325ull
 #define FNV_PRIME 0x100000001b3ull
 
+/* As oracle_trajectory, also recording the applied events in order: their
+ * times ev_t[i] and reactions ev_j[i] for i < ev_cap (either may be NULL);
+ * *ev_n receives the number of applied events.  This is the full event
+ * stream of the trajectory ("the full simulation results"),
+ * used by the union-time selective memory (NEXT 2). */
+int oracle_trajectory_events(const oracle_model *M, uint64_t id, uint64_t seed, double t_end, double dt,
+                             int32_t mode, int32_t *grid_x, uint64_t *grid_e, double *grid_t,
+                             oracle_summary *sum, int64_t ev_cap, double *ev_t, int32_t *ev_j, int64_t *ev_n);
+
 int oracle_trajectory(const oracle_model *M, uint64_t id, uint64_t seed, double t_end, double dt,
                       int32_t mode, int32_t *grid_x, uint64_t *grid_e, double *grid_t,
                       oracle_summary *sum)
+{
+    return oracle_trajectory_events(M, id, seed, t_end, dt, mode, grid_x, grid_e, grid_t, sum, 0, NULL, NULL, NULL);
+}
+
+int oracle_trajectory_events(const oracle_model *M, uint64_t id, uint64_t seed, double t_end, double dt,
+                             int32_t mode, int32_t *grid_x, uint64_t *grid_e, double *grid_t,
+                             oracle_summary *sum, int64_t ev_cap, double *ev_t, int32_t *ev_j, int64_t *ev_n)
 {
     int S = M->S, R = M->R;
     int64_t *x = (int64_t *)malloc(sizeof(int64_t) * (S > 0 ? S : 1));
@@ -477,10 +493,15 @@ int oracle_trajectory(const oracle_model *M, uint64_t id, uint64_t seed, double 
         /* a8 */
         for (int s = 0; s < S; ++s) x[s] += M->nu[(int64_t)j * S + s];
         t = tn;
+        if ((int64_t)e < ev_cap) {
+            if (ev_t) ev_t[e] = tn;
+            if (ev_j) ev_j[e] = j;
+        }
         e += 1;
         hash = (hash ^ (uint64_t)j) * FNV_PRIME;
     }
     if (status == OR_OK && g.overflow) status = OR_ERR_OVERFLOW;
+    if (ev_n) *ev_n = (int64_t)e;
     if (sum) {
         sum->events = e;
         sum->hash = hash;

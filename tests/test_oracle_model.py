@@ -239,3 +239,36 @@ def test_moments_exact_large_values(oracle_lib):
         ev = Fraction(n * s2 - s1 * s1, n * n)
         assert abs(var[c] - float(ev)) <= 2 * np.spacing(max(float(ev), 1e-300))
     assert var[2] == 0.0 and mean[2] == 2**31 - 1
+
+
+# ------------------------------------------------------------------ union-time selective memory (NEXT 2)
+def test_union_reduce_spec_example(oracle_lib):
+    """SPEC.md:250-262 worked example of Y-alignment at union times and of
+    X-reduction of k_x successive Y-points (golden file, with citation)."""
+    O = oracle_lib
+    g = gold("spec_union_k2.json")
+    streams = [(np.array(s["times"]), np.array(s["states"], np.int64)) for s in g["streams"]]
+    for key, kx in (("kx1", 1), ("kx2", 2)):
+        t, mean, var, n = O.union_reduce(streams, kx)
+        want = g[key]
+        assert np.allclose(t, want["times"], rtol=0, atol=1e-15)
+        assert np.array_equal(mean[:, 0], want["mean"]) and np.array_equal(var[:, 0], want["var"])
+        assert list(n) == want["n"]
+
+
+def test_union_reduce_identity_and_streams(oracle_lib):
+    """k = 1, k_x = 1 is the identity: the output is the
+    stream's own points; and a stream built from the event list replays the
+    grid states the trajectory oracle reports (zero-order hold at s_k)."""
+    O = oracle_lib
+    net = inputs.dimerization(50)
+    m = O.OracleModel(net)
+    t, x = O.stream(m, 3, 2, 4.0)
+    assert t[0] == 0.0 and t[-1] == 4.0 and np.all(np.diff(t) > 0)
+    ut, mean, var, n = O.union_reduce([(t, x)], 1)
+    assert np.array_equal(ut, t) and np.array_equal(mean, x.astype(float)) and np.all(var == 0)
+    tr = O.trajectory(m, 3, 2, 4.0, 0.5)
+    sk = np.arange(9) * 0.5
+    held = x[np.searchsorted(t, sk, side="right") - 1]
+    assert np.array_equal(held, tr.grid_x)
+    assert tr.summary["events"] in (len(t) - 2, len(t) - 1)   # horizon point appended unless an event is at t_end
