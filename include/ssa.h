@@ -225,6 +225,25 @@ ssa_status ssa_run_sweep(const ssa_model* model, int32_t n_points, const double*
                          uint64_t n_per_point, double t_end, double sample_dt, uint64_t seed, uint32_t reducers,
                          const ssa_run_options* opts, ssa_result* result);
 
+/* Selective memory at union times (PAPER.md:143-149
+ * §3.2.1, Fig. 3): simulate trajectories 0..n-1 on
+ * [0, t_end] (thread path), align them at EVERY distinct event time of the
+ * ensemble (the union times, plus 0 and t_end) by zero-order hold -- Avg-Y,
+ * with equal union times collapsed into one slice -- and reduce thin_kx
+ * successive aligned slices along time -- Avg-XY (thin_kx = 1: Avg-Y itself).
+ * Output point p: times[p] = mean of its slices' times (left-to-right sum /
+ * count), mean[p*S + s], var[p*S + s] (population), count[p] = n * slices.
+ * The output has ceil(slices / thin_kx) points; capacity is the number of
+ * points the caller's arrays hold (host, or device with
+ * opts->outputs_on_device).  *n_points always receives the number of points;
+ * if it exceeds capacity the call returns SSA_ERR_INVALID_ARG and writes
+ * nothing (call again with a larger capacity).  Work: the ensemble runs
+ * twice (event counts, then recording) and every event is stored (~24 B)
+ * and sorted; n is at most 2^24.  DESIGN.md §8d. */
+ssa_status ssa_run_union(const ssa_model* model, uint64_t n_trajectories, double t_end, uint64_t seed,
+                         uint32_t thin_kx, uint64_t capacity, double* times, double* mean, double* var,
+                         double* count, uint64_t* n_points, const ssa_run_options* opts, ssa_result* result);
+
 /* Merge n_roots shard roots (DEVICE memory, contiguous [n_roots][3][cells],
  * in rank order, each an aligned subtree of equal span) as the top levels of
  * the canonical tree, then finalize into result->mean/var/m2/count (host or

@@ -187,6 +187,14 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             }
         }
         // a8: apply the selected reaction
+#if SSA_K1_RECORD
+        {   // full event stream (union-time selective memory): time, reaction, pre-event counts
+            const ssa_u64 pos = P.rec_base[rel] + e;
+            P.rec_t[pos] = tn;
+            P.rec_j[pos] = j;
+            ssa_record_pre(j, x, P.rec_pre + pos * SSA_REC_U);
+        }
+#endif
         ssa_apply(j, x);
         t = tn;
         ++e;

@@ -384,11 +384,19 @@ static K1Gen k1_gen()
 // shared memory through kp); L: the constant layout the code indexes.
 // seed >= 0: the run's Philox key schedule is compiled in as immediates.
 static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump, bool sweep, const PoolLayout& L,
-                                long long seed_bits, bool use_seed)
+                                long long seed_bits, bool use_seed, bool record = false)
 {
     const int S = m.S, R = m.R;
     const K1Gen g = k1_gen();
     std::ostringstream o;
+    if (record) {
+        // event recording: the pre-event counts of the species reaction j changes, in nu order
+        size_t U = 1;
+        for (int j = 0; j < R; ++j) U = std::max(U, m.rx[j].nu.size());
+        o << "#define SSA_K1_RECORD 1\n#define SSA_REC_U " << U << "\n";
+    } else {
+        o << "#define SSA_K1_RECORD 0\n";
+    }
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
       << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
       << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
@@ -474,6 +482,17 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         }
         o << "  default: break;\n  }\n  (void)x;\n}\n";
     }
+    if (record) {
+        o << "static __device__ __forceinline__ void ssa_record_pre(int j, const double (&x)[SSA_S], int* out) {\n"
+          << "  switch (j) {\n";
+        for (int j = 0; j < R; ++j) {
+            if (m.rx[j].nu.empty()) continue;
+            o << "  case " << j << ":";
+            for (size_t q = 0; q < m.rx[j].nu.size(); ++q) o << " out[" << q << "] = (int)x[" << m.rx[j].nu[q].first << "];";
+            o << " break;\n";
+        }
+        o << "  default: break;\n  }\n  (void)x; (void)out;\n}\n";
+    }
     return o.str();
 }
 
@@ -521,17 +540,17 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
 // seed: the run's seed when the key schedule is compiled in (K1Gen::seed_imm),
 // else -1 (keys from the launch parameters).
 static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep,
-                                  long long seed = -1)
+                                  long long seed = -1, bool record = false)
 {
     const PoolLayout L = sweep ? *sweep : make_pool(m, 1, nullptr, nullptr);
     return std::string(kSsaDeviceSrc) + "\n" +
-           gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1) + "\n" + kK1ThreadSrc;
+           gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1, record) + "\n" + kK1ThreadSrc;
 }
 
-static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed)
+static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed, bool record)
 {
     std::ostringstream o;
-    o << block << "/" << minb << "/" << (dump ? 1 : 0) << "/" << seed;
+    o << block << "/" << minb << "/" << (dump ? 1 : 0) << "/" << seed << "/" << (record ? 1 : 0);
     if (sweep) {
         o << "/sweep:" << sweep->n;
         for (size_t j = 0; j < sweep->rate_slot.size(); ++j)
@@ -550,10 +569,10 @@ static int default_minb(const ssa_model& m, int block)
 
 // requires: current device == dev, m.mu held
 static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, const PoolLayout* sweep,
-                            K1Entry** out, double* jit_ms, long long seed = -1)
+                            K1Entry** out, double* jit_ms, long long seed = -1, bool record = false)
 {
     DevCache& dc = m.dev[dev];
-    const std::string key = k1_key(block, minb, dump, sweep, seed);
+    const std::string key = k1_key(block, minb, dump, sweep, seed, record);
     auto it = dc.k1.find(key);
     if (it != dc.k1.end()) {
         *out = &it->second;
@@ -564,7 +583,7 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
     e.block = block;
     e.minb = minb;
     std::vector<char> cubin;
-    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep, seed), cubin, e.log));
+    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep, seed, record), cubin, e.log));
     CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
     // constant pool (plain runs) and x0 into the module's constant memory
@@ -887,9 +906,19 @@ struct SweepSpec {
     std::vector<RangeOut> roots;   // per point
 };
 
+// Event recording (union-time selective memory): trajectory i's applied
+// events go to rows [base[i], base[i] + events_i) of the record arrays.
+struct RecordSpec {
+    const ssa_u64* base;   // device [n]
+    double* t;             // device [E]
+    int* j;                // device [E]
+    int* pre;              // device [E][U]
+};
+
 static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end, double t_end, double dt,
                             uint64_t seed, const ssa_run_options* o, Ctx& c, RangeOut root, RunInfo& info,
-                            const ssa_dump* dump, bool dump_on_device, const SweepSpec* sw = nullptr)
+                            const ssa_dump* dump, bool dump_on_device, const SweepSpec* sw = nullptr,
+                            const RecordSpec* rec = nullptr)
 {
     const long long K = grid_K(t_end, dt);
     const ssa_u64 G = (ssa_u64)K + 1, S = (ssa_u64)m->S, cells = G * S;
@@ -901,6 +930,8 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     if (path != SSA_PATH_THREAD && path != SSA_PATH_WARP) return fail(SSA_ERR_INVALID_ARG, "bad path %d", path);
     info.path = path;
     ssa_u64 C = span;
+    if (rec && (path != SSA_PATH_THREAD || sw))
+        return fail(SSA_ERR_UNSUPPORTED, "event recording runs on the thread path");
     if (sw) {
         // chunk = as many whole sweep points as the staging budget and the
         // shared-memory constant rows (<= 32 KiB) allow
@@ -941,7 +972,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // seed -1 is reserved for "keys from the parameters" (a seed of 2^64-1 takes that path)
             const long long kseed = k1_gen().seed_imm ? (long long)seed : -1;
             TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms,
-                          kseed));
+                          kseed, rec != nullptr));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
@@ -1050,6 +1081,10 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             }
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
             p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
+            if (rec) {
+                p.rec_base = rec->base + (cb - id_begin);
+                p.rec_t = rec->t; p.rec_j = rec->j; p.rec_pre = rec->pre;
+            }
             size_t smem = 0;
             if (sw) {
                 p.n_per_point = sw->N;
@@ -1299,6 +1334,130 @@ extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const 
         r->d2h_bytes += rp.d2h_bytes;
     }
     return st;
+}
+
+extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories, double t_end, uint64_t seed,
+                                    uint32_t thin_kx, uint64_t capacity, double* times, double* mean, double* var,
+                                    double* count, uint64_t* n_points, const ssa_run_options* o, ssa_result* r)
+{
+    TRY(check_common(m, t_end, t_end, r));
+    if (!n_points) return fail(SSA_ERR_INVALID_ARG, "n_points is null");
+    *n_points = 0;
+    if (n_trajectories == 0 || n_trajectories > (1ull << 24)) return fail(SSA_ERR_INVALID_ARG, "n_trajectories not in [1, 2^24]");
+    if (thin_kx == 0) return fail(SSA_ERR_INVALID_ARG, "thin_kx must be >= 1");
+    if (o && o->path == SSA_PATH_WARP) return fail(SSA_ERR_UNSUPPORTED, "event recording runs on the thread path");
+    if (o && o->dump) return fail(SSA_ERR_INVALID_ARG, "ssa_run_union takes no dump");
+    Ctx c;
+    TRY(setup_ctx(o, c));
+    cudaStream_t st = c.st;
+    const ssa_u64 n = n_trajectories, S = (ssa_u64)m->S;
+    const ssa_u64 cells = 2 * S;           // the grid {0, t_end}: a by-product of the runs
+    ssa_run_options ro = o ? *o : ssa_run_options{};
+    ro.path = SSA_PATH_THREAD;
+    ro.dump = nullptr;
+    ro.outputs_on_device = 0;
+    DevBuf rootb;
+    CU(rootb.alloc(sizeof(double) * 3 * cells, st));
+    double* rb = rootb.as<double>();
+    // pass 1: events per trajectory (dump summaries of every trajectory)
+    std::vector<uint64_t> ids(n);
+    for (ssa_u64 i = 0; i < n; ++i) ids[i] = i;
+    std::vector<ssa_traj_summary> sums(n);
+    ssa_dump d1{};
+    d1.n = n; d1.ids = ids.data(); d1.summary = sums.data();
+    RunInfo info1;
+    TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, info1, &d1, false));
+    TRY(fill_result(info1, r));
+    std::vector<ssa_u64> base(n);
+    ssa_u64 E = 0;
+    for (ssa_u64 i = 0; i < n; ++i) {
+        base[i] = E;
+        E += sums[i].events;
+    }
+    // pass 2: the same trajectories, recording every applied event
+    int U = 1;
+    for (int j = 0; j < m->R; ++j) U = std::max(U, (int)m->rx[j].nu.size());
+    DevBuf dbase, rt, rj, rpre;
+    CU(dbase.alloc(8 * n, st));
+    CU(cudaMemcpyAsync(dbase.p, base.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    CU(rt.alloc(8 * std::max<ssa_u64>(E, 1), st));
+    CU(rj.alloc(4 * std::max<ssa_u64>(E, 1), st));
+    CU(rpre.alloc(4 * (size_t)U * std::max<ssa_u64>(E, 1), st));
+    RecordSpec rec{dbase.as<ssa_u64>(), rt.as<double>(), rj.as<int>(), rpre.as<int>()};
+    RunInfo info;
+    TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, info, nullptr, false,
+                  nullptr, &rec));
+    if (info.stats.events != E) return fail(SSA_ERR_CUDA, "recorded %llu events, expected %llu",
+                                            (unsigned long long)info.stats.events, (unsigned long long)E);
+    // model tables for the reduction: changed species and net changes, ensemble sums of x0, x0^2
+    const int R1 = std::max(m->R, 1);
+    std::vector<int> nsp((size_t)R1 * U, -1), nd((size_t)R1 * U, 0);
+    for (int j = 0; j < m->R; ++j)
+        for (size_t q = 0; q < m->rx[j].nu.size(); ++q) {
+            nsp[(size_t)j * U + q] = m->rx[j].nu[q].first;
+            nd[(size_t)j * U + q] = (int)m->rx[j].nu[q].second;
+        }
+    std::vector<long long> s0(S), s0sq(S);
+    for (ssa_u64 q = 0; q < S; ++q) {
+        s0[q] = (long long)n * m->x0[q];
+        s0sq[q] = (long long)n * m->x0[q] * m->x0[q];
+    }
+    DevBuf dnsp, dnd, ds0, ds0sq, dout;
+    CU(dnsp.alloc(4 * nsp.size(), st));
+    CU(dnd.alloc(4 * nd.size(), st));
+    CU(ds0.alloc(8 * S, st));
+    CU(ds0sq.alloc(8 * S, st));
+    CU(cudaMemcpyAsync(dnsp.p, nsp.data(), 4 * nsp.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(dnd.p, nd.data(), 4 * nd.size(), cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(ds0.p, s0.data(), 8 * S, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(ds0sq.p, s0sq.data(), 8 * S, cudaMemcpyHostToDevice, st));
+    const bool on_dev = o && o->outputs_on_device;
+    ssa_union_args a{};
+    a.E = E; a.rec_t = rt.as<double>(); a.rec_j = rj.as<int>(); a.rec_pre = rpre.as<int>(); a.U = U;
+    a.S = (int)S; a.nu_sp = dnsp.as<int>(); a.nu_d = dnd.as<int>(); a.s0 = ds0.as<long long>();
+    a.s0sq = ds0sq.as<long long>(); a.k = n; a.t_end = t_end; a.kx = thin_kx; a.capacity = capacity;
+    if (on_dev) {
+        a.times = times; a.mean = mean; a.var = var; a.count = count;
+    } else if (capacity) {
+        CU(dout.alloc(sizeof(double) * capacity * (2 + 2 * S), st));
+        double* b = dout.as<double>();
+        a.times = b; a.count = b + capacity; a.mean = b + 2 * capacity; a.var = b + (2 + S) * capacity;
+    }
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, st));
+    ssa_u64 np = 0;
+    int launches = 0;
+    CU(ssa_union_reduce(a, st, &np, &launches));
+    CU(cudaEventRecord(e1, st));
+    CU(cudaEventSynchronize(e1));
+    float ums = 0.f;
+    cudaEventElapsedTime(&ums, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *n_points = np;
+    r->events = info.stats.events;
+    r->near_ties = info.stats.near_ties;
+    r->device_ms = info1.device_ms + info.device_ms + ums;
+    r->ssa_ms = info1.ssa_ms + info.ssa_ms;
+    r->reduce_ms = ums;
+    r->reduce_bytes = E * (8 + 4 + 4 * (ssa_u64)U);
+    r->jit_ms = info1.jit_ms + info.jit_ms;
+    r->kernel_launches = info1.launches + info.launches + launches;
+    r->h2d_bytes = info1.h2d + info.h2d + 8 * n + 8 * (nsp.size() + 2 * S);
+    if (np > capacity)
+        return fail(SSA_ERR_INVALID_ARG, "capacity %llu < %llu output points (n_points holds the size needed)",
+                    (unsigned long long)capacity, (unsigned long long)np);
+    if (!on_dev) {
+        if (times) CU(cudaMemcpyAsync(times, a.times, 8 * np, cudaMemcpyDeviceToHost, st));
+        if (count) CU(cudaMemcpyAsync(count, a.count, 8 * np, cudaMemcpyDeviceToHost, st));
+        if (mean) CU(cudaMemcpyAsync(mean, a.mean, 8 * np * S, cudaMemcpyDeviceToHost, st));
+        if (var) CU(cudaMemcpyAsync(var, a.var, 8 * np * S, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        r->d2h_bytes = 8 * np * (2 + 2 * S);
+    }
+    return SSA_OK;
 }
 
 extern "C" ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, uint64_t cells,

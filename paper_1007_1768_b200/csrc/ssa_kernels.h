@@ -37,3 +37,24 @@ cudaError_t ssa_tree_merge_launch(const ssa_tree_in& in, ssa_u64 count, ssa_u64 
                                   cudaStream_t st);
 cudaError_t ssa_finalize_launch(const double* n, const double* mean, const double* m2, ssa_u64 cells,
                                 double* o_mean, double* o_var, double* o_m2, double* o_count, cudaStream_t st);
+
+// union-time selective memory (union.cu)
+struct ssa_union_args {
+    ssa_u64 E;                          // recorded events
+    const double* rec_t;                // [E] event times
+    const int* rec_j;                   // [E] reactions
+    const int* rec_pre;                 // [E][U] pre-event counts of the species each reaction changes
+    int U;
+    int S;
+    const int* nu_sp;                   // [R][U] changed species (-1: none)
+    const int* nu_d;                    // [R][U] their net change
+    const long long* s0;                // [S] sum over the ensemble of x0
+    const long long* s0sq;              // [S] sum over the ensemble of x0^2
+    ssa_u64 k;                          // trajectories
+    double t_end;
+    ssa_u64 kx;                         // X-reduction: Y-points per output point
+    ssa_u64 capacity;                   // output points the buffers hold
+    double *times, *mean, *var, *count; // device outputs [capacity], [capacity][S], [capacity][S], [capacity]
+};
+cudaError_t ssa_union_reduce(ssa_union_args a, cudaStream_t st, ssa_u64* n_points, int* launches);
+

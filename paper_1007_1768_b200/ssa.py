@@ -111,6 +111,10 @@ def lib():
         L.ssa_run_sweep.argtypes = [C.c_void_p, C.c_int32, P(C.c_double), P(C.c_double), C.c_uint64, C.c_double,
                                     C.c_double, C.c_uint64, C.c_uint32, P(ssa_run_options), P(ssa_result)]
         L.ssa_run_sweep.restype = C.c_int
+        L.ssa_run_union.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_uint64, C.c_uint32, C.c_uint64,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_uint64),
+                                    P(ssa_run_options), P(ssa_result)]
+        L.ssa_run_union.restype = C.c_int
         L.ssa_merge_roots.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, P(ssa_run_options), P(ssa_result)]
         L.ssa_merge_roots.restype = C.c_int
         L.ssa_model_prepare.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
@@ -326,6 +330,43 @@ def run_sweep(model: Model, rates, n_per_point: int, t_end: float, sample_dt: fl
     if st != SSA_OK and (raise_on_error or st not in (3, 4)):
         _check(st)
     return _result_from(r, st, mean, var, m2, count, dump)
+
+
+@dataclass
+class UnionResult:
+    times: np.ndarray     # [P]
+    mean: np.ndarray      # [P, S]
+    var: np.ndarray       # [P, S]
+    count: np.ndarray     # [P]
+    result: RunResult
+
+
+def run_union(model: Model, n_trajectories: int, t_end: float, seed: int, thin_kx: int = 1, *,
+              capacity: Optional[int] = None, **opts) -> UnionResult:
+    """ssa_run_union (selective memory at union times, Avg-Y / Avg-XY).  With
+    capacity None the call is made twice: once to learn the number of output
+    points, once to fetch them."""
+    S = model.S
+    if capacity is None:
+        n = C.c_uint64()
+        r = ssa_result()
+        o = _options(**opts)
+        st = lib().ssa_run_union(model.handle, n_trajectories, t_end, seed, thin_kx, 0, None, None, None, None,
+                                 C.byref(n), C.byref(o), C.byref(r))
+        if st not in (SSA_OK, 1):
+            _check(st)
+        capacity = n.value
+    times = np.zeros(max(capacity, 1)); count = np.zeros(max(capacity, 1))
+    mean = np.zeros((max(capacity, 1), S)); var = np.zeros((max(capacity, 1), S))
+    n = C.c_uint64()
+    r = ssa_result()
+    o = _options(**opts)
+    st = lib().ssa_run_union(model.handle, n_trajectories, t_end, seed, thin_kx, capacity, times.ctypes.data,
+                             mean.ctypes.data, var.ctypes.data, count.ctypes.data, C.byref(n), C.byref(o), C.byref(r))
+    _check(st)
+    P = n.value
+    return UnionResult(times[:P], mean[:P], var[:P], count[:P],
+                       _result_from(r, st, None, None, None, None))
 
 
 def run_device(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed: int, out, *,

@@ -1,0 +1,66 @@
+"""GPU parity of the selective memory at union times (ssa_run_union; SURVEY.md
+§8(f) NEXT 2; §3.2.1 Fig. 3): the CUDA
+pipeline (K1 event recording, radix sort by time, exact integer scans,
+X-groups) against the oracle's offline brute-force definition
+(oracle.union_reduce over oracle.stream) on the same seeded trajectories."""
+import numpy as np
+import pytest
+
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    from paper_1007_1768_b200 import build
+    build.build()
+    from paper_1007_1768_b200 import ssa
+    return ssa
+
+
+def _oracle(net, n, t_end, seed, kx):
+    from oracle import oracle as O
+    m = O.OracleModel(net)
+    return O.union_reduce([O.stream(m, i, seed, t_end) for i in range(n)], kx)
+
+
+@pytest.mark.parametrize("kx", [1, 3, 16])
+def test_union_immigration_death(S, kx):
+    net = inputs.immigration_death()
+    n, t_end, seed = 16, 8.0, 31
+    got = S.run_union(S.Model(net), n, t_end, seed, kx)
+    t, mean, var, cnt = _oracle(net, n, t_end, seed, kx)
+    assert len(got.times) == len(t)
+    assert np.array_equal(got.times, t)                      # union times and group means: bitwise
+    assert np.array_equal(got.count, cnt.astype(float))
+    assert np.array_equal(got.mean, mean)                    # exact sums, one rounding each
+    assert np.allclose(got.var, var, rtol=1e-12, atol=0)
+
+
+def test_union_hiv_short(S):
+    """The paper's HIV model (Fig. 4's 16 trajectories), over a short horizon."""
+    net = inputs.hiv()
+    n, t_end, seed, kx = 16, 0.05, 5, 16
+    got = S.run_union(S.Model(net), n, t_end, seed, kx)
+    t, mean, var, cnt = _oracle(net, n, t_end, seed, kx)
+    assert np.array_equal(got.times, t) and np.array_equal(got.count, cnt.astype(float))
+    assert np.allclose(got.mean, mean, rtol=1e-15, atol=0)
+    assert np.allclose(got.var, var, rtol=1e-9, atol=0)
+    assert np.all(got.mean[:, 0] == 1.0)
+
+
+def test_union_capacity_and_empty(S):
+    """Too small a capacity reports the size needed; an empty network gives
+    the two held slices 0 and t_end."""
+    net = inputs.immigration_death()
+    m = S.Model(net)
+    with pytest.raises(S.SSAError) as ei:
+        S.run_union(m, 4, 5.0, 1, 1, capacity=3)
+    assert ei.value.status == 1
+    e = S.run_union(S.Model(inputs.empty_network((4, 2))), 5, 3.0, 1, 1)
+    assert np.array_equal(e.times, [0.0, 3.0]) and np.all(e.mean == [4, 2]) and np.all(e.var == 0)
+    assert np.all(e.count == 5)
