@@ -238,6 +238,55 @@ def run_sweep_bench(args, rank, world):
     return 0
 
 
+# ---------------------------------------------------------------- union-time workload
+def run_union_bench(args, rank, world):
+    """Selective memory at union times (NEXT 2): 16 HIV trajectories (Fig. 4,
+    "multiple trajectories (16x)") over config 2's horizon,
+    Avg-XY with k_x = 16 (SPEC.md's default k_x = k).  Device time of the whole
+    call (CUDA events inside the library: counting run, recording run, sort,
+    scans, X-groups); the reduction's own time and bytes are reported too."""
+    if world != 1:
+        print(json.dumps({"error": "the union workload runs on one GPU"}))
+        return 1
+    import torch
+
+    import inputs
+    from paper_1007_1768_b200 import build as B
+    B.build()
+    from paper_1007_1768_b200 import ssa as S
+    torch.cuda.set_device(0)
+    cfg = inputs.config(2)
+    n = args.n_per_gpu or 16
+    t_end = args.t_end or cfg.t_end
+    m = S.Model(inputs.hiv("B") if args.variant == "B" else cfg.network)
+    first = S.run_union(m, n, t_end, cfg.seed, args.kx)           # sizes the output (untimed)
+    cap = len(first.times)
+    for _ in range(max(args.warmup - 1, 0)):
+        S.run_union(m, n, t_end, cfg.seed, args.kx, capacity=cap)
+    dev_ms, red_ms, red_b, events, launches = [], [], 0, 0, 0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            u = S.run_union(m, n, t_end, cfg.seed, args.kx, capacity=cap)
+            dev_ms.append(u.result.device_ms)
+            red_ms.append(u.result.reduce_ms)
+            red_b = u.result.reduce_bytes
+            events += u.result.events
+            launches += u.result.kernel_launches
+    ms = sum(dev_ms)
+    line = {"metric": "ssa_events_per_s", "value": events / (ms / 1e3), "unit": "events/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+i64", "data": "synthetic",
+            "config": {"workload": "union-time-selective-memory", "model": m.network.name, "n_trajectories": n,
+                       "t_end": t_end, "thin_kx": args.kx, "seed": cfg.seed, "output_points": cap,
+                       "timing": "device time of each call (CUDA events in the library)"},
+            "events_per_step": events / args.steps, "gpu_launches": launches,
+            "union_reduction": {"ms": statistics.mean(red_ms), "recorded_bytes": red_b,
+                                "recorded_GBps": red_b / (statistics.mean(red_ms) / 1e3) / 1e9},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -255,8 +304,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variant", default="A", choices=["A", "B"],
                     help="HIV configs: B = the gated time-triggered mutation (SPEC.md:424, NEXT 3)")
-    ap.add_argument("--workload", default="config", choices=["config", "sweep"],
-                    help="sweep: the Fig. 4 delta_t sensitivity sweep (ssa_run_sweep, 1 GPU)")
+    ap.add_argument("--workload", default="config", choices=["config", "sweep", "union"],
+                    help="sweep: the Fig. 4 delta_t sensitivity sweep (ssa_run_sweep, 1 GPU); union: selective "
+                         "memory at union times over 16 HIV trajectories (ssa_run_union, Fig. 4's ensemble)")
+    ap.add_argument("--kx", type=int, default=16, help="union workload: X-reduction factor k_x")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -266,6 +317,8 @@ def main():
         return run_reference(args, rank, world)
     if args.workload == "sweep":
         return run_sweep_bench(args, rank, world)
+    if args.workload == "union":
+        return run_union_bench(args, rank, world)
 
     import numpy as np
     import torch
