@@ -188,11 +188,20 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         }
         // a8: apply the selected reaction
 #if SSA_K1_RECORD
-        {   // full event stream (union-time selective memory): time, reaction, pre-event counts
-            const ssa_u64 pos = P.rec_base[rel] + e;
-            P.rec_t[pos] = tn;
-            P.rec_j[pos] = j;
-            ssa_record_pre(j, x, P.rec_pre + pos * SSA_REC_U);
+        {   // full event stream (union-time selective memory): time, reaction,
+            // pre-event counts, appended at a row reserved with one atomic per warp
+            const unsigned act = __activemask();
+            const int lane = threadIdx.x & 31;
+            const int leader = __ffs(act) - 1;
+            ssa_u64 base = 0;
+            if (lane == leader) base = atomicAdd(P.rec_count, (ssa_u64)__popc(act));
+            base = __shfl_sync(act, base, leader);
+            const ssa_u64 pos = base + __popc(act & ((1u << lane) - 1u));
+            if (pos < P.rec_cap) {
+                P.rec_t[pos] = tn;
+                P.rec_j[pos] = j;
+                ssa_record_pre(j, x, P.rec_pre + pos * SSA_REC_U);
+            }
         }
 #endif
         ssa_apply(j, x);

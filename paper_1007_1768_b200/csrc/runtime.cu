@@ -814,6 +814,14 @@ struct DevBuf {  // stream-ordered device allocation
         return cudaMallocAsync(&p, bytes ? bytes : 8, s);
     }
     template <class T> T* as() const { return (T*)p; }
+    void reset()
+    {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+    }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
 };
 
 struct Ctx {
@@ -906,13 +914,15 @@ struct SweepSpec {
     std::vector<RangeOut> roots;   // per point
 };
 
-// Event recording (union-time selective memory): trajectory i's applied
-// events go to rows [base[i], base[i] + events_i) of the record arrays.
+// Event recording (union-time selective memory): every applied event is
+// appended (in no particular order) at a row reserved from *count; rows
+// >= cap are counted but not written.
 struct RecordSpec {
-    const ssa_u64* base;   // device [n]
-    double* t;             // device [E]
-    int* j;                // device [E]
-    int* pre;              // device [E][U]
+    ssa_u64* count;        // device counter (zeroed by the caller)
+    ssa_u64 cap;
+    double* t;             // device [cap]
+    int* j;                // device [cap]
+    int* pre;              // device [cap][U]
 };
 
 static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end, double t_end, double dt,
@@ -1082,7 +1092,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
             p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
             if (rec) {
-                p.rec_base = rec->base + (cb - id_begin);
+                p.rec_count = rec->count; p.rec_cap = rec->cap;
                 p.rec_t = rec->t; p.rec_j = rec->j; p.rec_pre = rec->pre;
             }
             size_t smem = 0;
@@ -1359,36 +1369,41 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     DevBuf rootb;
     CU(rootb.alloc(sizeof(double) * 3 * cells, st));
     double* rb = rootb.as<double>();
-    // pass 1: events per trajectory (dump summaries of every trajectory)
-    std::vector<uint64_t> ids(n);
-    for (ssa_u64 i = 0; i < n; ++i) ids[i] = i;
-    std::vector<ssa_traj_summary> sums(n);
-    ssa_dump d1{};
-    d1.n = n; d1.ids = ids.data(); d1.summary = sums.data();
-    RunInfo info1;
-    TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, info1, &d1, false));
-    TRY(fill_result(info1, r));
-    std::vector<ssa_u64> base(n);
-    ssa_u64 E = 0;
-    for (ssa_u64 i = 0; i < n; ++i) {
-        base[i] = E;
-        E += sums[i].events;
-    }
-    // pass 2: the same trajectories, recording every applied event
+    // one recording run (events appended in any order: they are sorted by time
+    // next); if the record buffer was too small, run again with the exact size
     int U = 1;
     for (int j = 0; j < m->R; ++j) U = std::max(U, (int)m->rx[j].nu.size());
-    DevBuf dbase, rt, rj, rpre;
-    CU(dbase.alloc(8 * n, st));
-    CU(cudaMemcpyAsync(dbase.p, base.data(), 8 * n, cudaMemcpyHostToDevice, st));
-    CU(rt.alloc(8 * std::max<ssa_u64>(E, 1), st));
-    CU(rj.alloc(4 * std::max<ssa_u64>(E, 1), st));
-    CU(rpre.alloc(4 * (size_t)U * std::max<ssa_u64>(E, 1), st));
-    RecordSpec rec{dbase.as<ssa_u64>(), rt.as<double>(), rj.as<int>(), rpre.as<int>()};
-    RunInfo info;
-    TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, info, nullptr, false,
-                  nullptr, &rec));
-    if (info.stats.events != E) return fail(SSA_ERR_CUDA, "recorded %llu events, expected %llu",
-                                            (unsigned long long)info.stats.events, (unsigned long long)E);
+    const size_t row = 12 + 4 * (size_t)U;
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    ssa_u64 cap = std::min<ssa_u64>((ssa_u64)(free_b / 8) / row, 1ull << 27);   // first guess: <= 1/8 of free HBM
+    if (const char* g = getenv("SSA_UNION_CAP0")) cap = strtoull(g, nullptr, 10);   // test hook: force the re-run
+    RunInfo info, info1;
+    DevBuf dcount, rt, rj, rpre;
+    CU(dcount.alloc(8, st));
+    ssa_u64 E = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        rt.reset(); rj.reset(); rpre.reset();
+        CU(rt.alloc(8 * std::max<ssa_u64>(cap, 1), st));
+        CU(rj.alloc(4 * std::max<ssa_u64>(cap, 1), st));
+        CU(rpre.alloc(4 * (size_t)U * std::max<ssa_u64>(cap, 1), st));
+        CU(cudaMemsetAsync(dcount.p, 0, 8, st));
+        RecordSpec rec{dcount.as<ssa_u64>(), cap, rt.as<double>(), rj.as<int>(), rpre.as<int>()};
+        RunInfo& ri = attempt == 0 ? info : info1;
+        ri = RunInfo();
+        TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, ri, nullptr,
+                      false, nullptr, &rec));
+        TRY(fill_result(ri, r));
+        CU(cudaMemcpy(&E, dcount.p, 8, cudaMemcpyDeviceToHost));
+        if (E <= cap) {
+            if (attempt == 1) info = info1;
+            break;
+        }
+        cap = E;   // rare: the exact size for the second run
+    }
+    if (info.stats.events != E)
+        return fail(SSA_ERR_CUDA, "recorded %llu events, ran %llu", (unsigned long long)E,
+                    (unsigned long long)info.stats.events);
     // model tables for the reduction: changed species and net changes, ensemble sums of x0, x0^2
     const int R1 = std::max(m->R, 1);
     std::vector<int> nsp((size_t)R1 * U, -1), nd((size_t)R1 * U, 0);
@@ -1439,13 +1454,13 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     *n_points = np;
     r->events = info.stats.events;
     r->near_ties = info.stats.near_ties;
-    r->device_ms = info1.device_ms + info.device_ms + ums;
-    r->ssa_ms = info1.ssa_ms + info.ssa_ms;
+    r->device_ms = info.device_ms + ums;
+    r->ssa_ms = info.ssa_ms;
     r->reduce_ms = ums;
     r->reduce_bytes = E * (8 + 4 + 4 * (ssa_u64)U);
-    r->jit_ms = info1.jit_ms + info.jit_ms;
-    r->kernel_launches = info1.launches + info.launches + launches;
-    r->h2d_bytes = info1.h2d + info.h2d + 8 * n + 8 * (nsp.size() + 2 * S);
+    r->jit_ms = info.jit_ms;
+    r->kernel_launches = info.launches + launches;
+    r->h2d_bytes = info.h2d + 8 * (nsp.size() + 2 * S);
     if (np > capacity)
         return fail(SSA_ERR_INVALID_ARG, "capacity %llu < %llu output points (n_points holds the size needed)",
                     (unsigned long long)capacity, (unsigned long long)np);

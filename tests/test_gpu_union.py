@@ -64,3 +64,15 @@ def test_union_capacity_and_empty(S):
     e = S.run_union(S.Model(inputs.empty_network((4, 2))), 5, 3.0, 1, 1)
     assert np.array_equal(e.times, [0.0, 3.0]) and np.all(e.mean == [4, 2]) and np.all(e.var == 0)
     assert np.all(e.count == 5)
+
+
+def test_union_record_buffer_rerun(S, monkeypatch):
+    """A too-small first record buffer (forced through the SSA_UNION_CAP0 test
+    hook) makes the library run once more with the exact size: same output."""
+    net = inputs.dimerization(60)
+    m = S.Model(net)
+    a = S.run_union(m, 8, 1.0, 3, 4)
+    monkeypatch.setenv("SSA_UNION_CAP0", "10")
+    b = S.run_union(m, 8, 1.0, 3, 4)
+    assert np.array_equal(a.times, b.times) and np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
+    assert a.result.events == b.result.events > 10
