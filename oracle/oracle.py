@@ -378,3 +378,31 @@ def union_reduce(streams, kx: int):
         ns.append(n)
     return np.array(times), np.array(means).reshape(-1, S), np.array(vars_).reshape(-1, S), np.array(ns)
 
+
+
+# --------------------------------------------------------------------------
+# Stride-sampled trajectory output (PAPER.md:175
+# "a 1:10 sampling (outputting 1 simulation point every 10)"
+# SamplingPolicy::Stride(s) "emit every s-th event plus first/last").
+# --------------------------------------------------------------------------
+def stride_points(model: OracleModel, tid: int, seed: int, t_end: float, stride: int, mode: int = 0):
+    """(event_index [P], times [P], states [P, S]) of trajectory `tid`: the
+    initial point (0, 0, x0), the point after every stride-th applied event
+    (k, t_k, x_k) for k = s, 2s, ..., and the horizon point (E, t_end, x_E)
+    unless the last emitted point is already at t_end."""
+    t, j = events(model, tid, seed, t_end, mode)
+    S = model.S
+    nu = model.nu.reshape(-1, max(S, 1))[:, :S] if model.R else np.zeros((0, S), np.int64)
+    x = np.array(model.x0, np.int64)
+    ks, ts, xs = [0], [0.0], [x.copy()]
+    for k, (tt, jj) in enumerate(zip(t, j), start=1):
+        x = x + nu[jj]
+        if k % stride == 0:
+            ks.append(k)
+            ts.append(float(tt))
+            xs.append(x.copy())
+    if ts[-1] < t_end:
+        ks.append(len(t))
+        ts.append(float(t_end))
+        xs.append(x.copy())
+    return np.array(ks, np.uint64), np.array(ts), np.array(xs, np.int64).reshape(len(ts), S)

@@ -272,3 +272,22 @@ def test_union_reduce_identity_and_streams(oracle_lib):
     held = x[np.searchsorted(t, sk, side="right") - 1]
     assert np.array_equal(held, tr.grid_x)
     assert tr.summary["events"] in (len(t) - 2, len(t) - 1)   # horizon point appended unless an event is at t_end
+
+
+# ------------------------------------------------------------------ stride-sampled output (NEXT 4)
+def test_stride_points_definition(oracle_lib):
+    """SPEC.md:162/:184 Stride(s): first and last points always; every s-th
+    event in between; the empty network gives exactly (0, x0), (t_end, x0);
+    stride 1 is the full point stream."""
+    O = oracle_lib
+    k, t, x = O.stride_points(O.OracleModel(inputs.empty_network((7,))), 0, 1, 10.0, 10)
+    assert list(k) == [0, 0] and list(t) == [0.0, 10.0] and np.all(x == 7)
+    m = O.OracleModel(inputs.immigration_death())
+    ts, xs = O.stream(m, 2, 1, 6.0)
+    k1, t1, x1 = O.stride_points(m, 2, 1, 6.0, 1)
+    assert np.array_equal(t1, ts) and np.array_equal(x1, xs)
+    k10, t10, x10 = O.stride_points(m, 2, 1, 6.0, 10)
+    E = int(k1[-1])
+    assert list(k10[1:-1]) == list(range(10, E + 1, 10))
+    assert np.array_equal(t10[1:-1], t1[10:E + 1:10]) and np.array_equal(x10[1:-1], x1[10:E + 1:10])
+    assert t10[-1] == 6.0 and np.array_equal(x10[-1], x1[-1])
