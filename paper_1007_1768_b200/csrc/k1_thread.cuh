@@ -76,6 +76,10 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         return true;
     };
 
+#if SSA_K1_RECORD
+#define SSA_REC_BLOCK 256
+    ssa_u64 rec_cur = 0, rec_end = 0;   // this lane's reserved record rows [rec_cur, rec_end)
+#endif
     bool live = start();
     while (live) {
         // a2: one Philox block per candidate event, counter (e, id)
@@ -189,14 +193,12 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // a8: apply the selected reaction
 #if SSA_K1_RECORD
         {   // full event stream (union-time selective memory): time, reaction,
-            // pre-event counts, appended at a row reserved with one atomic per warp
-            const unsigned act = __activemask();
-            const int lane = threadIdx.x & 31;
-            const int leader = __ffs(act) - 1;
-            ssa_u64 base = 0;
-            if (lane == leader) base = atomicAdd(P.rec_count, (ssa_u64)__popc(act));
-            base = __shfl_sync(act, base, leader);
-            const ssa_u64 pos = base + __popc(act & ((1u << lane) - 1u));
+            // pre-event counts, in this lane's current block of reserved rows
+            if (rec_cur == rec_end) {           // one atomic per SSA_REC_BLOCK events
+                rec_cur = atomicAdd(P.rec_count, (ssa_u64)SSA_REC_BLOCK);
+                rec_end = rec_cur + SSA_REC_BLOCK;
+            }
+            const ssa_u64 pos = rec_cur++;
             if (pos < P.rec_cap) {
                 P.rec_t[pos] = tn;
                 P.rec_j[pos] = j;
@@ -211,6 +213,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;   // firing hash: observable only through the dump
 #endif
     }
+#if SSA_K1_RECORD
+    // unused reserved rows sort last: time +inf
+    for (; rec_cur < rec_end; ++rec_cur)
+        if (rec_cur < P.rec_cap) { P.rec_t[rec_cur] = INF; P.rec_j[rec_cur] = 0; }
+#endif
     // warp-level reduction of the counters, then one atomic per warp
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {

@@ -1381,7 +1381,7 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     RunInfo info, info1;
     DevBuf dcount, rt, rj, rpre;
     CU(dcount.alloc(8, st));
-    ssa_u64 E = 0;
+    ssa_u64 E = 0, rows = 0;
     for (int attempt = 0; attempt < 2; ++attempt) {
         rt.reset(); rj.reset(); rpre.reset();
         CU(rt.alloc(8 * std::max<ssa_u64>(cap, 1), st));
@@ -1394,16 +1394,14 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
         TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, ri, nullptr,
                       false, nullptr, &rec));
         TRY(fill_result(ri, r));
-        CU(cudaMemcpy(&E, dcount.p, 8, cudaMemcpyDeviceToHost));
-        if (E <= cap) {
+        CU(cudaMemcpy(&rows, dcount.p, 8, cudaMemcpyDeviceToHost));
+        if (rows <= cap) {
             if (attempt == 1) info = info1;
             break;
         }
-        cap = E;   // rare: the exact size for the second run
+        cap = rows;   // rare: the reserved size for the second run
     }
-    if (info.stats.events != E)
-        return fail(SSA_ERR_CUDA, "recorded %llu events, ran %llu", (unsigned long long)E,
-                    (unsigned long long)info.stats.events);
+    E = info.stats.events;   // valid rows: the first E after sorting by time (unused rows are +inf)
     // model tables for the reduction: changed species and net changes, ensemble sums of x0, x0^2
     const int R1 = std::max(m->R, 1);
     std::vector<int> nsp((size_t)R1 * U, -1), nd((size_t)R1 * U, 0);
@@ -1428,7 +1426,7 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     CU(cudaMemcpyAsync(ds0sq.p, s0sq.data(), 8 * S, cudaMemcpyHostToDevice, st));
     const bool on_dev = o && o->outputs_on_device;
     ssa_union_args a{};
-    a.E = E; a.rec_t = rt.as<double>(); a.rec_j = rj.as<int>(); a.rec_pre = rpre.as<int>(); a.U = U;
+    a.E = E; a.rows = rows; a.rec_t = rt.as<double>(); a.rec_j = rj.as<int>(); a.rec_pre = rpre.as<int>(); a.U = U;
     a.S = (int)S; a.nu_sp = dnsp.as<int>(); a.nu_d = dnd.as<int>(); a.s0 = ds0.as<long long>();
     a.s0sq = ds0sq.as<long long>(); a.k = n; a.t_end = t_end; a.kx = thin_kx; a.capacity = capacity;
     if (on_dev) {

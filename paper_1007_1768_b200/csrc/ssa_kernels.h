@@ -40,7 +40,8 @@ cudaError_t ssa_finalize_launch(const double* n, const double* mean, const doubl
 
 // union-time selective memory (union.cu)
 struct ssa_union_args {
-    ssa_u64 E;                          // recorded events
+    ssa_u64 E;                          // recorded events (valid rows)
+    ssa_u64 rows;                       // reserved rows (>= E; the others have time +inf)
     const double* rec_t;                // [E] event times
     const int* rec_j;                   // [E] reactions
     const int* rec_pre;                 // [E][U] pre-event counts of the species each reaction changes

@@ -133,23 +133,24 @@ struct Scratch {
 
 cudaError_t ssa_union_reduce(ssa_union_args a, cudaStream_t st, ssa_u64* n_points, int* launches)
 {
-    const ssa_u64 E = a.E;
+    const ssa_u64 E = a.E, NR = a.rows;
     Scratch keys, keys2, idx, idx2, d1, d2, flags, ypos, nsel, temp;
     ssa_u64 D = 0;
     if (E > 0) {
-        UCHK(keys.alloc(8 * E, st));
-        UCHK(keys2.alloc(8 * E, st));
-        UCHK(idx.alloc(4 * E, st));
-        UCHK(idx2.alloc(4 * E, st));
-        k_keys<<<grid_for(E), 256, 0, st>>>(a.rec_t, E, (ssa_u64*)keys.p, (unsigned*)idx.p);
+        UCHK(keys.alloc(8 * NR, st));
+        UCHK(keys2.alloc(8 * NR, st));
+        UCHK(idx.alloc(4 * NR, st));
+        UCHK(idx2.alloc(4 * NR, st));
+        k_keys<<<grid_for(NR), 256, 0, st>>>(a.rec_t, NR, (ssa_u64*)keys.p, (unsigned*)idx.p);
         ++*launches;
-        // 1. sort by time
+        // 1. sort by time (the +inf rows of unused reservations go last; the
+        //    first E sorted rows are the events)
         size_t tb = 0;
         UCHK(cub::DeviceRadixSort::SortPairs(nullptr, tb, (const ssa_u64*)keys.p, (ssa_u64*)keys2.p,
-                                             (const unsigned*)idx.p, (unsigned*)idx2.p, (int64_t)E, 0, 64, st));
+                                             (const unsigned*)idx.p, (unsigned*)idx2.p, (int64_t)NR, 0, 64, st));
         UCHK(temp.alloc(tb, st));
         UCHK(cub::DeviceRadixSort::SortPairs(temp.p, tb, (const ssa_u64*)keys.p, (ssa_u64*)keys2.p,
-                                             (const unsigned*)idx.p, (unsigned*)idx2.p, (int64_t)E, 0, 64, st));
+                                             (const unsigned*)idx.p, (unsigned*)idx2.p, (int64_t)NR, 0, 64, st));
         ++*launches;
         const ssa_u64* sk = (const ssa_u64*)keys2.p;
         const unsigned* perm = (const unsigned*)idx2.p;
