@@ -244,6 +244,23 @@ ssa_status ssa_run_union(const ssa_model* model, uint64_t n_trajectories, double
                          uint32_t thin_kx, uint64_t capacity, double* times, double* mean, double* var,
                          double* count, uint64_t* n_points, const ssa_run_options* opts, ssa_result* result);
 
+/* Full-trajectory output with stride sampling (
+ * PAPER.md:133 "the worker can directly write the full simulation results",
+ * PAPER.md:175 "a 1:10 sampling (outputting 1 simulation point every 10)";
+ * SPEC.md:162 Stride(s)): simulate trajectories 0..n-1 on [0, t_end] (thread
+ * path) and return, ordered by trajectory then time, the points (0, x0), the
+ * state after every stride-th applied event, and the horizon point (t_end,
+ * held state) unless the last point is already at t_end.  Row p: traj[p],
+ * event[p] (events applied up to the point; the horizon point carries the
+ * total), time[p], states[p*S + s] (int32).  capacity, n_points and errors
+ * as ssa_run_union (host arrays, or device with opts->outputs_on_device);
+ * result->d2h_bytes counts the output copied to the host, result->reduce_ms
+ * the sort + gather.  n is at most 2^23. */
+ssa_status ssa_run_trajectories(const ssa_model* model, uint64_t n_trajectories, double t_end, uint64_t seed,
+                                uint64_t stride, uint64_t capacity, uint32_t* traj, uint64_t* event, double* time,
+                                int32_t* states, uint64_t* n_points, const ssa_run_options* opts,
+                                ssa_result* result);
+
 /* Merge n_roots shard roots (DEVICE memory, contiguous [n_roots][3][cells],
  * in rank order, each an aligned subtree of equal span) as the top levels of
  * the canonical tree, then finalize into result->mean/var/m2/count (host or

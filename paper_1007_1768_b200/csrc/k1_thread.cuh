@@ -77,10 +77,36 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     };
 
 #if SSA_K1_RECORD
-#define SSA_REC_BLOCK 256
+#define SSA_REC_BLOCK (SSA_K1_RECORD == 1 ? 256 : 32)
     ssa_u64 rec_cur = 0, rec_end = 0;   // this lane's reserved record rows [rec_cur, rec_end)
+    // one row from the lane's block (a new block every SSA_REC_BLOCK rows; rows >= cap are dropped)
+    auto rec_row = [&]() -> ssa_u64 {
+        if (rec_cur == rec_end) {
+            rec_cur = atomicAdd(P.rec_count, (ssa_u64)SSA_REC_BLOCK);
+            rec_end = rec_cur + SSA_REC_BLOCK;
+        }
+        return rec_cur++;
+    };
+#endif
+#if SSA_K1_RECORD == 2
+    // stride-sampled output (SPEC.md:162 Stride(s)): (0, x0), every s-th event, the horizon
+    ssa_u64 rec_left = 0;               // events until the next stride point
+    double rec_last_t = 0.0;            // time of the last point emitted
+    auto rec_point = [&](ssa_u64 seq, double tp) {
+        const ssa_u64 pos = rec_row();
+        if (pos < P.rec_cap) {
+            P.rec_key[pos] = (rel << 41) | seq;
+            P.rec_t[pos] = tp;
+#pragma unroll
+            for (int s = 0; s < SSA_S; ++s) P.rec_pre[pos * SSA_S + s] = (int)x[s];
+        }
+        rec_last_t = tp;
+    };
 #endif
     bool live = start();
+#if SSA_K1_RECORD == 2
+    if (live) { rec_left = P.rec_stride; rec_point(0, 0.0); }
+#endif
     while (live) {
         // a2: one Philox block per candidate event, counter (e, id)
 #if SSA_KS_IMM
@@ -186,19 +212,25 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     const ssa_u64 packed = (vid << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
                     atomicMin(&P.stats->first_err_id, packed);
                 }
+#if SSA_K1_RECORD == 2
+                // the horizon point (held state at s_K), unless the last point is already there
+                {
+                    const double hz = __dmul_rn((double)K, dt);
+                    if (rec_last_t < hz) rec_point(2 * e + 1, hz);
+                }
+#endif
                 live = start();
+#if SSA_K1_RECORD == 2
+                if (live) { rec_left = P.rec_stride; rec_point(0, 0.0); }
+#endif
                 continue;
             }
         }
         // a8: apply the selected reaction
-#if SSA_K1_RECORD
+#if SSA_K1_RECORD == 1
         {   // full event stream (union-time selective memory): time, reaction,
             // pre-event counts, in this lane's current block of reserved rows
-            if (rec_cur == rec_end) {           // one atomic per SSA_REC_BLOCK events
-                rec_cur = atomicAdd(P.rec_count, (ssa_u64)SSA_REC_BLOCK);
-                rec_end = rec_cur + SSA_REC_BLOCK;
-            }
-            const ssa_u64 pos = rec_cur++;
+            const ssa_u64 pos = rec_row();
             if (pos < P.rec_cap) {
                 P.rec_t[pos] = tn;
                 P.rec_j[pos] = j;
@@ -212,11 +244,24 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #if SSA_K1_DUMP
         hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;   // firing hash: observable only through the dump
 #endif
+#if SSA_K1_RECORD == 2
+        if (--rec_left == 0) {
+            rec_point(2 * e, t);
+            rec_left = P.rec_stride;
+        }
+#endif
     }
 #if SSA_K1_RECORD
     // unused reserved rows sort last: time +inf
     for (; rec_cur < rec_end; ++rec_cur)
-        if (rec_cur < P.rec_cap) { P.rec_t[rec_cur] = INF; P.rec_j[rec_cur] = 0; }
+        if (rec_cur < P.rec_cap) {
+            P.rec_t[rec_cur] = INF;
+#if SSA_K1_RECORD == 1
+            P.rec_j[rec_cur] = 0;
+#else
+            P.rec_key[rec_cur] = ~0ull;
+#endif
+        }
 #endif
     // warp-level reduction of the counters, then one atomic per warp
 #pragma unroll

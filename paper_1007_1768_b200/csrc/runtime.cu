@@ -384,16 +384,19 @@ static K1Gen k1_gen()
 // shared memory through kp); L: the constant layout the code indexes.
 // seed >= 0: the run's Philox key schedule is compiled in as immediates.
 static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump, bool sweep, const PoolLayout& L,
-                                long long seed_bits, bool use_seed, bool record = false)
+                                long long seed_bits, bool use_seed, int record = 0)
 {
     const int S = m.S, R = m.R;
     const K1Gen g = k1_gen();
     std::ostringstream o;
-    if (record) {
+    if (record == 1) {
         // event recording: the pre-event counts of the species reaction j changes, in nu order
         size_t U = 1;
         for (int j = 0; j < R; ++j) U = std::max(U, m.rx[j].nu.size());
         o << "#define SSA_K1_RECORD 1\n#define SSA_REC_U " << U << "\n";
+    } else if (record == 2) {
+        // stride-sampled points: the full state (S counts) per point
+        o << "#define SSA_K1_RECORD 2\n#define SSA_REC_U " << S << "\n";
     } else {
         o << "#define SSA_K1_RECORD 0\n";
     }
@@ -482,7 +485,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         }
         o << "  default: break;\n  }\n  (void)x;\n}\n";
     }
-    if (record) {
+    if (record == 1) {
         o << "static __device__ __forceinline__ void ssa_record_pre(int j, const double (&x)[SSA_S], int* out) {\n"
           << "  switch (j) {\n";
         for (int j = 0; j < R; ++j) {
@@ -540,17 +543,17 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
 // seed: the run's seed when the key schedule is compiled in (K1Gen::seed_imm),
 // else -1 (keys from the launch parameters).
 static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep,
-                                  long long seed = -1, bool record = false)
+                                  long long seed = -1, int record = 0)
 {
     const PoolLayout L = sweep ? *sweep : make_pool(m, 1, nullptr, nullptr);
     return std::string(kSsaDeviceSrc) + "\n" +
            gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1, record) + "\n" + kK1ThreadSrc;
 }
 
-static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed, bool record)
+static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed, int record)
 {
     std::ostringstream o;
-    o << block << "/" << minb << "/" << (dump ? 1 : 0) << "/" << seed << "/" << (record ? 1 : 0);
+    o << block << "/" << minb << "/" << (dump ? 1 : 0) << "/" << seed << "/" << record;
     if (sweep) {
         o << "/sweep:" << sweep->n;
         for (size_t j = 0; j < sweep->rate_slot.size(); ++j)
@@ -569,7 +572,7 @@ static int default_minb(const ssa_model& m, int block)
 
 // requires: current device == dev, m.mu held
 static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, const PoolLayout* sweep,
-                            K1Entry** out, double* jit_ms, long long seed = -1, bool record = false)
+                            K1Entry** out, double* jit_ms, long long seed = -1, int record = 0)
 {
     DevCache& dc = m.dev[dev];
     const std::string key = k1_key(block, minb, dump, sweep, seed, record);
@@ -918,6 +921,9 @@ struct SweepSpec {
 // appended (in no particular order) at a row reserved from *count; rows
 // >= cap are counted but not written.
 struct RecordSpec {
+    int mode;              // 1: events (time, reaction, pre-event counts); 2: stride points (key, time, state)
+    ssa_u64 stride;        // mode 2
+    ssa_u64* key;          // mode 2: device [cap] (trajectory << 41 | 2k or 2E+1)
     ssa_u64* count;        // device counter (zeroed by the caller)
     ssa_u64 cap;
     double* t;             // device [cap]
@@ -982,7 +988,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // seed -1 is reserved for "keys from the parameters" (a seed of 2^64-1 takes that path)
             const long long kseed = k1_gen().seed_imm ? (long long)seed : -1;
             TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms,
-                          kseed, rec != nullptr));
+                          kseed, rec ? rec->mode : 0));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
@@ -1092,7 +1098,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
             p.dump_t = p_t; p.dump_sum = p_sum; p.stats = statsb.as<ssa_dev_stats>();
             if (rec) {
-                p.rec_count = rec->count; p.rec_cap = rec->cap;
+                p.rec_count = rec->count; p.rec_cap = rec->cap; p.rec_key = rec->key; p.rec_stride = rec->stride;
                 p.rec_t = rec->t; p.rec_j = rec->j; p.rec_pre = rec->pre;
             }
             size_t smem = 0;
@@ -1388,7 +1394,7 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
         CU(rj.alloc(4 * std::max<ssa_u64>(cap, 1), st));
         CU(rpre.alloc(4 * (size_t)U * std::max<ssa_u64>(cap, 1), st));
         CU(cudaMemsetAsync(dcount.p, 0, 8, st));
-        RecordSpec rec{dcount.as<ssa_u64>(), cap, rt.as<double>(), rj.as<int>(), rpre.as<int>()};
+        RecordSpec rec{1, 0, nullptr, dcount.as<ssa_u64>(), cap, rt.as<double>(), rj.as<int>(), rpre.as<int>()};
         RunInfo& ri = attempt == 0 ? info : info1;
         ri = RunInfo();
         TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, ri, nullptr,
@@ -1470,6 +1476,106 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
         CU(cudaStreamSynchronize(st));
         r->d2h_bytes = 8 * np * (2 + 2 * S);
     }
+    return SSA_OK;
+}
+
+extern "C" ssa_status ssa_run_trajectories(const ssa_model* m, uint64_t n_trajectories, double t_end, uint64_t seed,
+                                           uint64_t stride, uint64_t capacity, uint32_t* traj, uint64_t* event,
+                                           double* time, int32_t* states, uint64_t* n_points,
+                                           const ssa_run_options* o, ssa_result* r)
+{
+    TRY(check_common(m, t_end, t_end, r));
+    if (!n_points) return fail(SSA_ERR_INVALID_ARG, "n_points is null");
+    *n_points = 0;
+    if (n_trajectories == 0 || n_trajectories > (1ull << 23)) return fail(SSA_ERR_INVALID_ARG, "n_trajectories not in [1, 2^23]");
+    if (stride == 0) return fail(SSA_ERR_INVALID_ARG, "stride must be >= 1");
+    if (o && o->path == SSA_PATH_WARP) return fail(SSA_ERR_UNSUPPORTED, "trajectory output runs on the thread path");
+    if (o && o->dump) return fail(SSA_ERR_INVALID_ARG, "ssa_run_trajectories takes no dump");
+    Ctx c;
+    TRY(setup_ctx(o, c));
+    cudaStream_t st = c.st;
+    const ssa_u64 n = n_trajectories, S = (ssa_u64)m->S, cells = 2 * S;
+    ssa_run_options ro = o ? *o : ssa_run_options{};
+    ro.path = SSA_PATH_THREAD;
+    ro.dump = nullptr;
+    ro.outputs_on_device = 0;
+    DevBuf rootb;
+    CU(rootb.alloc(sizeof(double) * 3 * cells, st));
+    double* rb = rootb.as<double>();
+    const size_t row = 16 + 4 * S;
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    ssa_u64 cap = std::min<ssa_u64>((ssa_u64)(free_b / 8) / row, 1ull << 26);
+    if (const char* g = getenv("SSA_UNION_CAP0")) cap = strtoull(g, nullptr, 10);   // test hook: force the re-run
+    RunInfo info, info1;
+    DevBuf dcount, rk, rt, rs;
+    CU(dcount.alloc(8, st));
+    ssa_u64 rows = 0;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        rk.reset(); rt.reset(); rs.reset();
+        CU(rk.alloc(8 * std::max<ssa_u64>(cap, 1), st));
+        CU(rt.alloc(8 * std::max<ssa_u64>(cap, 1), st));
+        CU(rs.alloc(4 * S * std::max<ssa_u64>(cap, 1), st));
+        CU(cudaMemsetAsync(dcount.p, 0, 8, st));
+        RecordSpec rec{2, stride, rk.as<ssa_u64>(), dcount.as<ssa_u64>(), cap, rt.as<double>(), nullptr, rs.as<int>()};
+        RunInfo& ri = attempt == 0 ? info : info1;
+        ri = RunInfo();
+        TRY(run_range(m, 0, n, t_end, t_end, seed, &ro, c, RangeOut{rb, rb + cells, rb + 2 * cells}, ri, nullptr,
+                      false, nullptr, &rec));
+        TRY(fill_result(ri, r));
+        CU(cudaMemcpy(&rows, dcount.p, 8, cudaMemcpyDeviceToHost));
+        if (rows <= cap) {
+            if (attempt == 1) info = info1;
+            break;
+        }
+        cap = rows;
+    }
+    const bool on_dev = o && o->outputs_on_device;
+    DevBuf dout;
+    unsigned* ot = nullptr;
+    ssa_u64* oe = nullptr;
+    double* otm = nullptr;
+    int* os = nullptr;
+    if (on_dev) {
+        ot = traj; oe = (ssa_u64*)event; otm = time; os = states;
+    } else if (capacity) {
+        CU(dout.alloc((size_t)capacity * (4 + 8 + 8 + 4 * S), st));
+        char* b = (char*)dout.p;
+        oe = (ssa_u64*)b; otm = (double*)(b + 8 * capacity); ot = (unsigned*)(b + 16 * capacity);
+        os = (int*)(b + 20 * capacity);
+    }
+    cudaEvent_t e0, e1, e2;
+    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1)); CU(cudaEventCreate(&e2));
+    CU(cudaEventRecord(e0, st));
+    ssa_u64 np = 0;
+    int launches = 0;
+    CU(ssa_points_gather(rk.as<ssa_u64>(), rt.as<double>(), rs.as<int>(), rows, (int)S, capacity, ot, oe, otm, os,
+                         &np, st, &launches));
+    CU(cudaEventRecord(e1, st));
+    *n_points = np;
+    const bool fits = np <= capacity;
+    if (fits && !on_dev) {   // the output phase: device -> host
+        if (time) CU(cudaMemcpyAsync(time, otm, 8 * np, cudaMemcpyDeviceToHost, st));
+        if (event) CU(cudaMemcpyAsync(event, oe, 8 * np, cudaMemcpyDeviceToHost, st));
+        if (traj) CU(cudaMemcpyAsync(traj, ot, 4 * np, cudaMemcpyDeviceToHost, st));
+        if (states) CU(cudaMemcpyAsync(states, os, 4 * S * np, cudaMemcpyDeviceToHost, st));
+        r->d2h_bytes += np * (20 + 4 * S);
+    }
+    CU(cudaEventRecord(e2, st));
+    CU(cudaEventSynchronize(e2));
+    float gms = 0.f, cms = 0.f;
+    cudaEventElapsedTime(&gms, e0, e1);
+    cudaEventElapsedTime(&cms, e1, e2);
+    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
+    r->device_ms = info.device_ms + gms + cms;
+    r->ssa_ms = info.ssa_ms;
+    r->reduce_ms = gms;                        // sort + gather of the points
+    r->reduce_bytes = rows * (16 + 4 * S);     // recorded point bytes
+    r->jit_ms = info.jit_ms;
+    r->kernel_launches = info.launches + launches;
+    if (!fits)
+        return fail(SSA_ERR_INVALID_ARG, "capacity %llu < %llu output points (n_points holds the size needed)",
+                    (unsigned long long)capacity, (unsigned long long)np);
     return SSA_OK;
 }
 

@@ -59,3 +59,9 @@ struct ssa_union_args {
 };
 cudaError_t ssa_union_reduce(ssa_union_args a, cudaStream_t st, ssa_u64* n_points, int* launches);
 
+// stride-sampled trajectory output (union.cu): sort the recorded points by
+// key and gather them (device outputs of `capacity` rows; *n_points = points)
+cudaError_t ssa_points_gather(const ssa_u64* keys, const double* t, const int* states, ssa_u64 rows, int S,
+                              ssa_u64 capacity, unsigned* o_traj, ssa_u64* o_event, double* o_time, int* o_state,
+                              ssa_u64* n_points, cudaStream_t st, int* launches);
+

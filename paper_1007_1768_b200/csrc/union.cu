@@ -214,3 +214,72 @@ cudaError_t ssa_union_reduce(ssa_union_args a, cudaStream_t st, ssa_u64* n_point
     UCHK(cudaGetLastError());
     return cudaStreamSynchronize(st);
 }
+
+// --------------------------------------------------------------------------
+// Stride-sampled trajectory output ("a
+// 1:10 sampling (outputting 1 simulation point every 10)"): the points K1's
+// stride-record variant appended (key = trajectory << 41 | seq, seq = 2k
+// after event k, 0 initial, 2E+1 horizon; unused rows key ~0) are sorted by
+// key and gathered into per-trajectory, time-ordered output rows.
+namespace {
+
+__global__ void k_iota(ssa_u64 n, unsigned* __restrict__ idx)
+{
+    for (ssa_u64 m = blockIdx.x * (ssa_u64)blockDim.x + threadIdx.x; m < n; m += (ssa_u64)gridDim.x * blockDim.x)
+        idx[m] = (unsigned)m;
+}
+
+__global__ void k_count_valid(const ssa_u64* __restrict__ keys, ssa_u64 n, ssa_u64* __restrict__ valid)
+{
+    for (ssa_u64 m = blockIdx.x * (ssa_u64)blockDim.x + threadIdx.x; m < n; m += (ssa_u64)gridDim.x * blockDim.x)
+        if (keys[m] != ~0ull && (m + 1 == n || keys[m + 1] == ~0ull)) *valid = m + 1;
+}
+
+__global__ void k_gather_points(const ssa_u64* __restrict__ keys, const unsigned* __restrict__ idx, ssa_u64 P, int S,
+                                const double* __restrict__ t, const int* __restrict__ st, ssa_u64 traj_base,
+                                unsigned* __restrict__ o_traj, ssa_u64* __restrict__ o_event,
+                                double* __restrict__ o_time, int* __restrict__ o_state)
+{
+    for (ssa_u64 m = blockIdx.x * (ssa_u64)blockDim.x + threadIdx.x; m < P; m += (ssa_u64)gridDim.x * blockDim.x) {
+        const ssa_u64 k = keys[m], src = idx[m];
+        o_traj[m] = (unsigned)(traj_base + (k >> 41));
+        o_event[m] = (k & ((1ull << 41) - 1)) >> 1;
+        o_time[m] = t[src];
+        for (int s = 0; s < S; ++s) o_state[m * S + s] = st[src * S + s];
+    }
+}
+
+}  // namespace
+
+cudaError_t ssa_points_gather(const ssa_u64* keys_in, const double* t, const int* states, ssa_u64 rows, int S,
+                              ssa_u64 capacity, unsigned* o_traj, ssa_u64* o_event, double* o_time, int* o_state,
+                              ssa_u64* n_points, cudaStream_t st, int* launches)
+{
+    *n_points = 0;
+    if (rows == 0) return cudaSuccess;
+    Scratch keys2, idx, idx2, temp, valid;
+    UCHK(keys2.alloc(8 * rows, st));
+    UCHK(idx.alloc(4 * rows, st));
+    UCHK(idx2.alloc(4 * rows, st));
+    UCHK(valid.alloc(8, st));
+    UCHK(cudaMemsetAsync(valid.p, 0, 8, st));
+    k_iota<<<grid_for(rows), 256, 0, st>>>(rows, (unsigned*)idx.p);
+    size_t tb = 0;
+    UCHK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys_in, (ssa_u64*)keys2.p, (const unsigned*)idx.p,
+                                         (unsigned*)idx2.p, (int64_t)rows, 0, 64, st));
+    UCHK(temp.alloc(tb, st));
+    UCHK(cub::DeviceRadixSort::SortPairs(temp.p, tb, keys_in, (ssa_u64*)keys2.p, (const unsigned*)idx.p,
+                                         (unsigned*)idx2.p, (int64_t)rows, 0, 64, st));
+    k_count_valid<<<grid_for(rows), 256, 0, st>>>((const ssa_u64*)keys2.p, rows, (ssa_u64*)valid.p);
+    *launches += 3;
+    ssa_u64 P = 0;
+    UCHK(cudaMemcpyAsync(&P, valid.p, 8, cudaMemcpyDeviceToHost, st));
+    UCHK(cudaStreamSynchronize(st));
+    *n_points = P;
+    if (P > capacity) return cudaSuccess;
+    k_gather_points<<<grid_for(P), 256, 0, st>>>((const ssa_u64*)keys2.p, (const unsigned*)idx2.p, P, S, t, states, 0,
+                                                 o_traj, o_event, o_time, o_state);
+    ++*launches;
+    UCHK(cudaGetLastError());
+    return cudaStreamSynchronize(st);
+}

@@ -115,6 +115,10 @@ def lib():
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_uint64),
                                     P(ssa_run_options), P(ssa_result)]
         L.ssa_run_union.restype = C.c_int
+        L.ssa_run_trajectories.argtypes = [C.c_void_p, C.c_uint64, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, P(C.c_uint64),
+                                           P(ssa_run_options), P(ssa_result)]
+        L.ssa_run_trajectories.restype = C.c_int
         L.ssa_merge_roots.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, P(ssa_run_options), P(ssa_result)]
         L.ssa_merge_roots.restype = C.c_int
         L.ssa_model_prepare.argtypes = [C.c_void_p, C.c_int32, C.c_int32]
@@ -367,6 +371,43 @@ def run_union(model: Model, n_trajectories: int, t_end: float, seed: int, thin_k
     P = n.value
     return UnionResult(times[:P], mean[:P], var[:P], count[:P],
                        _result_from(r, st, None, None, None, None))
+
+
+@dataclass
+class TrajectoryPoints:
+    traj: np.ndarray      # [P] uint32
+    event: np.ndarray     # [P] uint64
+    time: np.ndarray      # [P] float64
+    states: np.ndarray    # [P, S] int32
+    result: RunResult
+
+
+def run_trajectories(model: Model, n_trajectories: int, t_end: float, seed: int, stride: int = 10, *,
+                     capacity: Optional[int] = None, **opts) -> TrajectoryPoints:
+    """ssa_run_trajectories (stride-sampled full trajectories).  With capacity
+    None the call is made twice: once to learn the number of points."""
+    S = model.S
+    if capacity is None:
+        n = C.c_uint64()
+        r = ssa_result()
+        o = _options(**opts)
+        st = lib().ssa_run_trajectories(model.handle, n_trajectories, t_end, seed, stride, 0, None, None, None, None,
+                                        C.byref(n), C.byref(o), C.byref(r))
+        if st not in (SSA_OK, 1):
+            _check(st)
+        capacity = n.value
+    cap = max(capacity, 1)
+    traj = np.zeros(cap, np.uint32); event = np.zeros(cap, np.uint64); time = np.zeros(cap)
+    states = np.zeros((cap, S), np.int32)
+    n = C.c_uint64()
+    r = ssa_result()
+    o = _options(**opts)
+    st = lib().ssa_run_trajectories(model.handle, n_trajectories, t_end, seed, stride, capacity, traj.ctypes.data,
+                                    event.ctypes.data, time.ctypes.data, states.ctypes.data, C.byref(n), C.byref(o),
+                                    C.byref(r))
+    _check(st)
+    P = n.value
+    return TrajectoryPoints(traj[:P], event[:P], time[:P], states[:P], _result_from(r, st, None, None, None, None))
 
 
 def run_device(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed: int, out, *,

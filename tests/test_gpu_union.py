@@ -76,3 +76,37 @@ def test_union_record_buffer_rerun(S, monkeypatch):
     b = S.run_union(m, 8, 1.0, 3, 4)
     assert np.array_equal(a.times, b.times) and np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
     assert a.result.events == b.result.events > 10
+
+
+# ------------------------------------------------------------ stride-sampled output (NEXT 4)
+@pytest.mark.parametrize("stride", [1, 10])
+def test_trajectory_points_vs_oracle(S, stride):
+    """ssa_run_trajectories: per trajectory the points (0, x0), every
+    stride-th event and the horizon, bit-exact against oracle.stride_points."""
+    from oracle import oracle as O
+    net = inputs.dimerization(80)
+    n, t_end, seed = 9, 2.0, 41
+    got = S.run_trajectories(S.Model(net), n, t_end, seed, stride)
+    om = O.OracleModel(net)
+    assert np.all(np.diff(got.traj.astype(np.int64)) >= 0)
+    for i in range(n):
+        sel = got.traj == i
+        k, t, x = O.stride_points(om, i, seed, t_end, stride)
+        assert np.array_equal(got.event[sel], k)
+        assert np.array_equal(got.time[sel], t)
+        assert np.array_equal(got.states[sel], x.astype(np.int32))
+
+
+def test_trajectory_points_hiv_and_rerun(S, monkeypatch):
+    """The paper's HIV model with its 1:10 sampling over a short
+    horizon, with a forced re-run of the recording (too small a first buffer)."""
+    from oracle import oracle as O
+    net = inputs.hiv()
+    monkeypatch.setenv("SSA_UNION_CAP0", "100")
+    got = S.run_trajectories(S.Model(net), 4, 0.2, 3, 10)
+    om = O.OracleModel(net)
+    for i in range(4):
+        sel = got.traj == i
+        k, t, x = O.stride_points(om, i, 3, 0.2, 10)
+        assert np.array_equal(got.event[sel], k) and np.array_equal(got.time[sel], t)
+        assert np.array_equal(got.states[sel], x.astype(np.int32))
