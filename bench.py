@@ -287,6 +287,52 @@ def run_union_bench(args, rank, world):
     return 0
 
 
+# ---------------------------------------------------------------- full-trajectory output workload
+def run_traj_bench(args, rank, world):
+    """Stride-sampled full trajectories (NEXT 4): the paper's output
+    experiment, "a 1:10 sampling (outputting 1 simulation point every 10)"
+    (PAPER.md:175), for 16 HIV trajectories over config 2's horizon.  Device
+    time of each call (simulation + sort/gather + the device-to-host copy of
+    the points, CUDA events in the library)."""
+    if world != 1:
+        print(json.dumps({"error": "the trajectories workload runs on one GPU"}))
+        return 1
+    import torch
+
+    import inputs
+    from paper_1007_1768_b200 import build as B
+    B.build()
+    from paper_1007_1768_b200 import ssa as S
+    torch.cuda.set_device(0)
+    cfg = inputs.config(2)
+    n = args.n_per_gpu or 16
+    t_end = args.t_end or cfg.t_end
+    m = S.Model(cfg.network)
+    first = S.run_trajectories(m, n, t_end, cfg.seed, 10)
+    cap = len(first.time)
+    for _ in range(max(args.warmup - 1, 0)):
+        S.run_trajectories(m, n, t_end, cfg.seed, 10, capacity=cap)
+    dev_ms, events, d2h, red_ms = [], 0, 0, []
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            u = S.run_trajectories(m, n, t_end, cfg.seed, 10, capacity=cap)
+            dev_ms.append(u.result.device_ms)
+            red_ms.append(u.result.reduce_ms)
+            d2h = u.result.d2h_bytes
+            events += u.result.events
+    ms = sum(dev_ms)
+    line = {"metric": "ssa_events_per_s", "value": events / (ms / 1e3), "unit": "events/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "full-trajectories-1:10", "model": cfg.network.name, "n_trajectories": n,
+                       "t_end": t_end, "stride": 10, "seed": cfg.seed, "points": cap,
+                       "timing": "device time of each call incl. the D2H of the points (CUDA events in the library)"},
+            "points_per_s": cap * args.steps / (ms / 1e3), "output_bytes_per_step": d2h,
+            "sort_gather_ms": statistics.mean(red_ms), "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -304,7 +350,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variant", default="A", choices=["A", "B"],
                     help="HIV configs: B = the gated time-triggered mutation (SPEC.md:424, NEXT 3)")
-    ap.add_argument("--workload", default="config", choices=["config", "sweep", "union"],
+    ap.add_argument("--workload", default="config", choices=["config", "sweep", "union", "trajectories"],
                     help="sweep: the Fig. 4 delta_t sensitivity sweep (ssa_run_sweep, 1 GPU); union: selective "
                          "memory at union times over 16 HIV trajectories (ssa_run_union, Fig. 4's ensemble)")
     ap.add_argument("--kx", type=int, default=16, help="union workload: X-reduction factor k_x")
@@ -319,6 +365,8 @@ def main():
         return run_sweep_bench(args, rank, world)
     if args.workload == "union":
         return run_union_bench(args, rank, world)
+    if args.workload == "trajectories":
+        return run_traj_bench(args, rank, world)
 
     import numpy as np
     import torch
