@@ -228,7 +228,8 @@ int oracle_propensities(const oracle_model *M, const int64_t *x, double *a, int3
 /* summation orders (R13):                                         */
 /*  mode 0 "sequential": c_j = c_{j-1} + a_j left to right, a0 = c_{R-1},    */
 /*         j* = min{ j : c_j > r }.                                           */
-/*  mode 1 "warp32": P = ceil(R/32) contiguous reactions per lane l;          */
+/*  mode 1 "warp32" (mode 2 "warp16": the same with 16 lanes):              */
+/*         P = ceil(R/32) contiguous reactions per lane l;                     */
 /*         L_l = sequential sum of lane l's a_j;  Hillis-Steele inclusive     */
 /*         scan over the 32 L_l with offsets 1,2,4,8,16 gives v_l; a0 = v_31; */
 /*         lane* = min{ l : v_l > r };  p = v_{lane*-1} (0 for lane 0), then  */
@@ -253,28 +254,36 @@ static int select_sequential(const double *a, int R, double r)
     return -1; /* unreachable when r < a0 (R12) */
 }
 
-static void warp32_scan(const double *a, int R, double v[32])
+/* The warp orders with L lanes (L = 32: mode 1 "warp32", L = 16: mode 2
+ * "warp16", a half warp per trajectory): P = ceil(R/L) contiguous reactions
+ * per lane, lane sums from 0.0 in order, inclusive Hillis-Steele scan over
+ * the L lane sums with offsets 1, 2, 4, ... < L, a0 = v_{L-1}. */
+static int mode_lanes(int mode) { return mode == 2 ? 16 : 32; }
+
+static void warp_scan(const double *a, int R, int L, double v[32])
 {
-    int P = (R + 31) / 32;
-    double L[32];
-    for (int l = 0; l < 32; ++l) {
+    int P = (R + L - 1) / L;
+    if (P < 1) P = 1;
+    double lsum[32];
+    for (int l = 0; l < L; ++l) {
         double s = 0.0;
         for (int j = l * P; j < (l + 1) * P && j < R; ++j) s = s + a[j];
-        L[l] = s;
+        lsum[l] = s;
     }
-    for (int l = 0; l < 32; ++l) v[l] = L[l];
-    for (int o = 1; o < 32; o *= 2) {
+    for (int l = 0; l < L; ++l) v[l] = lsum[l];
+    for (int o = 1; o < L; o *= 2) {
         double nv[32];
-        for (int l = 0; l < 32; ++l) nv[l] = (l >= o) ? (v[l - o] + v[l]) : v[l];
-        for (int l = 0; l < 32; ++l) v[l] = nv[l];
+        for (int l = 0; l < L; ++l) nv[l] = (l >= o) ? (v[l - o] + v[l]) : v[l];
+        for (int l = 0; l < L; ++l) v[l] = nv[l];
     }
 }
 
-static int select_warp32(const double *a, int R, const double v[32], double r)
+static int select_warp(const double *a, int R, int L, const double v[32], double r)
 {
-    int P = (R + 31) / 32;
+    int P = (R + L - 1) / L;
+    if (P < 1) P = 1;
     int lane = -1;
-    for (int l = 0; l < 32; ++l) {
+    for (int l = 0; l < L; ++l) {
         if (v[l] > r) { lane = l; break; }
     }
     if (lane < 0) return -1;
@@ -290,7 +299,7 @@ static int select_warp32(const double *a, int R, const double v[32], double r)
     return -1;
 }
 
-/* Computes a0 and j* for given propensities and u2 (mode 0 or 1). */
+/* Computes a0 and j* for given propensities and u2 (mode 0, 1 or 2). */
 int oracle_select(const double *a, int32_t R, int32_t mode, double u2, double *a0_out, int32_t *j_out)
 {
     double a0, r;
@@ -301,10 +310,11 @@ int oracle_select(const double *a, int32_t R, int32_t mode, double u2, double *a
         j = (a0 > 0.0) ? select_sequential(a, R, r) : -1;
     } else {
         double v[32];
-        warp32_scan(a, R, v);
-        a0 = v[31];
+        const int L = mode_lanes(mode);
+        warp_scan(a, R, L, v);
+        a0 = v[L - 1];
         r = u2 * a0;
-        j = (a0 > 0.0) ? select_warp32(a, R, v, r) : -1;
+        j = (a0 > 0.0) ? select_warp(a, R, L, v, r) : -1;
     }
     *a0_out = a0;
     *j_out = j;
@@ -467,8 +477,8 @@ int oracle_trajectory_events(const oracle_model *M, uint64_t id, uint64_t seed, 
         if (mode == 0) {
             a0 = total_sequential(a, R);
         } else {
-            warp32_scan(a, R, v);
-            a0 = v[31];
+            warp_scan(a, R, mode_lanes(mode), v);
+            a0 = v[mode_lanes(mode) - 1];
         }
 
         /* a5 */
@@ -488,7 +498,7 @@ int oracle_trajectory_events(const oracle_model *M, uint64_t id, uint64_t seed, 
 
         /* a7 */
         double r = u2 * a0;
-        int j = (mode == 0) ? select_sequential(a, R, r) : select_warp32(a, R, v, r);
+        int j = (mode == 0) ? select_sequential(a, R, r) : select_warp(a, R, mode_lanes(mode), v, r);
 
         /* a8 */
         for (int s = 0; s < S; ++s) x[s] += M->nu[(int64_t)j * S + s];
