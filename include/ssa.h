@@ -116,7 +116,10 @@ int32_t ssa_model_n_reactions(const ssa_model* model);
 uint64_t ssa_grid_size(double t_end, double sample_dt);
 
 /* --------------------------------------------------------------- options */
-enum { SSA_PATH_AUTO = 0, SSA_PATH_THREAD = 1, SSA_PATH_WARP = 2 };
+/* THREAD: one trajectory per thread, sequential summation order; WARP: one
+ * trajectory per warp, order warp32; HALFWARP: two trajectories per warp
+ * (16 lanes each), order warp16. */
+enum { SSA_PATH_AUTO = 0, SSA_PATH_THREAD = 1, SSA_PATH_WARP = 2, SSA_PATH_HALFWARP = 3 };
 enum { SSA_REDUCE_MEAN = 1, SSA_REDUCE_VAR = 2 };
 
 /* Per-trajectory record of a dumped trajectory (a11). */
@@ -150,7 +153,7 @@ typedef struct {
 } ssa_dump;
 
 typedef struct {
-    int32_t path;                  /* SSA_PATH_*: AUTO picks THREAD for R <= 64, else WARP */
+    int32_t path;                  /* SSA_PATH_*: AUTO picks THREAD for R <= 64, HALFWARP for R <= 256, else WARP */
     int32_t device;                /* CUDA device ordinal; -1 = the calling thread's current device */
     void* stream;                  /* cudaStream_t to run on; NULL = a library-owned stream */
     uint64_t chunk;                /* trajectories per chunk (power of two); 0 = auto */
@@ -174,7 +177,7 @@ typedef struct {
     uint64_t n_errors;         /* trajectories that ended in SSA_ERR_NUMERIC / OVERFLOW */
     uint64_t first_error_id;   /* smallest erroring trajectory id (if n_errors > 0) */
     int32_t first_error_reaction; /* its reaction (numeric errors), else -1 */
-    int32_t path_used;         /* SSA_PATH_THREAD or SSA_PATH_WARP (fixes the summation order) */
+    int32_t path_used;         /* SSA_PATH_THREAD, _WARP or _HALFWARP (fixes the summation order) */
     double device_ms;          /* device time of simulation + reduction (CUDA events) */
     double ssa_ms;             /* device time inside the SSA kernels (K1/K2) */
     double jit_ms;             /* host time spent compiling the K1 kernel in this call (0 if cached) */

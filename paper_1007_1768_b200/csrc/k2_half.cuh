@@ -1,0 +1,282 @@
+// k2_half.cuh -- K2 with two trajectories per warp: a half warp (L = 16 lanes)
+// per trajectory (sm_100a, NVRTC).  Appended after k2_warp.cuh (whose
+// helpers -- k2_rx, k2_rxd, the propensity evaluators -- it uses) when the
+// generated section defines SSA_K2_HALF = 1.
+//
+// Order "warp16" (R13; oracle mode 2): lane l of the half owns
+// the P = ceil(R/16) contiguous reactions l*P + q; lane sums from 0.0, then an
+// inclusive Hillis-Steele scan over the 16 lanes (offsets 1, 2, 4, 8; the
+// shuffles are segmented with width 16), a0 = v_15, and the same speculative
+// selection as K2 within the half.  Per warp the scan, the broadcasts, the
+// division and the update/recompute passes now serve two events, which is
+// where the one-trajectory-per-warp kernel spent most of its instructions.
+//
+// Both halves execute the common path in lockstep (the shuffles are
+// full-warp); rare paths (grid crossing, end of a trajectory, refill, the
+// rounding fallback) run per half with half-warp masks.  A half with no work
+// left keeps executing the common path on a frozen, absorbed state and
+// records nothing.
+
+#if SSA_K2_HALF
+#define SSA_HL 16
+
+extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(const ssa_k2_params P)
+{
+    extern __shared__ __align__(16) unsigned char k2_smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int h = lane >> 4;                 // which half (trajectory slot) of the warp
+    const int hl = lane & 15;                // lane within the half
+    const unsigned FULL = 0xffffffffu;
+    const unsigned HALF = 0xFFFFu << (16 * h);
+    // shared: rx[R] | x0[S] | per warp, per half (x[S] | a[P][16]) | nu_off | nu_ent | dep_off | dep_ent | rxd
+    k2_rx* rx = (k2_rx*)k2_smem_raw;
+    double* x0 = (double*)(rx + SSA_R);
+    double* x = x0 + SSA_S + (size_t)warp * 2 * (SSA_S + SSA_HL * SSA_P) + (size_t)h * (SSA_S + SSA_HL * SSA_P);
+    double* a = x + SSA_S;                                     // a[q*16 + l]: reaction l*P + q
+    int* nu_off = (int*)(x0 + SSA_S + (size_t)SSA_K2_WARPS * 2 * (SSA_S + SSA_HL * SSA_P));
+    int* nu_ent = nu_off + (SSA_R + 1);
+    int* dep_off = nu_ent + P.n_ent;
+    int* dep_ent = dep_off + (SSA_R + 1);
+#if !SSA_HAS_M3
+    k2_rxd* rxd = (k2_rxd*)(k2_smem_raw + P.rxd_offset);
+#endif
+    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
+        k2_rx q;
+        q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i]; q.gw = P.gw[i];
+        rx[i] = q;
+    }
+    for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
+    for (int i = threadIdx.x; i <= SSA_R; i += SSA_K2_BLOCK) { nu_off[i] = P.nu_off[i]; dep_off[i] = P.dep_off[i]; }
+    for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_ent[i] = P.nu_ent[i];
+    for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dep_ent[i] = P.dep_ent[i];
+#if !SSA_HAS_M3
+    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
+        const ssa_u64 pk = P.pk[i];
+        const int n = (int)(pk & 3ull);
+        const int ms = (int)(pk >> 50);
+        k2_rxd d;
+        d.rate = P.rate[i];
+        d.modc = (ms != 0x3FFF) ? P.modc[i] : 0.0;
+        const int sa = n >= 1 ? (int)((pk >> 2) & 0x3FFF) : 0, sb = n >= 2 ? (int)((pk >> 18) & 0x3FFF) : 0;
+        const int ma = n >= 1 ? (int)((pk >> 16) & 3) : 0, mb = n >= 2 ? (int)((pk >> 32) & 3) : 0;
+        const int slot = (i % SSA_P) * SSA_HL + i / SSA_P;
+        d.sab = sa | (sb << 16);
+        d.sms = (ms != 0x3FFF ? ms : 0) | (slot << 16);
+        d.mab = ma | (mb << 8);
+        d.pad = 0;
+        d.gw = P.gw[i];
+        rxd[i] = d;
+    }
+#endif
+    __syncthreads();
+
+    const double INF = __longlong_as_double(0x7FF0000000000000ll);
+    const double dt = P.dt;
+    const long long K = P.K;
+    const ssa_u64 G = (ssa_u64)K + 1;
+    ssa_u64 my_events = 0, my_ties = 0;
+
+    // per-half trajectory state (uniform within the half)
+    bool live = false;
+    ssa_u64 rel = 0, id = 0, e = 0, ties = 0;
+    double t = 0.0, s_next = 0.0;
+    long long k = 0;
+    int status = 0, absorbed = 0, err_r = -1;
+#if SSA_K2_DUMP
+    long long slot = -1;
+    ssa_u64 hash = SSA_FNV_OFFSET;
+#endif
+    double Ec = 0.0, U2c = 0.0;
+
+    // a1 for this half: take the next id and initialise (half-warp collective)
+    auto start = [&]() {
+        ssa_u64 r0 = 0;
+        if (hl == 0) r0 = atomicAdd(P.work, 1ull);
+        rel = __shfl_sync(HALF, r0, 0, SSA_HL);
+        live = rel < P.n_ids;
+        id = P.id_begin + rel;
+#if SSA_K2_DUMP
+        slot = (live && P.n_dump) ? ssa_dump_slot(P.dump_ids, P.n_dump, id) : -1ll;
+        hash = SSA_FNV_OFFSET;
+#endif
+        for (int s = hl; s < SSA_S; s += SSA_HL) x[s] = x0[s];
+        __syncwarp(HALF);
+#pragma unroll
+        for (int q = 0; q < SSA_P; ++q) {
+            const int j = hl * SSA_P + q;
+            a[q * SSA_HL + hl] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+        }
+        __syncwarp(HALF);
+        t = 0.0; s_next = 0.0; e = 0; ties = 0; k = 0;
+        status = 0; absorbed = 0; err_r = -1;
+    };
+    start();
+
+    while (__any_sync(FULL, live)) {
+        // a2, amortised per half: lane l draws event e0 + l for the next 16 events
+        if ((e & 15ull) == 0) {
+            const ssa_u64 ee = e + (ssa_u64)hl;
+            const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)ee, (ssa_u32)(ee >> 32), (ssa_u32)id,
+                                                       (ssa_u32)(id >> 32), P.key0, P.key1);
+            Ec = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
+            U2c = ssa_u53(o.o3, o.o2);
+        }
+        // a4: lane sum, scan over the half (width 16)
+        double L = 0.0;
+#pragma unroll
+        for (int q = 0; q < SSA_P; ++q) L = __dadd_rn(L, a[q * SSA_HL + hl]);
+        double v = L;
+#pragma unroll
+        for (int o = 1; o < SSA_HL; o <<= 1) {
+            const double y = __shfl_up_sync(FULL, v, o, SSA_HL);
+            if (hl >= o) v = __dadd_rn(y, v);
+        }
+        const double a0 = __shfl_sync(FULL, v, SSA_HL - 1, SSA_HL);
+        // a5
+        const int src = (int)(e & 15ull);
+        const double E = __shfl_sync(FULL, Ec, src, SSA_HL);
+        const double u2 = __shfl_sync(FULL, U2c, src, SSA_HL);
+        const unsigned a0hi = (unsigned)__double2hiint(a0);
+        const bool fast = a0hi - (123u << 20) < ((1923u - 123u) << 20);   // a0 in [2^-900, 2^901)
+        double tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
+        // a7, speculatively in every lane (full warp: both halves)
+        const double r = __dmul_rn(u2, a0);
+        const double vprev = __shfl_up_sync(FULL, v, 1, SSA_HL);
+        double p = (hl > 0) ? vprev : 0.0;
+        int over = 0;
+#pragma unroll
+        for (int q = 0; q < SSA_P; ++q) {
+            p = __dadd_rn(p, a[q * SSA_HL + hl]);
+            over += (p > r) ? 1 : 0;
+        }
+        const int jl = over ? SSA_P - over : -1;
+        const unsigned bal = (__ballot_sync(FULL, v > r) >> (16 * h)) & 0xFFFFu;
+        const int ls = bal ? __ffs(bal) - 1 : 0;
+        const int jq = __shfl_sync(FULL, jl, ls, SSA_HL);
+
+        bool apply = live;
+        if (live && (!fast || tn > s_next)) {     // rare path of this half
+            bool fin = false;
+            if (!fast) {
+                if (a0 > 0.0 && a0 < INF) {
+                    tn = __dadd_rn(t, __ddiv_rn(E, a0));
+                } else if (a0 == 0.0) {
+                    tn = INF;
+                    absorbed = 1;
+                } else {
+                    status = 1;
+                    int bad = SSA_R;
+#pragma unroll
+                    for (int q = SSA_P - 1; q >= 0; --q)
+                        if (hl * SSA_P + q < SSA_R && !(fabs(a[q * SSA_HL + hl]) < INF)) bad = hl * SSA_P + q;
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(HALF, bad, o, SSA_HL));
+                    err_r = bad < SSA_R ? bad : -1;
+                    fin = true;
+                }
+            }
+            if (!fin && tn > s_next) {
+                do {
+                    const double tol = __dmul_rn(1e-9, s_next);
+                    const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
+                                      (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
+                    ties += near ? 1 : 0;
+                    int ovf = 0;
+                    for (int s = hl; s < SSA_S; s += SSA_HL) {
+                        const double xv = x[s];
+                        ovf |= (xv > 2147483647.0) ? 1 : 0;
+                        P.staging[((ssa_u64)k * SSA_S + s) * P.stride + rel] = (int)xv;
+#if SSA_K2_DUMP
+                        if (slot >= 0) P.dump_states[((ssa_u64)slot * G + (ssa_u64)k) * SSA_S + s] = (int)xv;
+#endif
+                    }
+                    if (__any_sync(HALF, ovf)) status = 2;
+#if SSA_K2_DUMP
+                    if (slot >= 0 && hl == 0) {
+                        P.dump_e[(ssa_u64)slot * G + (ssa_u64)k] = e;
+                        P.dump_t[(ssa_u64)slot * G + (ssa_u64)k] = (e > 0) ? t : 0.0;
+                    }
+#endif
+                    ++k;
+                    s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+                } while (tn > s_next);
+                fin = (k > K);
+            }
+            if (fin) {
+                // trajectory done: records, then refill this half
+                if (hl == 0) {
+                    my_events += e;
+                    my_ties += ties;
+#if SSA_K2_DUMP
+                    if (slot >= 0) {
+                        ssa_dev_summary sm;
+                        sm.events = e; sm.hash = hash; sm.t_last = t; sm.near_ties = ties;
+                        sm.absorbed = absorbed; sm.status = status == 1 ? 3 : (status == 2 ? 4 : 0);
+                        sm.err_reaction = err_r; sm.pad = 0;
+                        P.dump_sum[slot] = sm;
+                    }
+#endif
+                    if (status) {
+                        const ssa_u64 code = status == 1 ? SSA_DEV_ERR_NUMERIC : SSA_DEV_ERR_OVERFLOW;
+                        atomicAdd(&P.stats->n_errors, 1ull);
+                        atomicOr(&P.stats->err_code, code);
+                        const ssa_u64 packed = (id << 24) | (code << 20) | ((ssa_u64)(err_r + 1) & 0xFFFFFull);
+                        atomicMin(&P.stats->first_err_id, packed);
+                    }
+                }
+                start();
+                apply = false;
+            }
+        }
+        if (apply) {
+            int j;
+            if (jq >= 0) {
+                j = ls * SSA_P + jq;
+            } else {
+                // rounding fallback (rare): the largest j <= lane*'s last index with a_j > 0
+                int lp = -1;
+#pragma unroll
+                for (int q = 0; q < SSA_P; ++q)
+                    if (a[q * SSA_HL + hl] > 0.0) lp = hl * SSA_P + q;
+                const unsigned m2 = (__ballot_sync(HALF, lp >= 0 && hl <= ls) >> (16 * h)) & 0xFFFFu;
+                j = __shfl_sync(HALF, lp, 31 - __clz(m2), SSA_HL);
+            }
+            // a8: state update (lane t of the half takes the t-th net change)
+            const int nb = nu_off[j], ne = nu_off[j + 1];
+            for (int q = nb + hl; q < ne; q += SSA_HL) {
+                const int ent = nu_ent[q];
+                const int sp = ent & 0xFFFF;
+                x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));
+            }
+            __syncwarp(HALF);
+            // a3: the half recomputes dep(j)
+            const int db = dep_off[j], de = dep_off[j + 1];
+            for (int q = db + hl; q < de; q += SSA_HL) {
+                const int jj = dep_ent[q];
+#if !SSA_HAS_M3
+                const k2_rxd d = rxd[jj];
+                a[(unsigned)d.sms >> 16] = k2_propensity_d(d, x);
+#else
+                const int l = jj / SSA_P, qq = jj - l * SSA_P;
+                a[qq * SSA_HL + l] = k2_propensity(rx[jj], x);
+#endif
+            }
+            __syncwarp(HALF);
+            t = tn;
+            ++e;
+#if SSA_K2_DUMP
+            hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
+#endif
+        }
+        __syncwarp();
+    }
+    // per-warp counter totals (lanes 0 and 16 hold their halves' sums)
+    my_events += __shfl_down_sync(FULL, my_events, 16);
+    my_ties += __shfl_down_sync(FULL, my_ties, 16);
+    if (lane == 0) {
+        atomicAdd(&P.stats->events, my_events);
+        if (my_ties) atomicAdd(&P.stats->near_ties, my_ties);
+    }
+}
+#endif

@@ -124,6 +124,7 @@ static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const dou
 
 #define SSA_K2_WARPS (SSA_K2_BLOCK / 32)
 
+#if !SSA_K2_HALF
 extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(const ssa_k2_params P)
 {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
@@ -382,3 +383,4 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         if (my_ties) atomicAdd(&P.stats->near_ties, my_ties);
     }
 }
+#endif  // !SSA_K2_HALF

@@ -81,6 +81,7 @@ struct K2Kernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t fn = nullptr;
     size_t smem = 0;
+    size_t rxd_offset = 0;
     int blocks_per_sm = 0;
 };
 
@@ -611,26 +612,35 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
     return SSA_OK;
 }
 
+// SSA_PATH_AUTO: the thread path for R <= 64 (registers hold the prefix),
+// two trajectories per warp for R <= 256 (P = ceil(R/16) <= 16), else one
+// trajectory per warp.
+static int auto_path(const ssa_model& m)
+{
+    return m.R <= 64 ? SSA_PATH_THREAD : (m.R <= 256 ? SSA_PATH_HALFWARP : SSA_PATH_WARP);
+}
+
 // requires: current device == dev, m.mu held.  The K2 tables live in one
 // device block whose image is kept in page-locked host memory; every run
 // re-uploads it (the run's model inputs) with one async copy.  The kernel
 // itself is NVRTC-compiled per (block, dump) with S, R and P baked in.
 // dynamic shared memory of K2: rx[R] (32 B) | x0[S] | per warp (x[S] | a[32P]) |
 // nu_off | nu_ent | dep_off | dep_ent | (16-byte aligned) decoded descriptors [R] (40 B)
-static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block)
+static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false)
 {
     const size_t warps = (size_t)(block / 32);
-    const size_t b = 32 * (size_t)R + 8 * (size_t)S + warps * 8 * ((size_t)S + 32 * (size_t)P) +
+    const size_t per_warp = half ? 2 * ((size_t)S + 16 * (size_t)P) : ((size_t)S + 32 * (size_t)P);
+    const size_t b = 32 * (size_t)R + 8 * (size_t)S + warps * 8 * per_warp +
                      4 * ((size_t)R + 1 + (size_t)n_ent + (size_t)R + 1 + (size_t)n_dep);
     return (b + 15) & ~(size_t)15;
 }
 
-static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block)
+static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false)
 {
-    return k2_rxd_offset(S, R, P, n_ent, n_dep, block) + 40 * (size_t)R;
+    return k2_rxd_offset(S, R, P, n_ent, n_dep, block, half) + 40 * (size_t)R;
 }
 
-static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump)
+static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump, bool half)
 {
     // longest net-change list and longest per-reaction dependency list (as
     // built by ensure_k2), and whether any reactant has coefficient 3
@@ -656,21 +666,24 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
     std::ostringstream o;
     o << "#define SSA_S " << m.S << "\n#define SSA_R " << m.R << "\n#define SSA_P " << P << "\n#define SSA_K2_BLOCK "
       << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0)
+      << "\n#define SSA_K2_HALF " << (half ? 1 : 0)
       << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
     return o.str();
 }
 
-static std::string k2_full_source(const ssa_model& m, int P, int block, int minb, bool dump)
+// half: two trajectories per warp (k2_half.cuh, order warp16), P = ceil(R/16)
+static std::string k2_full_source(const ssa_model& m, int P, int block, int minb, bool dump, bool half = false)
 {
-    return std::string(kSsaDeviceSrc) + "\n" + gen_k2_model(m, P, block, minb, dump) + "\n" + kK2WarpSrc;
+    return std::string(kSsaDeviceSrc) + "\n" + gen_k2_model(m, P, block, minb, dump, half) + "\n" + kK2WarpSrc +
+           "\n" + kK2HalfSrc;
 }
 
 // minb: the __launch_bounds__ residency target (1 = let the compiler use the
 // registers it wants)
 static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bool dump, K2Dev** out,
-                            K2Kernel** kout, double* jit_ms)
+                            K2Kernel** kout, double* jit_ms, bool half = false)
 {
     K2Dev& k = m.dev[dev].k2;
     const int R = m.R, S = m.S;
@@ -770,17 +783,21 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         k.ready = true;
     }
     *out = &k;
-    const std::string key = std::to_string(block) + "/" + std::to_string(minb) + "/" + (dump ? "1" : "0");
+    const std::string key = std::to_string(block) + "/" + std::to_string(minb) + "/" + (dump ? "1" : "0") + "/" +
+                            (half ? "h" : "w");
+    const int PL = half ? std::max(1, (R + 15) / 16) : k.P;
     auto it = k.kern.find(key);
     if (it == k.kern.end()) {
         auto t0 = std::chrono::steady_clock::now();
         K2Kernel kk;
         std::vector<char> cubin;
         std::string log;
-        TRY(nvrtc_compile(k2_full_source(m, k.P, block, minb, dump), cubin, log));
+        if (half && PL > 16) return fail(SSA_ERR_UNSUPPORTED, "half-warp path supports at most 256 reactions (got %d)", R);
+        TRY(nvrtc_compile(k2_full_source(m, PL, block, minb, dump, half), cubin, log));
         CU(cudaLibraryLoadData(&kk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
         CU(cudaLibraryGetKernel(&kk.fn, kk.lib, "ssa_k2"));
-        kk.smem = k2_smem_bytes(S, R, k.P, k.n_ent, k.n_dep, block);
+        kk.smem = k2_smem_bytes(S, R, PL, k.n_ent, k.n_dep, block, half);
+        kk.rxd_offset = k2_rxd_offset(S, R, PL, k.n_ent, k.n_dep, block, half);
         if (kk.smem > 227 * 1024)
             return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", kk.smem);
         CU(cudaFuncSetAttribute((const void*)kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kk.smem));
@@ -942,8 +959,9 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     const ssa_u64 span = next_pow2(n_ids);
     const ssa_u64 budget = (o && o->staging_budget_bytes) ? o->staging_budget_bytes : (32ull << 30);
     int path = o ? o->path : SSA_PATH_AUTO;
-    if (path == SSA_PATH_AUTO) path = (m->R <= 64) ? SSA_PATH_THREAD : SSA_PATH_WARP;
-    if (path != SSA_PATH_THREAD && path != SSA_PATH_WARP) return fail(SSA_ERR_INVALID_ARG, "bad path %d", path);
+    if (path == SSA_PATH_AUTO) path = auto_path(*m);
+    if (path != SSA_PATH_THREAD && path != SSA_PATH_WARP && path != SSA_PATH_HALFWARP)
+        return fail(SSA_ERR_INVALID_ARG, "bad path %d", path);
     info.path = path;
     ssa_u64 C = span;
     if (rec && (path != SSA_PATH_THREAD || sw))
@@ -994,14 +1012,16 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             grid = sms * bps;
             grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + block - 1) / block);
         } else {
-            // default residency 4 x 256 threads (64 registers; measured best on B200)
-            const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : 4;
-            TRY(ensure_k2(*m, c.device, block, minb, dump && dump->n > 0, &k2, &k2k, &info.jit_ms));
+            // default residency: 4 x 256 threads for one trajectory per warp (64
+            // registers), 3 x 256 for two per warp (80 registers)
+            const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : (path == SSA_PATH_HALFWARP ? 3 : 4);
+            TRY(ensure_k2(*m, c.device, block, minb, dump && dump->n > 0, &k2, &k2k, &info.jit_ms,
+                          path == SSA_PATH_HALFWARP));
             int bps = k2k->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
-            const int wpb = block / 32;
+            const int tpb = (block / 32) * (path == SSA_PATH_HALFWARP ? 2 : 1);   // trajectories per block
             grid = sms * bps;
-            grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + wpb - 1) / wpb);
+            grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + tpb - 1) / tpb);
         }
     }
     grid = std::max(grid, 1);
@@ -1117,7 +1137,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             p.n_ent = k2->n_ent; p.n_dep = k2->n_dep;
             p.pk = k2->pk; p.gw = k2->gw; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
             p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
-            p.rxd_offset = k2_rxd_offset(m->S, m->R, k2->P, k2->n_ent, k2->n_dep, block);
+            p.rxd_offset = k2k->rxd_offset;
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
@@ -1306,7 +1326,8 @@ extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const 
     if (!rates) return fail(SSA_ERR_INVALID_ARG, "rates is null");
     if (n_per_point == 0) return fail(SSA_ERR_INVALID_ARG, "n_per_point must be >= 1");
     if ((ssa_u64)n_points * n_per_point > (1ull << 40)) return fail(SSA_ERR_INVALID_ARG, "n_points * n_per_point > 2^40");
-    if (o && o->path == SSA_PATH_WARP) return fail(SSA_ERR_UNSUPPORTED, "parameter sweeps run on the thread path");
+    if (o && (o->path == SSA_PATH_WARP || o->path == SSA_PATH_HALFWARP))
+        return fail(SSA_ERR_UNSUPPORTED, "parameter sweeps run on the thread path");
     const size_t R = (size_t)m->R;
     for (size_t i = 0; i < (size_t)n_points * R; ++i) {
         if (!std::isfinite(rates[i]) || rates[i] < 0.0)
@@ -1361,7 +1382,8 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     *n_points = 0;
     if (n_trajectories == 0 || n_trajectories > (1ull << 24)) return fail(SSA_ERR_INVALID_ARG, "n_trajectories not in [1, 2^24]");
     if (thin_kx == 0) return fail(SSA_ERR_INVALID_ARG, "thin_kx must be >= 1");
-    if (o && o->path == SSA_PATH_WARP) return fail(SSA_ERR_UNSUPPORTED, "event recording runs on the thread path");
+    if (o && (o->path == SSA_PATH_WARP || o->path == SSA_PATH_HALFWARP))
+        return fail(SSA_ERR_UNSUPPORTED, "event recording runs on the thread path");
     if (o && o->dump) return fail(SSA_ERR_INVALID_ARG, "ssa_run_union takes no dump");
     Ctx c;
     TRY(setup_ctx(o, c));
@@ -1489,7 +1511,8 @@ extern "C" ssa_status ssa_run_trajectories(const ssa_model* m, uint64_t n_trajec
     *n_points = 0;
     if (n_trajectories == 0 || n_trajectories > (1ull << 23)) return fail(SSA_ERR_INVALID_ARG, "n_trajectories not in [1, 2^23]");
     if (stride == 0) return fail(SSA_ERR_INVALID_ARG, "stride must be >= 1");
-    if (o && o->path == SSA_PATH_WARP) return fail(SSA_ERR_UNSUPPORTED, "trajectory output runs on the thread path");
+    if (o && (o->path == SSA_PATH_WARP || o->path == SSA_PATH_HALFWARP))
+        return fail(SSA_ERR_UNSUPPORTED, "trajectory output runs on the thread path");
     if (o && o->dump) return fail(SSA_ERR_INVALID_ARG, "ssa_run_trajectories takes no dump");
     Ctx c;
     TRY(setup_ctx(o, c));
@@ -1609,7 +1632,7 @@ extern "C" ssa_status ssa_model_prepare(const ssa_model* m, int32_t device, int3
     o.device = device;
     Ctx c;
     TRY(setup_ctx(&o, c));
-    if (path == SSA_PATH_AUTO) path = (m->R <= 64) ? SSA_PATH_THREAD : SSA_PATH_WARP;
+    if (path == SSA_PATH_AUTO) path = auto_path(*m);
     std::lock_guard<std::mutex> lk(m->mu);
     if (path == SSA_PATH_THREAD) {
         K1Entry* e = nullptr;
@@ -1617,7 +1640,8 @@ extern "C" ssa_status ssa_model_prepare(const ssa_model* m, int32_t device, int3
     }
     K2Dev* k = nullptr;
     K2Kernel* kk = nullptr;
-    return ensure_k2(*m, c.device, SSA_K2_BLOCK, 4, false, &k, &kk, nullptr);
+    return ensure_k2(*m, c.device, SSA_K2_BLOCK, path == SSA_PATH_HALFWARP ? 3 : 4, false, &k, &kk, nullptr,
+                     path == SSA_PATH_HALFWARP);
 }
 
 // ------------------------------------------------------------------ misc
@@ -1670,7 +1694,9 @@ extern "C" const char* ssa_debug_k2_source(const ssa_model* m, int32_t block, in
 {
     static thread_local std::string s;
     if (!m) return "";
-    s = k2_full_source(*m, std::max(1, (m->R + 31) / 32), block, 1, dump != 0);
+    // dump: bit 0 = the dump variant, bit 1 = two trajectories per warp (HALFWARP)
+    const bool half = (dump & 2) != 0;
+    s = k2_full_source(*m, std::max(1, (m->R + (half ? 15 : 31)) / (half ? 16 : 32)), block, 1, (dump & 1) != 0, half);
     return s.c_str();
 }
 
@@ -1680,7 +1706,10 @@ extern "C" ssa_status ssa_debug_k2_compile(const ssa_model* m, int32_t block, in
     if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
     std::vector<char> cubin;
     std::string lg;
-    ssa_status st = nvrtc_compile(k2_full_source(*m, std::max(1, (m->R + 31) / 32), block, 1, dump != 0), cubin, lg);
+    const bool half = (dump & 2) != 0;
+    ssa_status st = nvrtc_compile(
+        k2_full_source(*m, std::max(1, (m->R + (half ? 15 : 31)) / (half ? 16 : 32)), block, 1, (dump & 1) != 0, half),
+        cubin, lg);
     if (log && log_cap) {
         std::string all = (st == SSA_OK) ? lg : g_err;
         strncpy(log, all.c_str(), (size_t)log_cap - 1);

@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libssa.so")
 
 SSA_OK = 0
-SSA_PATH_AUTO, SSA_PATH_THREAD, SSA_PATH_WARP = 0, 1, 2
+SSA_PATH_AUTO, SSA_PATH_THREAD, SSA_PATH_WARP, SSA_PATH_HALFWARP = 0, 1, 2, 3
 SSA_REDUCE_MEAN, SSA_REDUCE_VAR = 1, 2
 STATUS_NAMES = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARG", 2: "SSA_ERR_MODEL", 3: "SSA_ERR_NUMERIC",
                 4: "SSA_ERR_OVERFLOW", 5: "SSA_ERR_OOM", 6: "SSA_ERR_CUDA", 7: "SSA_ERR_JIT",
@@ -199,13 +199,13 @@ class Model:
         seed >= 0: the variant with that seed's Philox key schedule compiled in)."""
         return lib().ssa_debug_k1_source(self.handle, block, minb, int(dump), seed).decode()
 
-    def k2_source(self, block: int = 256, dump: bool = False) -> str:
-        """Generated K2 (warp path) source."""
-        return _k2_source(self, block, dump)
+    def k2_source(self, block: int = 256, dump: bool = False, half: bool = False) -> str:
+        """Generated K2 (warp path; half=True: two trajectories per warp) source."""
+        return _k2_source(self, block, int(dump) | (2 if half else 0))
 
-    def k2_compile(self, block: int = 256, dump: bool = False):
+    def k2_compile(self, block: int = 256, dump: bool = False, half: bool = False):
         """NVRTC-compile the model's K2 kernel (no device needed); returns (status, log, cubin bytes)."""
-        return _k2_compile(self, block, dump)
+        return _k2_compile(self, block, int(dump) | (2 if half else 0))
 
     def k1_compile(self, block: int = 128, minb: int = 4, dump: bool = False):
         """NVRTC-compile the model's K1 kernel (no device needed); returns (status, log, cubin bytes)."""
@@ -215,14 +215,14 @@ class Model:
         return st, buf.value.decode(errors="replace"), nb.value
 
 
-def _k2_source(model, block: int = 256, dump: bool = False) -> str:
-    return lib().ssa_debug_k2_source(model.handle, block, int(dump)).decode()
+def _k2_source(model, block: int = 256, flags: int = 0) -> str:
+    return lib().ssa_debug_k2_source(model.handle, block, int(flags)).decode()
 
 
-def _k2_compile(model, block: int = 256, dump: bool = False):
+def _k2_compile(model, block: int = 256, flags: int = 0):
     buf = C.create_string_buffer(1 << 16)
     nb = C.c_uint64()
-    st = lib().ssa_debug_k2_compile(model.handle, block, int(dump), buf, len(buf), C.byref(nb))
+    st = lib().ssa_debug_k2_compile(model.handle, block, int(flags), buf, len(buf), C.byref(nb))
     return st, buf.value.decode(errors="replace"), nb.value
 
 

@@ -13,8 +13,8 @@ from .helpers import assert_dump_equal, assert_moments_close, exact_moments, ora
 
 pytestmark = pytest.mark.gpu
 
-THREAD, WARP = 1, 2
-MODE = {THREAD: 0, WARP: 1}
+THREAD, WARP, HALF = 1, 2, 3
+MODE = {THREAD: 0, WARP: 1, HALF: 2}     # summation orders: sequential, warp32, warp16
 
 
 @pytest.fixture(scope="module")
@@ -44,13 +44,13 @@ def _parity(S, net, n, t_end, dt, seed, path, dump_ids=None, **opts):
 
 
 # ------------------------------------------------------------ configs 0 and 1
-@pytest.mark.parametrize("path", [THREAD, WARP])
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_config0_full_parity(S, path):
     cfg = inputs.config(0)
     _parity(S, cfg.network, cfg.n_trajectories, cfg.t_end, cfg.dt, cfg.seed, path)
 
 
-@pytest.mark.parametrize("path", [THREAD, WARP])
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_config1_parity_ragged(S, path):
     """Several reduction tiles and a ragged tail (5000 = 2*2048 + 904)."""
     cfg = inputs.config(1)
@@ -65,7 +65,7 @@ def test_config1_full_size(S):
 
 
 # ------------------------------------------------------------ HIV (configs 2, 4)
-@pytest.mark.parametrize("path", [THREAD, WARP])
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_hiv_short_horizon_parity(S, path):
     cfg = inputs.config(2)
     _parity(S, cfg.network, 300, 5.0, cfg.dt, cfg.seed, path)
@@ -146,6 +146,13 @@ def test_config4_shards_sampled(S):
 def test_config3_warp_parity(S):
     cfg = inputs.config(3)
     _parity(S, cfg.network, 96, cfg.t_end, cfg.dt, cfg.seed, WARP)
+
+
+def test_config3_halfwarp_parity(S):
+    """Config 3 on the half-warp path (two trajectories per warp, order
+    warp16), with an odd count so the last warp has one idle half."""
+    cfg = inputs.config(3)
+    _parity(S, cfg.network, 97, cfg.t_end, cfg.dt, cfg.seed, HALF)
 
 
 def test_config3_thread_parity(S):
@@ -236,11 +243,11 @@ def test_edge_cases(S):
     assert np.all(r.mean == np.array([7, 0, 3])) and np.all(r.var == 0)
     assert np.all(r.dump.summary["absorbed"] == 1) and r.events == 0
     # pure death to extinction (absorbing mid-run), both paths
-    for path in (THREAD, WARP):
+    for path in (THREAD, WARP, HALF):
         _parity(S, inputs.pure_death(1.0, 5), 257, 10.0, 0.5, 3, path)
 
 
-@pytest.mark.parametrize("path", [THREAD, WARP])
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_trimolecular_and_modifier_network(S, path):
     """Reactant coefficient 3 (C(x,3)), a bimolecular 2A term, a catalyst and a
     negative rate modifier on a small network, both paths (the warp path then
@@ -263,7 +270,7 @@ def test_numeric_error_reported(S):
         _rx([(0, 1)], [(0, 2)], 1e308),           # A doubles; a = 1e308 * A overflows at A = 2
     ))
     m = S.Model(net)
-    for path in (THREAD, WARP):
+    for path in (THREAD, WARP, HALF):
         r = S.run(m, 8, 10.0, 1.0, 1, path=path, dump_ids=np.arange(8), raise_on_error=False)
         assert r.status == 3 and r.n_errors == 8
         assert r.first_error_id == 0 and r.first_error_reaction == 1
@@ -295,7 +302,7 @@ def test_device_outputs_and_determinism(S):
 
 
 # ------------------------------------------------------------ gated propensities (NEXT 3)
-@pytest.mark.parametrize("path", [THREAD, WARP])
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_gated_networks_parity(S, path):
     """SPEC.md:424-style gates and the mass-action switch on both paths,
     bit-exact against the oracle: the one-shot event, constant-rate depletion,
