@@ -57,16 +57,20 @@ def alg_instr_per_event(net, path: int) -> float:
     return philox + u53 + plog + tau + props + prefix + select + update + rest
 
 
-def alg_warp_instr_per_event(net) -> float:
-    """Algorithmic WARP-instructions per applied event of the warp path (K2,
-    DESIGN.md §7): one trajectory per warp, P = ceil(R/32) propensities per
-    lane.  Lane sum (P loads + P adds), 5-step scan (2 shuffles + add), 3
-    broadcasts, tau (IEEE divide 9 + add), grid check, r, selection (P adds +
-    P compares + vprev shuffle + ballot/ffs/broadcast), update and dependency
-    recompute (one lane-parallel pass each), Philox + u53 + plog amortised
-    over 32 events, loop."""
-    P = max(1, -(-net.R // 32))
-    return 2 * P + 15 + 6 + 10 + 2 + (2 * P + 5) + 5 + 15 + 78 / 32 + 3
+def alg_warp_instr_per_event(net, lanes: int = 32) -> float:
+    """Algorithmic WARP-instructions per applied event of the warp paths (K2,
+    DESIGN.md §7), `lanes` = 32 (one trajectory per warp, order warp32) or 16
+    (two per warp, order warp16), P = ceil(R/lanes) propensities per lane.
+    Per warp iteration: lane sum (P loads + P adds), log2(lanes)-step scan (2
+    shuffles + add), 3 broadcasts, tau (IEEE divide 9 + add), grid check, r,
+    selection (P adds + P compares + vprev shuffle + ballot/ffs/broadcast),
+    update and dependency recompute (one lane-parallel pass each), Philox +
+    u53 + plog amortised over `lanes` events, loop; divided by the
+    32/lanes trajectories a warp advances per iteration."""
+    P = max(1, -(-net.R // lanes))
+    steps = 5 if lanes == 32 else 4
+    per_iter = 2 * P + 3 * steps + 6 + 10 + 2 + (2 * P + 5) + 5 + 15 + 78 / lanes + 3
+    return per_iter / (32 // lanes)
 
 
 class ClockSampler:
@@ -492,11 +496,11 @@ def main():
         I = alg_instr_per_event(net, path)                                # thread-instructions per event
         achieved = per_rank_events * I / 32.0 / (k1_ms / 1e3) / 1e9      # G warp-instr/s
     else:
-        I = alg_warp_instr_per_event(net)                                 # warp-instructions per event
+        I = alg_warp_instr_per_event(net, 16 if path == 3 else 32)        # warp-instructions per event
         achieved = per_rank_events * I / (k1_ms / 1e3) / 1e9
     peak = n_sm * 4 * sm_max * 1e6 / 1e9                                  # G warp-instr/s
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "ssa_k1" if path == 1 else "ssa_k2",
+                "traffic": None, "kernel": "ssa_k1" if path == 1 else ("ssa_k2" if path == 2 else "ssa_k2 (half-warp)"),
                 ("alg_thread_instr_per_event" if path == 1 else "alg_warp_instr_per_event"): I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
 
@@ -526,7 +530,7 @@ def main():
         "config": {"workload": f"config{args.config}-{cfg.name}" + ("-variantB" if args.variant == "B" else ""),
                    "model": net.name, "species": net.S,
                    "reactions": net.R, "n_trajectories_per_gpu": n_per, "global_batch": n_total, "t_end": t_end,
-                   "sample_dt": dt, "grid_points": G, "seed": cfg.seed, "path": "thread" if path == 1 else "warp",
+                   "sample_dt": dt, "grid_points": G, "seed": cfg.seed, "path": {1: "thread", 2: "warp", 3: "halfwarp"}[path],
                    "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)"},
         "trajectories_per_s": traj_per_s,
         "events_per_step": events / args.steps,

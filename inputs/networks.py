@@ -202,7 +202,7 @@ class Config:
     t_end: float
     dt: float
     seed: int
-    path: int          # 1 thread path, 2 warp path
+    path: int          # 1 thread path, 2 warp path, 3 half-warp path
     n_dump: int = 0
 
 
@@ -211,7 +211,7 @@ def configs() -> List[Config]:
         Config(0, "immigration-death", immigration_death(), 1000, 100.0, 1.0, 1, 1),
         Config(1, "dimerization-decay", dimerization(), 65536, 20.0, 0.1, 2, 1),
         Config(2, "hiv-100d", hiv(), 1 << 18, 100.0, 1.0, 3, 1),
-        Config(3, "synthetic-64x256", synthetic(64, 256, 4), 1 << 20, 10.0, 0.05, 4, 2),
+        Config(3, "synthetic-64x256", synthetic(64, 256, 4), 1 << 20, 10.0, 0.05, 4, 3),
         Config(4, "hiv-400d-box", hiv(), 1 << 24, 400.0, 1.0, 5, 1, 65536),
     ]
 
