@@ -30,8 +30,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     const unsigned FULL = 0xffffffffu;
     const unsigned HALF = 0xFFFFu << (16 * h);
     // shared: rx[R] | x0[S] | per warp, per half (x[S] | a[P][16]) | nu_off | nu_ent | dep_off | dep_ent | rxd
+    // the packed table rx is needed only by the general evaluator (coefficient-3 models)
     k2_rx* rx = (k2_rx*)k2_smem_raw;
-    double* x0 = (double*)(rx + SSA_R);
+    double* x0 = (double*)(rx + (SSA_HAS_M3 ? SSA_R : 0));
     double* x = x0 + SSA_S + (size_t)warp * 2 * (SSA_S + SSA_HL * SSA_P) + (size_t)h * (SSA_S + SSA_HL * SSA_P);
     double* a = x + SSA_S;                                     // a[q*16 + l]: reaction l*P + q
     int* nu_off = (int*)(x0 + SSA_S + (size_t)SSA_K2_WARPS * 2 * (SSA_S + SSA_HL * SSA_P));
@@ -41,11 +42,15 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #if !SSA_HAS_M3
     k2_rxd* rxd = (k2_rxd*)(k2_smem_raw + P.rxd_offset);
 #endif
+#if SSA_HAS_M3
     for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
         k2_rx q;
         q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i]; q.gw = P.gw[i];
         rx[i] = q;
     }
+#else
+    (void)rx;
+#endif
     for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
     for (int i = threadIdx.x; i <= SSA_R; i += SSA_K2_BLOCK) { nu_off[i] = P.nu_off[i]; dep_off[i] = P.dep_off[i]; }
     for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_ent[i] = P.nu_ent[i];
@@ -105,7 +110,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #pragma unroll
         for (int q = 0; q < SSA_P; ++q) {
             const int j = hl * SSA_P + q;
+#if SSA_HAS_M3
             a[q * SSA_HL + hl] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+#else
+            a[q * SSA_HL + hl] = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
+#endif
         }
         __syncwarp(HALF);
         t = 0.0; s_next = 0.0; e = 0; ties = 0; k = 0;

@@ -132,8 +132,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     const int warp = threadIdx.x >> 5;
     const unsigned FULL = 0xffffffffu;
     // shared: rx[R] | x0[S] | per warp (x[S] | a[P][32]) | nu_off[R+1] | nu_ent | dep_off[R+1] | dep_ent
+    // the packed table rx is needed only by the general evaluator (coefficient-3 models)
     k2_rx* rx = (k2_rx*)k2_smem_raw;
-    double* x0 = (double*)(rx + SSA_R);
+    double* x0 = (double*)(rx + (SSA_HAS_M3 ? SSA_R : 0));
     double* x = x0 + SSA_S + (size_t)warp * (SSA_S + 32 * SSA_P);
     double* a = x + SSA_S;                                     // a[q*32 + l]: reaction l*P + q
     int* nu_off = (int*)(x0 + SSA_S + (size_t)SSA_K2_WARPS * (SSA_S + 32 * SSA_P));
@@ -143,11 +144,15 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #if !SSA_HAS_M3
     k2_rxd* rxd = (k2_rxd*)(k2_smem_raw + P.rxd_offset);   // 16-byte aligned, after dep_ent
 #endif
+#if SSA_HAS_M3
     for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
         k2_rx q;
         q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i]; q.gw = P.gw[i];
         rx[i] = q;
     }
+#else
+    (void)rx;
+#endif
     for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
     for (int i = threadIdx.x; i <= SSA_R; i += SSA_K2_BLOCK) { nu_off[i] = P.nu_off[i]; dep_off[i] = P.dep_off[i]; }
     for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_ent[i] = P.nu_ent[i];
@@ -195,7 +200,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #pragma unroll
         for (int q = 0; q < SSA_P; ++q) {
             const int j = lane * SSA_P + q;
+#if SSA_HAS_M3
             a[q * 32 + lane] = (j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+#else
+            a[q * 32 + lane] = (j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
+#endif
         }
         __syncwarp();
 

@@ -626,18 +626,27 @@ static int auto_path(const ssa_model& m)
 // itself is NVRTC-compiled per (block, dump) with S, R and P baked in.
 // dynamic shared memory of K2: rx[R] (32 B) | x0[S] | per warp (x[S] | a[32P]) |
 // nu_off | nu_ent | dep_off | dep_ent | (16-byte aligned) decoded descriptors [R] (40 B)
-static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false)
+static bool has_m3(const ssa_model& m)
+{
+    for (auto& q : m.rx)
+        for (auto& t : q.reac)
+            if (t.second == 3) return true;
+    return false;
+}
+
+// rx: whether the packed table is staged (models with coefficient-3 reactants)
+static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false, bool rx = true)
 {
     const size_t warps = (size_t)(block / 32);
     const size_t per_warp = half ? 2 * ((size_t)S + 16 * (size_t)P) : ((size_t)S + 32 * (size_t)P);
-    const size_t b = 32 * (size_t)R + 8 * (size_t)S + warps * 8 * per_warp +
+    const size_t b = (rx ? 32 * (size_t)R : 0) + 8 * (size_t)S + warps * 8 * per_warp +
                      4 * ((size_t)R + 1 + (size_t)n_ent + (size_t)R + 1 + (size_t)n_dep);
     return (b + 15) & ~(size_t)15;
 }
 
-static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false)
+static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false, bool rx = true)
 {
-    return k2_rxd_offset(S, R, P, n_ent, n_dep, block, half) + 40 * (size_t)R;
+    return k2_rxd_offset(S, R, P, n_ent, n_dep, block, half, rx) + 40 * (size_t)R;
 }
 
 static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump, bool half)
@@ -796,8 +805,9 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         TRY(nvrtc_compile(k2_full_source(m, PL, block, minb, dump, half), cubin, log));
         CU(cudaLibraryLoadData(&kk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
         CU(cudaLibraryGetKernel(&kk.fn, kk.lib, "ssa_k2"));
-        kk.smem = k2_smem_bytes(S, R, PL, k.n_ent, k.n_dep, block, half);
-        kk.rxd_offset = k2_rxd_offset(S, R, PL, k.n_ent, k.n_dep, block, half);
+        const bool m3 = has_m3(m);
+        kk.smem = k2_smem_bytes(S, R, PL, k.n_ent, k.n_dep, block, half, m3);
+        kk.rxd_offset = k2_rxd_offset(S, R, PL, k.n_ent, k.n_dep, block, half, m3);
         if (kk.smem > 227 * 1024)
             return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", kk.smem);
         CU(cudaFuncSetAttribute((const void*)kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kk.smem));
