@@ -1,10 +1,22 @@
+#!/bin/bash
+# Round-end GPU check (run on the B200 box through gpurun from the repo root):
+#   build, every GPU parity test, smoke(), the default bench line, the other
+#   workloads, the reference arm, and the ncu launch list of the default bench.
+# Outputs land in gpurun_out/ (scratch); copy what is kept into profiles/.
+#   usage: bash scripts/gpu_check.sh [quick]
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-lscpu | head -20 > gpurun_out/lscpu.txt
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
-timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -3 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
+timeout 1800 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
 cat gpurun_out/bench_default.json
-timeout 600 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err; echo "bench c3 rc=$?"
-cat gpurun_out/bench_c3.json
+[ "$1" = "quick" ] && exit 0
+timeout 900 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 900 python bench.py --workload sweep > gpurun_out/bench_sweep.json 2> gpurun_out/bench_sweep.err
+timeout 900 python bench.py --workload union --steps 2 --warmup 1 > gpurun_out/bench_union.json 2> gpurun_out/bench_union.err
+timeout 900 python bench.py --workload trajectories --steps 2 --warmup 1 > gpurun_out/bench_traj.json 2> gpurun_out/bench_traj.err
+timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+tail -n1 gpurun_out/bench_c3.json gpurun_out/bench_sweep.json gpurun_out/bench_union.json gpurun_out/bench_traj.json gpurun_out/bench_ref.json
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+  python bench.py --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo "ncu rc=$?"
