@@ -199,10 +199,11 @@ def test_chunk_block_and_schedule_invariance(S):
         assert np.array_equal(r.mean, base.mean) and np.array_equal(r.var, base.var), opts
         assert np.array_equal(r.m2, base.m2)
         assert np.array_equal(r.dump.states, base.dump.states)
-    for opts in (dict(chunk=512), dict(block=128)):
-        a = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=WARP)
-        b = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=WARP, **opts)
-        assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
+    for path in (WARP, HALF):
+        a = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=path)
+        for opts in (dict(chunk=512), dict(block=128), dict(block=512, blocks_per_sm=1)):
+            b = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=path, **opts)
+            assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var), (path, opts)
 
 
 @pytest.mark.parametrize("W", [2, 4, 8])
@@ -281,10 +282,11 @@ def test_numeric_error_reported(S):
         assert np.array_equal(r.dump.summary["events"], sm["events"])
 
 
-def test_overflow_reported(S):
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
+def test_overflow_reported(S, path):
     net = Network(("A",), (2**31 - 5,), (_rx([], [(0, 1)], 100.0),))
     m = S.Model(net)
-    r = S.run(m, 4, 1.0, 0.5, 1, raise_on_error=False)
+    r = S.run(m, 4, 1.0, 0.5, 1, path=path, raise_on_error=False)
     assert r.status == 4 and r.n_errors == 4
 
 
