@@ -29,6 +29,26 @@
 
 // ssa_k1_params is defined in ssa_device.cuh (shared with the host runtime).
 
+// a7: j* = LO + #{ j in [LO, R-2] : c_j <= r }, valid when c_j <= r for all
+// j < LO (c is nondecreasing and r < a0 = c_{R-1}); compare + predicated
+// increment, in four independent partial sums to shorten the dependency chain.
+template <int LO>
+static __device__ __forceinline__ int ssa_count_from(const double (&c)[SSA_R > 0 ? SSA_R : 1], double r)
+{
+    int jp[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = LO; q < SSA_R - 1; ++q) {
+        if (SSA_K1_SEL == 1 || (SSA_K1_SEL == 2 && (q & 1)))
+            // c_j, r >= +0 and not NaN: their bit patterns order as int64 (ALU pipe)
+            asm("{\n\t.reg .pred p;\n\tsetp.le.s64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                : "+r"(jp[q & 3]) : "l"(__double_as_longlong(c[q])), "l"(__double_as_longlong(r)));
+        else
+            asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                : "+r"(jp[q & 3]) : "d"(c[q]), "d"(r));
+    }
+    return LO + ((jp[0] + jp[1]) + (jp[2] + jp[3]));
+}
+
 extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(const ssa_k1_params P)
 {
     const double INF = __longlong_as_double(0x7FF0000000000000ll);
@@ -130,18 +150,22 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // j* = #{ j : c_j <= r } (c nondecreasing, r < a0), counted in four
         // independent partial sums to shorten the dependency chain.
         const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
-        int jp[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int q = 0; q < SSA_R - 1; ++q) {   // compare + predicated increment
-            if (SSA_K1_SEL == 1 || (SSA_K1_SEL == 2 && (q & 1)))
-                // c_j, r >= +0 and not NaN: their bit patterns order as int64 (ALU pipe)
-                asm("{\n\t.reg .pred p;\n\tsetp.le.s64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
-                    : "+r"(jp[q & 3]) : "l"(__double_as_longlong(c[q])), "l"(__double_as_longlong(r)));
-            else
-                asm("{\n\t.reg .pred p;\n\tsetp.le.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
-                    : "+r"(jp[q & 3]) : "d"(c[q]), "d"(r));
-        }
-        const int j = (jp[0] + jp[1]) + (jp[2] + jp[3]);
+#if SSA_K1_TAIL
+        // warp-uniform pruning (c nondecreasing): if every active lane's r is
+        // at or above c_A, then c_j <= r for all j <= A in every lane and only
+        // the entries past A need comparing.  Anchors A = R-3 (selection among
+        // the last two reactions) and A = R/2, tested in that order.
+        const unsigned act = __activemask();
+        int j;
+        if (__all_sync(act, c[SSA_R - 3] <= r))
+            j = ssa_count_from<SSA_R - 2>(c, r);
+        else if (__all_sync(act, c[SSA_R / 2] <= r))
+            j = ssa_count_from<SSA_R / 2 + 1>(c, r);
+        else
+            j = ssa_count_from<0>(c, r);
+#else
+        const int j = ssa_count_from<0>(c, r);
+#endif
         // a5: tau = E / a0 by the fast in-range IEEE division (speculative:
         // replaced on the rare path when a0 is outside [2^-900, 2^901))
         const unsigned a0hi = (unsigned)__double2hiint(a0);

@@ -363,6 +363,7 @@ static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L)
 struct K1Gen {
     bool flat_switch = true;
     bool seed_imm = true;   // keys=imm|param: Philox round keys as instruction immediates (kernel per seed)
+    bool tail = true;       // tail=on|off: warp-vote pruning of the selection compares (R >= 8)
     int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
 };
 
@@ -374,6 +375,7 @@ static K1Gen k1_gen()
         const std::string s = e ? e : "";
         if (s.find("upd=switch") != std::string::npos) r.flat_switch = false;
         if (s.find("keys=param") != std::string::npos) r.seed_imm = false;
+        if (s.find("tail=off") != std::string::npos) r.tail = false;
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
         return r;
@@ -402,7 +404,8 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         o << "#define SSA_K1_RECORD 0\n";
     }
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
-      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
+      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_TAIL "
+      << ((g.tail && R >= 8) ? 1 : 0) << "\n#define SSA_K1_DUMP "
       << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
     if (use_seed) {
         const ssa_u32 k0 = (ssa_u32)(unsigned long long)seed_bits, k1 = (ssa_u32)((unsigned long long)seed_bits >> 32);
