@@ -150,22 +150,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // j* = #{ j : c_j <= r } (c nondecreasing, r < a0), counted in four
         // independent partial sums to shorten the dependency chain.
         const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
-#if SSA_K1_TAIL
-        // warp-uniform pruning (c nondecreasing): if every active lane's r is
-        // at or above c_A, then c_j <= r for all j <= A in every lane and only
-        // the entries past A need comparing.  Anchors A = R-3 (selection among
-        // the last two reactions) and A = R/2, tested in that order.
-        const unsigned act = __activemask();
-        int j;
-        if (__all_sync(act, c[SSA_R - 3] <= r))
-            j = ssa_count_from<SSA_R - 2>(c, r);
-        else if (__all_sync(act, c[SSA_R / 2] <= r))
-            j = ssa_count_from<SSA_R / 2 + 1>(c, r);
-        else
-            j = ssa_count_from<0>(c, r);
-#else
         const int j = ssa_count_from<0>(c, r);
-#endif
         // a5: tau = E / a0 by the fast in-range IEEE division (speculative:
         // replaced on the rare path when a0 is outside [2^-900, 2^901))
         const unsigned a0hi = (unsigned)__double2hiint(a0);

@@ -358,12 +358,12 @@ static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L)
 // K1 code-generation variants (tuning; the arithmetic is identical in all of
 // them).  SSA_K1_GEN is read once per process:
 //   upd=brx|switch   a8 as one brx.idx jump table (default) or a C++ switch
-// (Measured and dropped: int64-pattern selection compares on the ALU pipe and
-// species counts in shared memory with a table update were both slower.)
+// (Measured and dropped: int64-pattern selection compares on the ALU pipe,
+// species counts in shared memory with a table update, and a warp-vote
+// pruning of the selection compares at static anchors were all slower.)
 struct K1Gen {
     bool flat_switch = true;
     bool seed_imm = true;   // keys=imm|param: Philox round keys as instruction immediates (kernel per seed)
-    bool tail = true;       // tail=on|off: warp-vote pruning of the selection compares (R >= 8)
     int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
 };
 
@@ -375,7 +375,6 @@ static K1Gen k1_gen()
         const std::string s = e ? e : "";
         if (s.find("upd=switch") != std::string::npos) r.flat_switch = false;
         if (s.find("keys=param") != std::string::npos) r.seed_imm = false;
-        if (s.find("tail=off") != std::string::npos) r.tail = false;
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
         return r;
@@ -404,8 +403,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         o << "#define SSA_K1_RECORD 0\n";
     }
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
-      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_TAIL "
-      << ((g.tail && R >= 8) ? 1 : 0) << "\n#define SSA_K1_DUMP "
+      << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
       << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
     if (use_seed) {
         const ssa_u32 k0 = (ssa_u32)(unsigned long long)seed_bits, k1 = (ssa_u32)((unsigned long long)seed_bits >> 32);
@@ -1017,7 +1015,13 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // target (its register budget is 64K / (block * blocks_per_sm))
             const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : default_minb(*m, block);
             // seed -1 is reserved for "keys from the parameters" (a seed of 2^64-1 takes that path)
-            const long long kseed = k1_gen().seed_imm ? (long long)seed : -1;
+            // (kernels per seed are cached; past 32 compiled variants of this model on
+            // this device, new seeds take the launch-parameter keys to bound the cache)
+            long long kseed = k1_gen().seed_imm ? (long long)seed : -1;
+            if (kseed != -1 && m->dev[c.device].k1.size() >= 32 &&
+                !m->dev[c.device].k1.count(k1_key(block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, kseed,
+                                                  rec ? rec->mode : 0)))
+                kseed = -1;
             TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms,
                           kseed, rec ? rec->mode : 0));
             int bps = k1->blocks_per_sm;
