@@ -64,7 +64,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     for (int q = threadIdx.x; q < P.n_pts * P.n_pool; q += blockDim.x) s_k[q] = P.pconst[q];
     __syncthreads();
     const double* kp = s_k;
-    const ssa_u64 pt0 = P.id_begin / P.n_per_point;
 #endif
     double x[SSA_S];
     double t = 0.0, s_next = 0.0;
@@ -74,16 +73,24 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 
     // a1: take the next trajectory id (atomic counter) and initialise it
     auto start = [&]() -> bool {
-        rel = atomicAdd(P.work, 1ull);
-        if (rel >= P.n_ids) return false;
-        vid = P.id_begin + rel;
 #if SSA_K1_SWEEP
         {
-            const ssa_u64 pt = vid / P.n_per_point;
-            id = vid - pt * P.n_per_point;       // trajectory id within its sweep point (RNG key)
-            kp = s_k + (pt - pt0) * (ssa_u64)P.n_pool;
+            // sweep points are interleaved in the order lanes take work (w mod
+            // points), so trajectories of short and long points mix over the
+            // whole launch; the staging column stays point-major (dense per point)
+            const ssa_u64 w = atomicAdd(P.work, 1ull);
+            if (w >= P.n_ids) return false;
+            const ssa_u64 ptl = w % (ssa_u64)P.n_pts;
+            id = w / (ssa_u64)P.n_pts;          // trajectory id within its sweep point (RNG key)
+            rel = ptl * P.n_per_point + id;
+            kp = s_k + ptl * (ssa_u64)P.n_pool;
         }
 #else
+        rel = atomicAdd(P.work, 1ull);
+        if (rel >= P.n_ids) return false;
+#endif
+        vid = P.id_begin + rel;
+#if !SSA_K1_SWEEP
         id = vid;
 #endif
 #if SSA_K1_DUMP
