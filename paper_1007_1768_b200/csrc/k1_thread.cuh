@@ -65,6 +65,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     __syncthreads();
     const double* kp = s_k;
 #endif
+    // small ensembles (spread launch): one working lane per warp and one warp
+    // per block, so each trajectory has an SM sub-partition to itself
+    if (P.spread && (threadIdx.x & 31) != 0) return;
     double x[SSA_S];
     double t = 0.0, s_next = 0.0;
     ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0, vid = 0;
@@ -279,6 +282,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #endif
         }
 #endif
+    if (P.spread) {   // one lane per warp: no warp reduction
+        atomicAdd(&P.stats->events, my_events);
+        if (my_ties) atomicAdd(&P.stats->near_ties, my_ties);
+        return;
+    }
     // warp-level reduction of the counters, then one atomic per warp
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {

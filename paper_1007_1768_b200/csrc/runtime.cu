@@ -1008,6 +1008,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     int block = (o && o->block > 0) ? o->block : (path == SSA_PATH_THREAD ? 128 : SSA_K2_BLOCK);
     if (block % 32 || block > 1024) return fail(SSA_ERR_INVALID_ARG, "block %d must be a multiple of 32 <= 1024", block);
     int grid = 0;
+    bool spread = false;
     {
         std::lock_guard<std::mutex> lk(m->mu);
         if (path == SSA_PATH_THREAD) {
@@ -1028,6 +1029,12 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
             grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + block - 1) / block);
+            // small ensembles (at most one trajectory per SM sub-partition): one
+            // working lane per block of one warp, spread over the SMs
+            if (n_ids <= (ssa_u64)sms * 4 && !(o && o->block > 0)) {
+                spread = true;
+                grid = (int)n_ids;
+            }
         } else {
             // default residency: 4 x 256 threads for one trajectory per warp (64
             // registers), 3 x 256 for two per warp (80 registers)
@@ -1146,8 +1153,9 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
                 p.pconst = pconst.as<double>() + (cb / sw->N) * (ssa_u64)sw->L.n;
                 smem = sizeof(double) * (size_t)p.n_pts * (size_t)p.n_pool;
             }
+            p.spread = spread ? 1 : 0;
             void* args[] = {&p};
-            CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(block), args, smem, st));
+            CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(spread ? 32 : block), args, smem, st));
             info.launches += 1;
         } else {
             ssa_k2_params p{};
