@@ -76,18 +76,38 @@ static __device__ __forceinline__ void wf_merge_full(double& mA, double& m2A, do
 static __device__ __forceinline__ void tree_block_full(const int4 q0, const int4 q1, double& mean, double& m2)
 {
     __shared__ double shm[SSA_TREE_BLOCK / 32], shq[SSA_TREE_BLOCK / 32];
-    // 8 adjacent leaves per thread: levels h = 1, 2, 4
-    double m[8] = {(double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w,
-                   (double)q1.x, (double)q1.y, (double)q1.z, (double)q1.w};
-    double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    wf_merge_full(m[0], v[0], m[1], v[1], 0.5);
-    wf_merge_full(m[2], v[2], m[3], v[3], 0.5);
-    wf_merge_full(m[4], v[4], m[5], v[5], 0.5);
-    wf_merge_full(m[6], v[6], m[7], v[7], 0.5);
-    wf_merge_full(m[0], v[0], m[2], v[2], 1.0);
-    wf_merge_full(m[4], v[4], m[6], v[6], 1.0);
-    wf_merge_full(m[0], v[0], m[4], v[4], 2.0);
-    double mm = m[0], vv = v[0];
+    // 8 adjacent leaves per thread: levels h = 1, 2, 4.
+    double mm, vv;
+    const unsigned lim = 1u << 20;
+    if ((unsigned)q0.x < lim && (unsigned)q0.y < lim && (unsigned)q0.z < lim && (unsigned)q0.w < lim &&
+        (unsigned)q1.x < lim && (unsigned)q1.y < lim && (unsigned)q1.z < lim && (unsigned)q1.w < lim) {
+        // Counts below 2^20: every operation of these three merge levels is
+        // exact in fp64 (means are multiples of 2^-3 below 2^20, deltas have
+        // <= 22 significant bits so their squares <= 44, the M2 sums stay below
+        // 2^49 with <= 4 fractional bits), so the tree yields the exact
+        // mean = S1/8 and M2 = (8 S2 - S1^2)/8 -- computed here in integers,
+        // bitwise equal to the fp64 merges and without their FP64 work.
+        const unsigned long long s1 = (unsigned long long)q0.x + q0.y + q0.z + q0.w + q1.x + q1.y + q1.z + q1.w;
+        const unsigned long long s2 =
+            (unsigned long long)q0.x * q0.x + (unsigned long long)q0.y * q0.y + (unsigned long long)q0.z * q0.z +
+            (unsigned long long)q0.w * q0.w + (unsigned long long)q1.x * q1.x + (unsigned long long)q1.y * q1.y +
+            (unsigned long long)q1.z * q1.z + (unsigned long long)q1.w * q1.w;
+        mm = __dmul_rn((double)s1, 0.125);
+        vv = __dmul_rn((double)(8ull * s2 - s1 * s1), 0.125);
+    } else {
+        double m[8] = {(double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w,
+                       (double)q1.x, (double)q1.y, (double)q1.z, (double)q1.w};
+        double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        wf_merge_full(m[0], v[0], m[1], v[1], 0.5);
+        wf_merge_full(m[2], v[2], m[3], v[3], 0.5);
+        wf_merge_full(m[4], v[4], m[5], v[5], 0.5);
+        wf_merge_full(m[6], v[6], m[7], v[7], 0.5);
+        wf_merge_full(m[0], v[0], m[2], v[2], 1.0);
+        wf_merge_full(m[4], v[4], m[6], v[6], 1.0);
+        wf_merge_full(m[0], v[0], m[4], v[4], 2.0);
+        mm = m[0];
+        vv = v[0];
+    }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp levels: subtrees of 8*o leaves, h/2 = 4*o
 #pragma unroll

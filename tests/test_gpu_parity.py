@@ -206,6 +206,23 @@ def test_chunk_block_and_schedule_invariance(S):
             assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var), (path, opts)
 
 
+def test_reduction_paths_bitwise_equal(S):
+    """K3's full-tile kernel takes an integer fast path for 8-leaf groups below
+    2^20 and the fp64 Chan merges otherwise; both must give the canonical
+    tree's bits.  Counts straddling 2^20 (immigration from 2^20 - 40) mix the
+    two paths in one tile; a chunk of 1024 ids (partial tiles only, general
+    kernel) must agree bitwise, and the moments must match the exact ones."""
+    net = Network(("A",), (2**20 - 40,), (_rx([], [(0, 1)], 20.0),))
+    m = S.Model(net)
+    n = 4096
+    full = S.run(m, n, 4.0, 0.5, 13, path=THREAD, dump_ids=np.arange(n))
+    part = S.run(m, n, 4.0, 0.5, 13, path=THREAD, chunk=1024)
+    assert np.array_equal(full.mean, part.mean) and np.array_equal(full.m2, part.m2)
+    assert np.any(full.dump.states >= 2**20) and np.any(full.dump.states < 2**20)
+    ref_mean, ref_var = exact_moments(full.dump.states)
+    assert_moments_close(full.mean, full.var, ref_mean, ref_var)
+
+
 @pytest.mark.parametrize("W", [2, 4, 8])
 def test_shard_merge_equals_single_run(S, W):
     """The multi-GPU form (ssa_run_shard per rank + ssa_merge_roots), run here
