@@ -6,8 +6,6 @@
 // K1 (thread path, k1_thread.cuh) and K2 (warp path, k2_warp.cuh) are
 // model-specialised and compiled by NVRTC at run time (runtime.cu).
 #include <cuda_runtime.h>
-
-#include <algorithm>
 #include <stdint.h>
 
 #include "ssa_device.cuh"
@@ -142,45 +140,31 @@ __global__ void __launch_bounds__(SSA_TREE_BLOCK, 4) ssa_tree_leaf_full(const in
                                                                        ssa_u64 stride, ssa_u64 n_full,
                                                                        ssa_u64 rows, ssa_tree_out out)
 {
-    // persistent: work item = (row, pair of adjacent full tiles); the loads of
-    // the next item are issued before the current one is reduced, so each
-    // thread keeps 128 B in flight across the block-level reduction
-    const ssa_u64 pairs = (n_full + 1) / 2, items = rows * pairs;
-    ssa_u64 it = blockIdx.x;
-    if (it >= items) return;
-    auto load = [&](ssa_u64 w, int4& x0, int4& x1, int4& y0, int4& y1) {
-        const ssa_u64 row = w / pairs, t0 = 2 * (w - row * pairs);
-        const int* src = staging + row * stride + (ssa_u64)threadIdx.x * 8;
-        x0 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN));
-        x1 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN + 4));
-        if (t0 + 1 < n_full) {
-            y0 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN));
-            y1 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN + 4));
-        }
-    };
-    int4 a0, a1, b0 = make_int4(0, 0, 0, 0), b1 = b0;
-    load(it, a0, a1, b0, b1);
-    for (; it < items; it += gridDim.x) {
-        const ssa_u64 nx = it + gridDim.x;
-        int4 na0 = a0, na1 = a1, nb0 = b0, nb1 = b1;
-        if (nx < items) load(nx, na0, na1, nb0, nb1);
-        const ssa_u64 row = it / pairs, t0 = 2 * (it - row * pairs);
-        double mean = 0.0, m2 = 0.0;
-        tree_block_full(a0, a1, mean, m2);
+    const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    if (row >= rows) return;
+    const ssa_u64 t0 = 2ull * blockIdx.x;                 // first tile of this block
+    const int* src = staging + row * stride + (ssa_u64)threadIdx.x * 8;
+    const bool two = t0 + 1 < n_full;
+    const int4 a0 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN));
+    const int4 a1 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN + 4));
+    int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
+    if (two) {
+        b0 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN));
+        b1 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN + 4));
+    }
+    double mean = 0.0, m2 = 0.0;
+    tree_block_full(a0, a1, mean, m2);
+    if (threadIdx.x == 0) {
+        const ssa_u64 o = row * out.row_stride + t0 * out.elem_stride + out.offset;
+        out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
+    }
+    if (two) {
+        __syncthreads();                                   // shared scratch of tree_block_full reused
+        tree_block_full(b0, b1, mean, m2);
         if (threadIdx.x == 0) {
-            const ssa_u64 o = row * out.row_stride + t0 * out.elem_stride + out.offset;
+            const ssa_u64 o = row * out.row_stride + (t0 + 1) * out.elem_stride + out.offset;
             out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
         }
-        __syncthreads();                                   // shared scratch of tree_block_full reused
-        if (t0 + 1 < n_full) {
-            tree_block_full(b0, b1, mean, m2);
-            if (threadIdx.x == 0) {
-                const ssa_u64 o = row * out.row_stride + (t0 + 1) * out.elem_stride + out.offset;
-                out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
-            }
-            __syncthreads();
-        }
-        a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
     }
 }
 
@@ -269,16 +253,8 @@ cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 cou
     const bool aligned = stride % 4 == 0 && ((uintptr_t)staging % 16) == 0;
     const ssa_u64 n_full = aligned ? count / SSA_TREE_SPAN : 0;
     if (n_full) {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            if (sms <= 0) sms = 148;
-        }
-        const ssa_u64 items = rows * ((n_full + 1) / 2);
-        const unsigned grid = (unsigned)std::min<ssa_u64>(items, (ssa_u64)sms * 8);
-        ssa_tree_leaf_full<<<grid, SSA_TREE_BLOCK, 0, st>>>(staging, stride, n_full, rows, out);
+        ssa_tree_leaf_full<<<tree_grid((n_full + 1) / 2, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, n_full,
+                                                                                          rows, out);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         ++*launches;
