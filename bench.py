@@ -33,6 +33,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def measured_traffic(workload: str, kernel: str, default_size: bool):
+    """DRAM read+write bytes per launch of `kernel` from the committed ncu pass (profiles/traffic.json),
+    for the default-size workload only (other sizes: None)."""
+    if not default_size or not os.path.exists(TRAFFIC_FILE):
+        return None
+    e = json.load(open(TRAFFIC_FILE)).get(workload, {}).get(kernel)
+    return None if e is None else int(e["read"] + e["write"])
 
 
 # ---------------------------------------------------------------- helpers
@@ -499,8 +509,12 @@ def main():
         I = alg_warp_instr_per_event(net, 16 if path == 3 else 32)        # warp-instructions per event
         achieved = per_rank_events * I / (k1_ms / 1e3) / 1e9
     peak = n_sm * 4 * sm_max * 1e6 / 1e9                                  # G warp-instr/s
+    workload = f"config{args.config}-{cfg.name}" + ("-variantB" if args.variant == "B" else "")
+    default_size = not args.n_per_gpu and not args.t_end
+    kname = "ssa_k1" if path == 1 else "ssa_k2"
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "ssa_k1" if path == 1 else ("ssa_k2" if path == 2 else "ssa_k2 (half-warp)"),
+                "traffic": measured_traffic(workload, kname, default_size),
+                "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)", "kernel": "ssa_k1" if path == 1 else ("ssa_k2" if path == 2 else "ssa_k2 (half-warp)"),
                 ("alg_thread_instr_per_event" if path == 1 else "alg_warp_instr_per_event"): I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
 
@@ -509,7 +523,8 @@ def main():
     r_ms = statistics.mean(red_ms) if red_ms else float("nan")
     r_gbs = red_bytes / (r_ms / 1e3) / 1e9 if red_ms and r_ms > 0 else None
     roofline_reduce = {"bound": "hbm", "achieved": r_gbs, "peak": hbm_peak, "unit": "GB/s",
-                       "frac": (r_gbs / hbm_peak) if r_gbs else None, "traffic": None, "kernel": "ssa_tree_leaf",
+                       "frac": (r_gbs / hbm_peak) if r_gbs else None,
+                       "traffic": measured_traffic(workload, "ssa_tree_leaf", default_size), "kernel": "ssa_tree_leaf",
                        "bytes_per_launch": red_bytes, "kernel_ms": r_ms,
                        "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200 nominal"}
 

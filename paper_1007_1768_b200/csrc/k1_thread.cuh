@@ -4,7 +4,8 @@
 // generated model section (runtime.cu: gen_k1_model) that defines
 //   SSA_S, SSA_R, SSA_K1_BLOCK, SSA_K1_MINB
 //   __constant__ double c_k[] (distinct rate / modifier constants), c_x0[]
-//   ssa_prefix(x, c)      a3 + a4: c_j = c_{j-1} + a_j, sequential order (R13)
+//   ssa_khat(x, kh)       the modified rates k^ = max(0, k + d x_m), cached per trajectory
+//   ssa_prefix(x, kh, c)  a3 + a4: c_j = c_{j-1} + a_j, sequential order (R13)
 //   ssa_apply(j, x)       a8: x += nu_j (one indirect branch through a table)
 //   ssa_first_bad(x)      first reaction with a non-finite propensity
 // so that species counts (fp64, exact integers) and the propensity prefix
@@ -69,6 +70,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     // per block, so each trajectory has an SM sub-partition to itself
     if (P.spread && (threadIdx.x & 31) != 0) return;
     double x[SSA_S];
+    double kh[SSA_NKH > 0 ? SSA_NKH : 1];   // cached modified rates k^ (ssa_khat)
     double t = 0.0, s_next = 0.0;
     ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0, vid = 0;
     long long k = 0, slot = -1;
@@ -101,6 +103,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #endif
 #pragma unroll
         for (int s = 0; s < SSA_S; ++s) x[s] = c_x0[s];
+        ssa_khat(x, kh SSA_KP_ARG);
         t = 0.0; s_next = 0.0; e = 0; k = 0; hash = SSA_FNV_OFFSET; ties = 0;
         status = 0; absorbed = 0; err_r = -1;
         return true;
@@ -150,7 +153,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // independent dependency chains in one basic block, so the scheduler
         // interleaves them.
         double c[SSA_R > 0 ? SSA_R : 1];
-        const double a0 = ssa_prefix(x, c SSA_KP_ARG);
+        const double a0 = ssa_prefix(x, kh, c SSA_KP_ARG);
         // keep the prefix in registers: without this barrier the compiler
         // recomputes the whole propensity chain for the selection (a7)
 #pragma unroll
@@ -258,6 +261,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         }
 #endif
         ssa_apply(j, x);
+        if (ssa_khat_dirty(j)) ssa_khat(x, kh SSA_KP_ARG);   // a modifier species changed
         t = tn;
         ++e;
 #if SSA_K1_DUMP

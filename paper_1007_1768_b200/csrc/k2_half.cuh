@@ -138,8 +138,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         double v = L;
 #pragma unroll
         for (int o = 1; o < SSA_HL; o <<= 1) {
-            const double y = __shfl_up_sync(FULL, v, o, SSA_HL);
-            if (hl >= o) v = __dadd_rn(y, v);
+            v = ssa_scan_step(v, o, 0x1000);     // width 16
         }
         const double a0 = __shfl_sync(FULL, v, SSA_HL - 1, SSA_HL);
         // a5
@@ -157,7 +156,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #pragma unroll
         for (int q = 0; q < SSA_P; ++q) {
             p = __dadd_rn(p, a[q * SSA_HL + hl]);
-            over += (p > r) ? 1 : 0;
+            asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                : "+r"(over) : "d"(p), "d"(r));
         }
         const int jl = over ? SSA_P - over : -1;
         const unsigned bal = (__ballot_sync(FULL, v > r) >> (16 * h)) & 0xFFFFu;
@@ -238,9 +238,13 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                 apply = false;
             }
         }
-        if (apply) {
-            int j;
-            if (jq >= 0) {
+        // Both halves run the update and the recompute loops (a half that does not
+        // apply an event has empty ranges), so the two syncs are full-warp ones: a
+        // half mask compiles to a convergence check (MATCH/REDUX/VOTE) per sync.
+        {
+            int j = 0;
+            if (!apply) {
+            } else if (jq >= 0) {
                 j = ls * SSA_P + jq;
             } else {
                 // rounding fallback (rare): the largest j <= lane*'s last index with a_j > 0
@@ -252,15 +256,15 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                 j = __shfl_sync(HALF, lp, 31 - __clz(m2), SSA_HL);
             }
             // a8: state update (lane t of the half takes the t-th net change)
-            const int nb = nu_off[j], ne = nu_off[j + 1];
+            const int nb = apply ? nu_off[j] : 0, ne = apply ? nu_off[j + 1] : 0;
             for (int q = nb + hl; q < ne; q += SSA_HL) {
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
                 x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));
             }
-            __syncwarp(HALF);
+            __syncwarp();
             // a3: the half recomputes dep(j)
-            const int db = dep_off[j], de = dep_off[j + 1];
+            const int db = apply ? dep_off[j] : 0, de = apply ? dep_off[j + 1] : 0;
             for (int q = db + hl; q < de; q += SSA_HL) {
                 const int jj = dep_ent[q];
 #if !SSA_HAS_M3
@@ -271,14 +275,15 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                 a[qq * SSA_HL + l] = k2_propensity(rx[jj], x);
 #endif
             }
-            __syncwarp(HALF);
-            t = tn;
-            ++e;
+            __syncwarp();
+            if (apply) {
+                t = tn;
+                ++e;
 #if SSA_K2_DUMP
-            hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
+                hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
 #endif
+            }
         }
-        __syncwarp();
     }
     // per-warp counter totals (lanes 0 and 16 hold their halves' sums)
     my_events += __shfl_down_sync(FULL, my_events, 16);

@@ -81,10 +81,20 @@ struct k2_rxd {
     ssa_u64 gw;      // gate word (as k2_rx)
 };
 
+// select without a branch (selp on the 64-bit value; ptxas would otherwise
+// turn the ternaries of the factor into divergent branches)
+static __device__ __forceinline__ double k2_sel(bool p, double a, double b)
+{
+    double r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+        : "=d"(r) : "d"(a), "d"(b), "r"((int)p));
+    return r;
+}
+
 static __device__ __forceinline__ double k2_factor_bf(double x, int m)
 {
     const double x2 = __dmul_rn(__dmul_rn(x, __dadd_rn(x, -1.0)), 0.5);   // C(x,2)
-    return (m == 2) ? x2 : ((m == 1) ? x : 1.0);
+    return k2_sel(m == 2, x2, k2_sel(m == 1, x, 1.0));
 }
 
 // Branch-free form (the 32 lanes evaluate different reactions, so branches
@@ -238,10 +248,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             double v = L;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const double y = __shfl_up_sync(FULL, v, o);
-                // v = y + v on lanes >= o: one predicated add (no selects)
-                asm("{\n\t.reg .pred p;\n\tsetp.ge.s32 p, %2, %3;\n\t@p add.rn.f64 %0, %1, %0;\n\t}"
-                    : "+d"(v) : "d"(y), "r"(lane), "r"(o));
+                v = ssa_scan_step(v, o, 0);          // width 32
             }
             const double a0 = __shfl_sync(FULL, v, 31);
             // a5

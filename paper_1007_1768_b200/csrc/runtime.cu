@@ -327,11 +327,14 @@ static ssa_status pinned_constants(const ssa_model& m, double** out, size_t* byt
 
 // a3 for reaction j: k^ (rate, or the clamped linear modifier of P:93), then
 // a = k^ * h.
-static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L)
+// kh >= 0: the reaction's modified rate k^ is the cached register kh[kh] (K1)
+static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L, int kh = -1)
 {
     std::ostringstream o;
     const std::string rate = "SSA_K(" + std::to_string(L.rate_slot[j]) + ")";
-    if (q.mod_sp >= 0) {
+    if (kh >= 0) {
+        o << "k = kh[" << kh << "]; ";
+    } else if (q.mod_sp >= 0) {
         const std::string modc = "SSA_K(" + std::to_string(L.mod_slot[j]) + ")";
         o << "k = __dadd_rn(" << rate << ", __dmul_rn(" << modc << ", x[" << q.mod_sp << "])); ";
         if (L.clamp[j]) o << "k = (k < 0.0) ? 0.0 : k; ";
@@ -429,10 +432,68 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
     }
     o << "__constant__ double c_x0[" << S << "];\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
-    o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], double (&c)[SSA_R > 0 ? SSA_R : 1] SSA_KP_PARAM) {\n";
-    o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)c;\n";
+    // a3's modified rates k^ = max(0, k + d x_m) (R4) depend on x_m alone: each
+    // distinct (k, d, m) is kept in a register (kh) and recomputed only after
+    // an event that changes a modifier species (and at the start of a
+    // trajectory).  Same expression, same bits as evaluating it every event.
+    std::vector<int> kh_of(R, -1);
+    std::vector<int> kh_first;   // a reaction that defines each cached term
     for (int j = 0; j < R; ++j) {
-        o << "  { " << prop_stmts(m.rx[j], j, L) << " "
+        if (m.rx[j].mod_sp < 0) continue;
+        for (size_t i = 0; i < kh_first.size() && kh_of[j] < 0; ++i) {
+            const int f = kh_first[i];
+            if (L.rate_slot[f] == L.rate_slot[j] && L.mod_slot[f] == L.mod_slot[j] &&
+                m.rx[f].mod_sp == m.rx[j].mod_sp && L.clamp[f] == L.clamp[j])
+                kh_of[j] = (int)i;
+        }
+        if (kh_of[j] < 0) {
+            kh_of[j] = (int)kh_first.size();
+            kh_first.push_back(j);
+        }
+    }
+    if (kh_first.size() > 8) {   // register budget: evaluate inline instead
+        kh_first.clear();
+        std::fill(kh_of.begin(), kh_of.end(), -1);
+    }
+    const int NKH = (int)kh_first.size();
+    o << "#define SSA_NKH " << NKH << "\n";
+    o << "static __device__ __forceinline__ void ssa_khat(const double (&x)[SSA_S], double (&kh)[SSA_NKH > 0 ? SSA_NKH : 1] SSA_KP_PARAM) {\n";
+    o << "  double k; (void)k; (void)x; (void)kh;\n";
+    for (int i = 0; i < NKH; ++i) {
+        const int j = kh_first[i];
+        o << "  { k = __dadd_rn(SSA_K(" << L.rate_slot[j] << "), __dmul_rn(SSA_K(" << L.mod_slot[j] << "), x["
+          << m.rx[j].mod_sp << "])); ";
+        if (L.clamp[j]) o << "k = (k < 0.0) ? 0.0 : k; ";
+        o << "kh[" << i << "] = k; }\n";
+    }
+    o << "}\n";
+    {
+        // reactions whose net change touches a modifier species of a cached term
+        std::vector<int> dirty;
+        for (int j = 0; j < R; ++j) {
+            bool d = false;
+            for (auto& nu : m.rx[j].nu)
+                for (int f : kh_first) d = d || (nu.second != 0 && nu.first == m.rx[f].mod_sp);
+            if (d) dirty.push_back(j);
+        }
+        o << "static __device__ __forceinline__ bool ssa_khat_dirty(int j) { (void)j; return ";
+        if (dirty.empty()) {
+            o << "false";
+        } else if (dirty.size() <= 4) {
+            for (size_t i = 0; i < dirty.size(); ++i) o << (i ? " || " : "") << "j == " << dirty[i];
+        } else if (R <= 64) {
+            unsigned long long mask = 0;
+            for (int j : dirty) mask |= 1ull << j;
+            o << "((0x" << std::hex << mask << std::dec << "ull >> j) & 1ull) != 0";
+        } else {
+            o << "true";
+        }
+        o << "; }\n";
+    }
+    o << "static __device__ __forceinline__ double ssa_prefix(const double (&x)[SSA_S], const double (&kh)[SSA_NKH > 0 ? SSA_NKH : 1], double (&c)[SSA_R > 0 ? SSA_R : 1] SSA_KP_PARAM) {\n";
+    o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)c; (void)kh;\n";
+    for (int j = 0; j < R; ++j) {
+        o << "  { " << prop_stmts(m.rx[j], j, L, kh_of[j]) << " "
           << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
     }
     o << "  return acc;\n}\n";

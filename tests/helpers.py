@@ -16,6 +16,19 @@ def _oracle_chunk(args):
     return r.grid_x, r.grid_e, r.grid_t, r.summaries, r.status
 
 
+_CTX = None
+
+
+def _pool_context():
+    """Worker processes come from a fork server started before any CUDA or torch threads exist in
+    it (forking the multi-threaded test process itself is unsafe once CUDA is initialised)."""
+    global _CTX
+    if _CTX is None:
+        _CTX = mp.get_context("forkserver")
+        _CTX.set_forkserver_preload(["numpy", "oracle.oracle", "tests.helpers"])
+    return _CTX
+
+
 def oracle_replay(net, ids, seed, t_end, dt, mode, procs=None):
     """Run the oracle on `ids` in parallel worker processes; returns
     (grid_x [n,G,S], grid_e [n,G], grid_t [n,G], summaries [n])."""
@@ -25,7 +38,7 @@ def oracle_replay(net, ids, seed, t_end, dt, mode, procs=None):
     if procs == 1 or len(parts) == 1:
         outs = [_oracle_chunk((net, p, seed, t_end, dt, mode)) for p in parts]
     else:
-        with mp.get_context("fork").Pool(procs) as pool:
+        with _pool_context().Pool(procs) as pool:
             outs = pool.map(_oracle_chunk, [(net, p, seed, t_end, dt, mode) for p in parts])
     gx = np.concatenate([o[0] for o in outs])
     ge = np.concatenate([o[1] for o in outs])
