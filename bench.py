@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+FP64_PER_SMSP_CLK = 0.497   # DADD/DMUL/DFMA issue rate per SMSP per clock, profiles/r1h_pipe_peaks.txt
 
 
 def measured_traffic(workload: str, kernel: str, default_size: bool):
@@ -57,14 +58,37 @@ def alg_instr_per_event(net, path: int) -> float:
     for r in net.reactions:
         fac = sum(0 if m == 1 else (3 if m == 2 else 14) for _, m in r.reactants)
         props += fac + max(len(r.reactants) - 1, 0) + (1 if r.reactants else 0)
-        if r.modifier_species >= 0:
-            props += 3
+        # a modified rate k^ = max(0, k + d x_m) is a function of x_m alone: it is
+        # evaluated when x_m changes (rare; HIV: F only grows by V4 -> F + V4), not per event
     R = net.R
     prefix = max(R - 1, 0)
     select = 2 * max(R - 1, 0)   # compare + predicated add per prefix entry
     update = 4
     rest = 1 + 2 + 5 + 3          # r = u2 a0, grid check, hash, counter/loop
     return philox + u53 + plog + tau + props + prefix + select + update + rest
+
+
+def alg_fp64_per_event(net) -> float:
+    """Algorithmic FP64-pipe instructions per applied event of the thread path:
+    u53 (1 exact add each) 2, plog (in-range divide 8, Horner 10, recombination and fold 6) 24,
+    tau (divide 8 + add) 9, per reaction the factor ops (C(x,2): add + 2 multiplies; C(x,3): 7),
+    the products and k*h, prefix R-1 adds, selection R-1 compares, r = u2 a0, the grid compare,
+    and the update's count adds (mean |nu_j| over reactions)."""
+    props = 0
+    for r in net.reactions:
+        props += sum(0 if m == 1 else (3 if m == 2 else 7) for _, m in r.reactants)
+        props += max(len(r.reactants) - 1, 0) + (1 if r.reactants else 0)
+    R = net.R
+    upd = 0
+    for r in net.reactions:
+        nu = {}
+        for sp, m in r.reactants:
+            nu[sp] = nu.get(sp, 0) - m
+        for sp, m in r.products:
+            nu[sp] = nu.get(sp, 0) + m
+        upd += sum(1 for v in nu.values() if v != 0)
+    upd /= max(R, 1)
+    return 2 + 24 + 9 + props + 2 * max(R - 1, 0) + 1 + 1 + upd
 
 
 def alg_warp_instr_per_event(net, lanes: int = 32) -> float:
@@ -517,6 +541,16 @@ def main():
                 "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)", "kernel": "ssa_k1" if path == 1 else ("ssa_k2" if path == 2 else "ssa_k2 (half-warp)"),
                 ("alg_thread_instr_per_event" if path == 1 else "alg_warp_instr_per_event"): I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
+    if path == 1:
+        # the co-bound: the FP64 pipe issues 0.497 warp-instructions per clock per SMSP
+        # (measured, profiles/r1h_pipe_peaks.txt), and about half of K1's work is FP64
+        F = alg_fp64_per_event(net)
+        f_ach = per_rank_events * F / 32.0 / (k1_ms / 1e3) / 1e9
+        f_peak = n_sm * 4 * FP64_PER_SMSP_CLK * sm_max * 1e6 / 1e9
+        roofline["fp64_pipe"] = {"achieved": f_ach, "peak": f_peak, "unit": "Gwarp-inst/s", "frac": f_ach / f_peak,
+                                 "alg_fp64_thread_instr_per_event": F,
+                                 "peak_basis": f"{n_sm} SMs x 4 SMSPs x {FP64_PER_SMSP_CLK} FP64 warp-inst/clk "
+                                               f"(scripts/pipe_peaks.cu) x {sm_max:.0f} MHz"}
 
     # secondary: the chunk reduction (K3) reads the staged grid samples once -- HBM bound
     hbm_peak = float(peaks.get("hbm_gbs", 7700.0))
