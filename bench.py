@@ -371,6 +371,62 @@ def run_traj_bench(args, rank, world):
     return 0
 
 
+def run_dump_bench(args, rank, world):
+    """Raw-trajectory dump (a11; north_star: "achieved HBM GB/s for the raw-trajectory dump"):
+    config 2 (HIV, 2^18 trajectories, 100 d) with 65,536 dumped ids (R24) into page-locked host
+    arrays.  The K1 dump variant writes each dumped trajectory's grid states, event counts and
+    last-event times to HBM as it crosses grid points; the library copies them to the host after
+    the run (timed separately with CUDA events: `dump_ms`)."""
+    if world != 1:
+        print(json.dumps({"error": "the dump workload runs on one GPU"}))
+        return 1
+    import torch
+
+    import inputs
+    from paper_1007_1768_b200 import build as B
+    B.build()
+    from paper_1007_1768_b200 import ssa as S
+    torch.cuda.set_device(0)
+    cfg = inputs.config(2)
+    n = args.n_per_gpu or cfg.n_trajectories
+    t_end = args.t_end or cfg.t_end
+    n_dump = min(65536, n)
+    ids = inputs.dump_ids(n, n_dump, cfg.seed)
+    m = S.Model(cfg.network)
+    base = [S.run(m, n, t_end, cfg.dt, cfg.seed) for _ in range(2)][-1]    # K1 without the dump
+    for _ in range(args.warmup):
+        S.run(m, n, t_end, cfg.dt, cfg.seed, dump_ids=ids, dump_pinned=True)
+    dev_ms, ssa_ms, dump_ms, events, dbytes, launches = [], [], [], 0, 0, 0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            r = S.run(m, n, t_end, cfg.dt, cfg.seed, dump_ids=ids, dump_pinned=True)
+            dev_ms.append(r.device_ms + r.dump_ms)
+            ssa_ms.append(r.ssa_ms)
+            dump_ms.append(r.dump_ms)
+            events += r.events
+            dbytes = r.dump_bytes
+            launches += r.kernel_launches
+    ms = sum(dev_ms)
+    k1 = statistics.mean(ssa_ms)
+    dm = statistics.mean(dump_ms)
+    line = {"metric": "ssa_events_per_s", "value": events / (ms / 1e3), "unit": "events/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config2-hiv-100d-dump65536", "model": cfg.network.name, "n_trajectories": n,
+                       "n_dump": n_dump, "t_end": t_end, "sample_dt": cfg.dt, "seed": cfg.seed,
+                       "timing": "device time of each call incl. the D2H of the dump (CUDA events in the library)"},
+            "dump": {"bytes_per_step": dbytes, "d2h_ms": dm, "d2h_GBps": dbytes / (dm / 1e3) / 1e9 if dm > 0 else None,
+                     "host_memory": "page-locked",
+                     "written_in_loop_GBps": dbytes / (k1 / 1e3) / 1e9,
+                     "note": "the dump is written by K1 while it simulates (grid crossings of the dumped "
+                             "ids), so its HBM write rate is set by the event loop, not by bandwidth",
+                     "k1_ms_with_dump": k1, "k1_ms_without_dump": base.ssa_ms,
+                     "k1_overhead": k1 / base.ssa_ms - 1.0},
+            "gpu_launches": launches, "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ---------------------------------------------------------------- our arm
 def main():
     ap = argparse.ArgumentParser()
@@ -388,7 +444,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--variant", default="A", choices=["A", "B"],
                     help="HIV configs: B = the gated time-triggered mutation (SPEC.md:424, NEXT 3)")
-    ap.add_argument("--workload", default="config", choices=["config", "sweep", "union", "trajectories"],
+    ap.add_argument("--workload", default="config", choices=["config", "sweep", "union", "trajectories", "dump"],
                     help="sweep: the Fig. 4 delta_t sensitivity sweep (ssa_run_sweep, 1 GPU); union: selective "
                          "memory at union times over 16 HIV trajectories (ssa_run_union, Fig. 4's ensemble)")
     ap.add_argument("--kx", type=int, default=16, help="union workload: X-reduction factor k_x")
@@ -405,6 +461,8 @@ def main():
         return run_union_bench(args, rank, world)
     if args.workload == "trajectories":
         return run_traj_bench(args, rank, world)
+    if args.workload == "dump":
+        return run_dump_bench(args, rank, world)
 
     import numpy as np
     import torch

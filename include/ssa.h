@@ -187,6 +187,9 @@ typedef struct {
     int32_t pad2;
     double reduce_ms;          /* device time of the chunk reductions (K3 + tile merges, CUDA events) */
     uint64_t reduce_bytes;     /* staged sample bytes those reductions read (4 per trajectory x grid cell) */
+    double dump_ms;            /* device time of the dump's device->host copies (CUDA events; 0 when the dump
+                                  arrays are device memory or there is no dump) */
+    uint64_t dump_bytes;       /* bytes of raw-trajectory dump produced (states, events_at, time_at, summaries) */
 } ssa_result;
 
 /* StochRxn_ff on one GPU: simulate trajectories 0..n_trajectories-1 on

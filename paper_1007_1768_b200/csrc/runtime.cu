@@ -967,8 +967,8 @@ struct RangeOut {
 struct RunInfo {
     ssa_dev_stats stats;
     int path = 0;
-    double device_ms = 0, ssa_ms = 0, jit_ms = 0, reduce_ms = 0;
-    uint64_t h2d = 0, d2h = 0, reduce_bytes = 0;
+    double device_ms = 0, ssa_ms = 0, jit_ms = 0, reduce_ms = 0, dump_ms = 0;
+    uint64_t h2d = 0, d2h = 0, reduce_bytes = 0, dump_bytes = 0;
     int launches = 0;
 };
 
@@ -1279,16 +1279,30 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     CU(cudaEventRecord(ev1, st));
     CU(cudaMemcpyAsync(&info.stats, statsb.p, sizeof(ssa_dev_stats), cudaMemcpyDeviceToHost, st));
     info.d2h += sizeof(ssa_dev_stats);
+    cudaEvent_t evd0 = nullptr, evd1 = nullptr;
+    if (n_dump) {
+        info.dump_bytes = (dump->states ? sizeof(int) * n_dump * cells : 0) + (dump->events_at ? 8 * n_dump * G : 0) +
+                          (dump->time_at ? 8 * n_dump * G : 0) + (dump->summary ? sizeof(ssa_dev_summary) * n_dump : 0);
+    }
     if (n_dump && !dump_on_device) {
-        info.d2h += (dump->states ? sizeof(int) * n_dump * cells : 0) + (dump->events_at ? 8 * n_dump * G : 0) +
-                    (dump->time_at ? 8 * n_dump * G : 0) + (dump->summary ? sizeof(ssa_dev_summary) * n_dump : 0);
+        info.d2h += info.dump_bytes;
+        CU(cudaEventCreate(&evd0));
+        CU(cudaEventCreate(&evd1));
+        CU(cudaEventRecord(evd0, st));
         if (dump->states) CU(cudaMemcpyAsync(dump->states, p_states, sizeof(int) * n_dump * cells, cudaMemcpyDeviceToHost, st));
         if (dump->events_at) CU(cudaMemcpyAsync(dump->events_at, p_e, sizeof(ssa_u64) * n_dump * G, cudaMemcpyDeviceToHost, st));
         if (dump->time_at) CU(cudaMemcpyAsync(dump->time_at, p_t, sizeof(double) * n_dump * G, cudaMemcpyDeviceToHost, st));
         if (dump->summary) CU(cudaMemcpyAsync(dump->summary, p_sum, sizeof(ssa_dev_summary) * n_dump, cudaMemcpyDeviceToHost, st));
+        CU(cudaEventRecord(evd1, st));
     }
     CU(cudaStreamSynchronize(st));
     float ms = 0.f;
+    if (evd0) {
+        CU(cudaEventElapsedTime(&ms, evd0, evd1));
+        info.dump_ms = ms;
+        cudaEventDestroy(evd0);
+        cudaEventDestroy(evd1);
+    }
     CU(cudaEventElapsedTime(&ms, ev0, ev1));
     info.device_ms = ms;
     info.ssa_ms = ssa_ms_total;
@@ -1308,6 +1322,8 @@ static ssa_status fill_result(const RunInfo& info, ssa_result* r)
     r->ssa_ms = info.ssa_ms;
     r->reduce_ms = info.reduce_ms;
     r->reduce_bytes = info.reduce_bytes;
+    r->dump_ms = info.dump_ms;
+    r->dump_bytes = info.dump_bytes;
     r->jit_ms = info.jit_ms;
     r->h2d_bytes = info.h2d;
     r->d2h_bytes = info.d2h;
@@ -1570,6 +1586,8 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     r->ssa_ms = info.ssa_ms;
     r->reduce_ms = ums;
     r->reduce_bytes = E * (8 + 4 + 4 * (ssa_u64)U);
+    r->dump_ms = 0.0;
+    r->dump_bytes = 0;
     r->jit_ms = info.jit_ms;
     r->kernel_launches = info.launches + launches;
     r->h2d_bytes = info.h2d + 8 * (nsp.size() + 2 * S);
@@ -1680,6 +1698,8 @@ extern "C" ssa_status ssa_run_trajectories(const ssa_model* m, uint64_t n_trajec
     r->ssa_ms = info.ssa_ms;
     r->reduce_ms = gms;                        // sort + gather of the points
     r->reduce_bytes = rows * (16 + 4 * S);     // recorded point bytes
+    r->dump_ms = 0.0;
+    r->dump_bytes = 0;
     r->jit_ms = info.jit_ms;
     r->kernel_launches = info.launches + launches;
     if (!fits)
@@ -1700,8 +1720,8 @@ extern "C" ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, ui
     r->events = r->near_ties = r->n_errors = r->first_error_id = 0;
     r->first_error_reaction = -1;
     r->path_used = 0;
-    r->device_ms = r->ssa_ms = r->jit_ms = r->reduce_ms = 0.0;
-    r->reduce_bytes = 0;
+    r->device_ms = r->ssa_ms = r->jit_ms = r->reduce_ms = r->dump_ms = 0.0;
+    r->reduce_bytes = r->dump_bytes = 0;
     r->h2d_bytes = r->d2h_bytes = 0;
     r->kernel_launches = 0;
     // element (cell, rank) at d_roots[rank * 3 * cells + {0,1,2} * cells + cell]

@@ -77,7 +77,8 @@ class ssa_result(C.Structure):
                 ("first_error_id", C.c_uint64), ("first_error_reaction", C.c_int32), ("path_used", C.c_int32),
                 ("device_ms", C.c_double), ("ssa_ms", C.c_double), ("jit_ms", C.c_double),
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("kernel_launches", C.c_int32),
-                ("pad2", C.c_int32), ("reduce_ms", C.c_double), ("reduce_bytes", C.c_uint64)]
+                ("pad2", C.c_int32), ("reduce_ms", C.c_double), ("reduce_bytes", C.c_uint64),
+                ("dump_ms", C.c_double), ("dump_bytes", C.c_uint64)]
 
 
 _lib = None
@@ -257,6 +258,8 @@ class RunResult:
     dump: Optional[Dump] = None
     reduce_ms: float = 0.0           # device time of the chunk reductions (K3)
     reduce_bytes: int = 0            # staged bytes they read
+    dump_ms: float = 0.0             # device time of the dump's D2H copies (host dump arrays)
+    dump_bytes: int = 0              # raw-trajectory dump bytes produced
 
 
 def _options(path=SSA_PATH_AUTO, device=-1, stream=None, chunk=0, staging_budget_bytes=0, block=0,
@@ -271,11 +274,23 @@ def _options(path=SSA_PATH_AUTO, device=-1, stream=None, chunk=0, staging_budget
     return o
 
 
-def _make_dump(ids, G, S):
+def _host_array(shape, dtype, pinned: bool) -> np.ndarray:
+    """Zeroed host array; pinned=True places it in page-locked memory (torch's pinned allocator) so
+    the library's device->host copies run at full link speed."""
+    dtype = np.dtype(dtype)
+    if not pinned:
+        return np.zeros(shape, dtype)
+    import torch
+    nbytes = int(np.prod(shape)) * dtype.itemsize
+    buf = torch.zeros(max(nbytes, 1), dtype=torch.uint8, pin_memory=True)
+    return buf.numpy()[:nbytes].view(dtype).reshape(shape)   # the view keeps the tensor alive
+
+
+def _make_dump(ids, G, S, pinned: bool = False):
     ids = np.ascontiguousarray(np.asarray(ids, dtype=np.uint64))
     n = len(ids)
-    d = Dump(ids, np.zeros((n, G, S), np.int32), np.zeros((n, G), np.uint64), np.zeros((n, G), np.float64),
-             np.zeros(n, SUMMARY_DTYPE))
+    d = Dump(ids, _host_array((n, G, S), np.int32, pinned), _host_array((n, G), np.uint64, pinned),
+             _host_array((n, G), np.float64, pinned), _host_array(n, SUMMARY_DTYPE, pinned))
     cd = ssa_dump(n, ids.ctypes.data_as(C.POINTER(C.c_uint64)), d.states.ctypes.data, d.events_at.ctypes.data,
                   d.time_at.ctypes.data, d.summary.ctypes.data)
     return d, cd
@@ -284,19 +299,21 @@ def _make_dump(ids, G, S):
 def _result_from(r: ssa_result, st: int, mean, var, m2, count, dump=None) -> RunResult:
     return RunResult(mean, var, m2, count, r.events, r.near_ties, r.n_errors, r.first_error_id,
                      r.first_error_reaction, r.path_used, r.device_ms, r.ssa_ms, r.jit_ms, r.h2d_bytes,
-                     r.d2h_bytes, r.kernel_launches, st, dump, r.reduce_ms, r.reduce_bytes)
+                     r.d2h_bytes, r.kernel_launches, st, dump, r.reduce_ms, r.reduce_bytes, r.dump_ms,
+                     r.dump_bytes)
 
 
 def run(model: Model, n_trajectories: int, t_end: float, sample_dt: float, seed: int, *,
         reducers: int = SSA_REDUCE_MEAN | SSA_REDUCE_VAR, path: int = SSA_PATH_AUTO, dump_ids=None,
-        raise_on_error: bool = True, **opts) -> RunResult:
-    """ssa_run with host outputs: mean/var/m2/count as [G, S] numpy arrays."""
+        dump_pinned: bool = False, raise_on_error: bool = True, **opts) -> RunResult:
+    """ssa_run with host outputs: mean/var/m2/count as [G, S] numpy arrays (the dump's arrays in
+    page-locked memory with dump_pinned=True)."""
     G = grid_size(t_end, sample_dt)
     S = model.S
     mean = np.zeros((G, S)); var = np.zeros((G, S)); m2 = np.zeros((G, S)); count = np.zeros((G, S))
     dump = cdump = None
     if dump_ids is not None and len(dump_ids):
-        dump, cdump = _make_dump(dump_ids, G, S)
+        dump, cdump = _make_dump(dump_ids, G, S, dump_pinned)
     o = _options(path=path, dump=cdump, **opts)
     r = ssa_result()
     r.mean, r.var, r.m2, r.count = mean.ctypes.data, var.ctypes.data, m2.ctypes.data, count.ctypes.data
