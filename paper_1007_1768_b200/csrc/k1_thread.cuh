@@ -251,16 +251,20 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // a8: apply the selected reaction
 #if SSA_K1_RECORD == 1
         {   // full event stream (union-time selective memory): time, reaction,
-            // pre-event counts, in this lane's current block of reserved rows
+            // pre-event counts, in this lane's current block of reserved rows;
+            // the counts are stored by the update's own jump-table case
             const ssa_u64 pos = rec_row();
+            int* out = nullptr;
             if (pos < P.rec_cap) {
                 P.rec_t[pos] = tn;
                 P.rec_j[pos] = j;
-                ssa_record_pre(j, x, P.rec_pre + pos * SSA_REC_U);
+                out = P.rec_pre + pos * SSA_REC_U;
             }
+            ssa_apply_rec(j, x, out);
         }
-#endif
+#else
         ssa_apply(j, x);
+#endif
         if (ssa_khat_dirty(j)) ssa_khat(x, kh SSA_KP_ARG);   // a modifier species changed
         t = tn;
         ++e;

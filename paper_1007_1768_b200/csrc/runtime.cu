@@ -514,18 +514,31 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
     bool exact_imm = true;   // every delta is an exact fp64 immediate (|d| < 2^53)
     for (int j = 0; j < R; ++j)
         for (auto& d : m.rx[j].nu) exact_imm = exact_imm && std::llabs(d.second) < (1ll << 53);
-    o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
-    if (g.flat_switch && any_nu && exact_imm && S <= 28 && R <= 4096) {
-        // a8 as ONE indirect branch through a jump table (PTX brx.idx): the
-        // C++ switch compiles to a decision tree of small tables, several
-        // dependent branches deep.  Operands: %0..%(S-1) = x, %S = j.
-        o << "  asm volatile(\"{\\n\\t"
-          << "ssa_apply_tab: .branchtargets ";
-        for (int j = 0; j < R; ++j) o << (j ? ", " : "") << "ssa_apply_" << j;
-        o << ";\\n\\tbrx.idx %" << S << ", ssa_apply_tab;\\n\\t";
-        for (int j = 0; j < R; ++j) {
-            o << "ssa_apply_" << j << ":\\n\\t";
-            for (auto& d : m.rx[j].nu) {
+    const bool use_brx = g.flat_switch && any_nu && exact_imm && S <= 28 && R <= 4096;
+    // a8 as ONE indirect branch through a jump table (PTX brx.idx): the C++
+    // switch compiles to a decision tree of small tables, several dependent
+    // branches deep.  Operands: %0..%(S-1) = x, %S = j; with rec (event
+    // recording), %(S+1) = the row's pre-event count slots (null: row dropped),
+    // written in the same case as the update (the C++ switch of the record
+    // costs another decision tree per event).
+    auto emit_brx = [&](bool rec) {
+        const std::string pfx = rec ? "ssa_applyr_" : "ssa_apply_";
+        o << "  asm volatile(\"{\\n\\t";
+        if (rec) o << ".reg .pred pst;\\n\\t.reg .s32 rr;\\n\\tsetp.ne.u64 pst, %" << S + 1 << ", 0;\\n\\t";
+        o << pfx << "tab: .branchtargets ";
+        for (int jj = 0; jj < R; ++jj) o << (jj ? ", " : "") << pfx << jj;
+        o << ";\\n\\tbrx.idx %" << S << ", " << pfx << "tab;\\n\\t";
+        for (int jj = 0; jj < R; ++jj) {
+            o << pfx << jj << ":\\n\\t";
+            if (rec) {
+                int q = 0;
+                for (auto& d : m.rx[jj].nu) {
+                    o << "cvt.rzi.s32.f64 rr, %" << d.first << ";\\n\\t@pst st.global.s32 [%" << S + 1 << "+" << 4 * q
+                      << "], rr;\\n\\t";
+                    ++q;
+                }
+            }
+            for (auto& d : m.rx[jj].nu) {
                 double v = (double)d.second;
                 unsigned long long bits;
                 memcpy(&bits, &v, 8);
@@ -533,31 +546,42 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
                 snprintf(hx, sizeof hx, "0d%016llX", bits);
                 o << "add.rn.f64 %" << d.first << ", %" << d.first << ", " << hx << ";\\n\\t";
             }
-            o << "bra ssa_apply_end;\\n\\t";
+            o << "bra " << pfx << "end;\\n\\t";
         }
-        o << "ssa_apply_end:\\n\\t}\"\n    : ";
+        o << pfx << "end:\\n\\t}\"\n    : ";
         for (int s2 = 0; s2 < S; ++s2) o << (s2 ? ", " : "") << "\"+d\"(x[" << s2 << "])";
-        o << "\n    : \"r\"(j));\n}\n";
+        o << "\n    : \"r\"(j)" << (rec ? ", \"l\"(out)" : "") << (rec ? "\n    : \"memory\"" : "") << ");\n";
+    };
+    o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
+    if (use_brx) {
+        emit_brx(false);
+        o << "}\n";
     } else {
         o << "  switch (j) {\n";
-        for (int j = 0; j < R; ++j) {
-            if (m.rx[j].nu.empty()) continue;
-            o << "  case " << j << ":";
-            for (auto& d : m.rx[j].nu) o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
+        for (int jj = 0; jj < R; ++jj) {
+            if (m.rx[jj].nu.empty()) continue;
+            o << "  case " << jj << ":";
+            for (auto& d : m.rx[jj].nu) o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
             o << " break;\n";
         }
         o << "  default: break;\n  }\n  (void)x;\n}\n";
     }
     if (record == 1) {
-        o << "static __device__ __forceinline__ void ssa_record_pre(int j, const double (&x)[SSA_S], int* out) {\n"
-          << "  switch (j) {\n";
-        for (int j = 0; j < R; ++j) {
-            if (m.rx[j].nu.empty()) continue;
-            o << "  case " << j << ":";
-            for (size_t q = 0; q < m.rx[j].nu.size(); ++q) o << " out[" << q << "] = (int)x[" << m.rx[j].nu[q].first << "];";
-            o << " break;\n";
+        // pre-event counts of the species reaction j changes, in nu order, then x += nu_j
+        o << "static __device__ __forceinline__ void ssa_apply_rec(int j, double (&x)[SSA_S], int* out) {\n";
+        if (use_brx) {
+            emit_brx(true);
+        } else {
+            o << "  if (out) switch (j) {\n";
+            for (int jj = 0; jj < R; ++jj) {
+                if (m.rx[jj].nu.empty()) continue;
+                o << "  case " << jj << ":";
+                for (size_t q = 0; q < m.rx[jj].nu.size(); ++q) o << " out[" << q << "] = (int)x[" << m.rx[jj].nu[q].first << "];";
+                o << " break;\n";
+            }
+            o << "  default: break;\n  }\n  ssa_apply(j, x);\n";
         }
-        o << "  default: break;\n  }\n  (void)x; (void)out;\n}\n";
+        o << "}\n";
     }
     return o.str();
 }
@@ -1776,7 +1800,7 @@ extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, in
 {
     static thread_local std::string s;
     if (!m) return "";
-    s = k1_full_source(*m, block, minb, dump != 0, nullptr, seed);
+    s = k1_full_source(*m, block, minb, (dump & 1) != 0, nullptr, seed, (dump >> 1) & 3);   // bits 1-2: record mode
     return s.c_str();
 }
 
