@@ -37,6 +37,18 @@ TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
 FP64_PER_SMSP_CLK = 0.497   # DADD/DMUL/DFMA issue rate per SMSP per clock, profiles/r1h_pipe_peaks.txt
 
 
+def profiled_activity(workload: str, kernel: str):
+    """ncu's issue-slot and FP64-pipe activity of `kernel` (smsp__issue_active,
+    sm__pipe_fp64_cycles_active) from the committed capture named in profiles/traffic.json."""
+    if not os.path.exists(TRAFFIC_FILE):
+        return None
+    e = json.load(open(TRAFFIC_FILE)).get(workload, {}).get(kernel, {})
+    if "issue_active" not in e:
+        return None
+    return {"issue_active": e["issue_active"], "fp64_pipe_active": e.get("fp64_pipe_active"),
+            "source": e.get("activity_source")}
+
+
 def measured_traffic(workload: str, kernel: str, default_size: bool):
     """DRAM read+write bytes per launch of `kernel` from the committed ncu pass (profiles/traffic.json),
     for the default-size workload only (other sizes: None)."""
@@ -596,7 +608,8 @@ def main():
     kname = "ssa_k1" if path == 1 else "ssa_k2"
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
                 "traffic": measured_traffic(workload, kname, default_size),
-                "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)", "kernel": "ssa_k1" if path == 1 else ("ssa_k2" if path == 2 else "ssa_k2 (half-warp)"),
+                "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write per launch)",
+                "ncu_activity": profiled_activity(workload, kname), "kernel": "ssa_k1" if path == 1 else ("ssa_k2" if path == 2 else "ssa_k2 (half-warp)"),
                 ("alg_thread_instr_per_event" if path == 1 else "alg_warp_instr_per_event"): I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
     if path == 1:

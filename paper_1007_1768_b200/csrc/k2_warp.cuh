@@ -108,8 +108,12 @@ static __device__ __forceinline__ double k2_propensity_d(const k2_rxd& d, const 
     const double f1 = k2_factor_bf(x[d.sab & 0xFFFF], d.mab & 0xFF);
     const double f2 = k2_factor_bf(x[(unsigned)d.sab >> 16], d.mab >> 8);
     const double h = __dmul_rn(f1, f2);
+#if SSA_HAS_MODS
     double k = __dadd_rn(d.rate, __dmul_rn(d.modc, x[d.sms & 0xFFFF]));
     k = (k < 0.0) ? 0.0 : k;
+#else
+    const double k = d.rate;   // no modifier in the model: k + 0*x = k exactly
+#endif
     return k2_gated(__dmul_rn(k, h), d.gw, x);
 }
 #endif

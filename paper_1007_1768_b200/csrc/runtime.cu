@@ -739,11 +739,12 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
 {
     // longest net-change list and longest per-reaction dependency list (as
     // built by ensure_k2), and whether any reactant has coefficient 3
-    int nu_max = 0, dep_max = 0, m3 = 0, gates = 0;
+    int nu_max = 0, dep_max = 0, m3 = 0, gates = 0, mods = 0;
     std::vector<std::vector<int>> readers(m.S);
     for (int j = 0; j < m.R; ++j) {
         nu_max = std::max(nu_max, (int)m.rx[j].nu.size());
         gates |= !m.rx[j].gates.empty();
+        mods |= (m.rx[j].mod_sp >= 0);
         for (auto& t : m.rx[j].reac) {
             readers[t.first].push_back(j);
             m3 |= (t.second == 3);
@@ -762,7 +763,7 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
     o << "#define SSA_S " << m.S << "\n#define SSA_R " << m.R << "\n#define SSA_P " << P << "\n#define SSA_K2_BLOCK "
       << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0)
       << "\n#define SSA_K2_HALF " << (half ? 1 : 0)
-      << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
+      << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_HAS_MODS " << mods << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
     o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
     return o.str();

@@ -16,7 +16,8 @@ timeout 900 python bench.py --config 3 --no-cpu-baseline > gpurun_out/bench_c3.j
 timeout 900 python bench.py --workload sweep > gpurun_out/bench_sweep.json 2> gpurun_out/bench_sweep.err
 timeout 900 python bench.py --workload union --steps 2 --warmup 1 > gpurun_out/bench_union.json 2> gpurun_out/bench_union.err
 timeout 900 python bench.py --workload trajectories --steps 2 --warmup 1 > gpurun_out/bench_traj.json 2> gpurun_out/bench_traj.err
+timeout 900 python bench.py --workload dump > gpurun_out/bench_dump.json 2> gpurun_out/bench_dump.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-tail -n1 gpurun_out/bench_c3.json gpurun_out/bench_sweep.json gpurun_out/bench_union.json gpurun_out/bench_traj.json gpurun_out/bench_ref.json
+tail -n1 gpurun_out/bench_c3.json gpurun_out/bench_sweep.json gpurun_out/bench_union.json gpurun_out/bench_traj.json gpurun_out/bench_dump.json gpurun_out/bench_ref.json
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1; echo "ncu rc=$?"

@@ -320,6 +320,26 @@ def test_device_outputs_and_determinism(S):
     assert np.array_equal(h.mean, h2.mean) and h.events == h2.events
 
 
+def test_dump_accounting_and_pinned(S):
+    """a11 dump: dump_bytes is the payload (states, events_at, time_at, summaries), the D2H is timed
+    (dump_ms), and page-locked host arrays receive the same bytes as pageable ones."""
+    cfg = inputs.config(0)
+    m = S.Model(cfg.network)
+    G = S.grid_size(cfg.t_end, cfg.dt)
+    ids = np.array([0, 3, 17, 999], dtype=np.uint64)
+    a = S.run(m, cfg.n_trajectories, cfg.t_end, cfg.dt, cfg.seed, dump_ids=ids)
+    b = S.run(m, cfg.n_trajectories, cfg.t_end, cfg.dt, cfg.seed, dump_ids=ids, dump_pinned=True)
+    n = len(ids)
+    assert a.dump_bytes == n * G * (4 * m.S + 8 + 8) + n * S.SUMMARY_DTYPE.itemsize
+    assert a.dump_bytes == b.dump_bytes and a.d2h_bytes >= a.dump_bytes
+    assert a.dump_ms > 0.0 and b.dump_ms > 0.0
+    for f in ("states", "events_at", "time_at"):
+        assert np.array_equal(getattr(a.dump, f), getattr(b.dump, f))
+    assert a.dump.summary.tobytes() == b.dump.summary.tobytes()
+    c = S.run(m, cfg.n_trajectories, cfg.t_end, cfg.dt, cfg.seed)
+    assert c.dump_bytes == 0 and c.dump_ms == 0.0
+
+
 # ------------------------------------------------------------ gated propensities (NEXT 3)
 @pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_gated_networks_parity(S, path):
