@@ -281,3 +281,43 @@ def test_hiv_variant_b_structure(oracle_lib):
         assert np.all(np.diff(gx[:, :, 9], axis=1) >= 0)
         assert np.all(gx[:, 0, 7] == 0)
         assert bool(np.any(gx[:, :, 7] > 0)) == expect_v4
+
+
+def test_hiv_linear_subnetwork_closed_form(oracle_lib):
+    """HIV network (Table 1) with the infection, mutation and infectivity rates set to
+    zero (beta = gamma = mu = K = 0): no cell is infected, so I4 = I5 = V4 = F = 0 and what remains is
+    first order -- U0 -> U0 + U (lambda), U -> T (d_ut), U -> Z4 and U -> Z5 (d_uz each), T, Z4, Z5
+    and V5 clearance.  For a first-order network the means solve the linear rate equations exactly:
+      U(t)  = A + B e^{-a t},  a = d_ut + 2 d_uz, A = lambda / a, B = U(0) - A
+      T(t)  = T0 e^{-d_t t} + d_ut [A (1 - e^{-d_t t}) / d_t + B (e^{-a t} - e^{-d_t t}) / (d_t - a)]
+      Zi(t) = Z0 e^{-d_z t} + d_uz [A (1 - e^{-d_z t}) / d_z + B (e^{-a t} - e^{-d_z t}) / (d_z - a)]
+    and V5 is a pure death: Binomial(100, e^{-d_v t}).  Pins the oracle's reading of Table 1's
+    reaction list (which species each reaction consumes and produces, and at which rate)."""
+    O = oracle_lib
+    p = inputs.networks.HIV_PARAMS
+    net = inputs.hiv(beta=0.0, gamma=0.0, mu=0.0, K=0.0)
+    n, t_end = 2000, 20.0
+    res = O.run(O.OracleModel(net), np.arange(n), 3, t_end, 1.0, keep=False)
+    assert res.status == 0
+    lam, d_ut, d_uz, d_t, d_z, d_v = p["lam"], p["d_ut"], p["d_uz"], p["d_t"], p["d_z"], p["d_v"]
+    x0 = net.x0
+    a = d_ut + 2 * d_uz
+    A = lam / a
+    B = x0[1] - A
+
+    def conv(rate_in, d, y0, t):
+        return y0 * math.exp(-d * t) + rate_in * (A * (1 - math.exp(-d * t)) / d
+                                                  + B * (math.exp(-a * t) - math.exp(-d * t)) / (d - a))
+
+    for k in range(1, int(t_end) + 1):
+        t = float(k)
+        mu = {1: A + B * math.exp(-a * t), 2: conv(d_ut, d_t, x0[2], t),
+              3: conv(d_uz, d_z, x0[3], t), 4: conv(d_uz, d_z, x0[4], t)}
+        for s, m_s in mu.items():
+            assert _zmean(res.mean[k, s], m_s, res.var[k, s], n) < 4.5, (k, s, res.mean[k, s], m_s)
+        q = math.exp(-d_v * t)
+        v5 = 100 * q
+        assert _zmean(res.mean[k, 8], v5, 100 * q * (1 - q), n) < 4.5, (k, res.mean[k, 8], v5)
+        for s in (5, 6, 7, 9):
+            assert res.mean[k, s] == 0 and res.var[k, s] == 0
+        assert res.mean[k, 0] == 1 and res.var[k, 0] == 0
