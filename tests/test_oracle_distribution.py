@@ -15,15 +15,15 @@ Z = 4.0
 
 
 def _zmean(m, mu, var, n):
-    if var == 0:
-        return 0.0 if m == mu else np.inf
+    if var < 1e-12:   # a point mass (CME moments carry rounding of order 1e-16)
+        return 0.0 if abs(m - mu) < 1e-9 else np.inf
     return abs(m - mu) / math.sqrt(var / n)
 
 
 def _zvar(v, var, mu4, n):
     # var of the sample (population) variance ~ (mu4 - sigma^4)/n
     d = mu4 - var * var
-    if d <= 0:
+    if d <= 1e-24:    # a point mass
         return 0.0 if abs(v - var) < 1e-12 else np.inf
     return abs(v - var) / math.sqrt(d / n)
 
@@ -321,3 +321,43 @@ def test_hiv_linear_subnetwork_closed_form(oracle_lib):
         for s in (5, 6, 7, 9):
             assert res.mean[k, s] == 0 and res.var[k, s] == 0
         assert res.mean[k, 0] == 1 and res.var[k, 0] == 0
+
+
+def _mini_hiv(swap_modifier_signs: bool = False):
+    """Table 1's reaction list on a finite state space: immigration (lambda), the bursts (pi) and the
+    productions that need no consumption (s1, s2, s3) off, F held at 2 so the infectivity modifiers
+    (d = -K on reactions 8 and 10, +K on 9 and 11) and the F-catalysed clearances
+    (reactions 2 and 7) are active; rates raised so every reaction fires within a few time units."""
+    p = dict(lam=0.0, d_uf=0.3, d_ut=0.5, d_uz=0.2, d_t=0.1, d_tf=0.2, beta=0.6, K=0.1, gamma=0.4,
+             s1=0.0, s2=0.0, d_iz=0.5, mu=0.3, pi=0.0, s3=0.0, d_z=0.1, d_v=0.3)
+    net = inputs.hiv(**p)
+    rx = list(net.reactions)
+    if swap_modifier_signs:
+        from inputs.networks import Reaction
+        for j in (7, 8, 9, 10):
+            r = rx[j]
+            rx[j] = Reaction(r.reactants, r.products, r.rate, r.modifier_species, -r.modifier_coef, r.name,
+                             r.mass_action, r.gates)
+    return Network(net.species, (1, 2, 2, 1, 1, 0, 0, 0, 2, 2), tuple(rx), "mini-hiv")
+
+
+def test_cme_mini_hiv_reaction_list(oracle_lib):
+    """The HIV reaction list (incl. the bimolecular infections, the I+Z clearances, the mutation and
+    the signed infectivity modifiers) against the chemical master equation on its 1155 reachable
+    states; the opposite modifier signs are rejected by the same data."""
+    O = oracle_lib
+    net = _mini_hiv()
+    t_end, dt, n = 3.0, 0.5, 20000
+    times = [k * dt for k in range(int(t_end / dt) + 1)]
+    ref, nstates = _cme_moments(net, times)
+    assert nstates == 1155
+    res = O.run(O.OracleModel(net), np.arange(n), 21, t_end, dt, keep=False)
+    assert res.status == 0
+    for k, (mu, var, mu4) in enumerate(ref):
+        for s in range(net.S):
+            assert _zmean(res.mean[k, s], mu[s], var[s], n) < Z, (k, s)
+            assert _zvar(res.var[k, s], var[s], mu4[s], n) < Z, (k, s)
+    ref_alt, _ = _cme_moments(_mini_hiv(swap_modifier_signs=True), times)
+    worst = max(_zmean(res.mean[k, s], ref_alt[k][0][s], ref_alt[k][1][s], n)
+                for k in range(1, len(times)) for s in (5, 6))
+    assert worst > 10, worst
