@@ -280,6 +280,15 @@ def test_trimolecular_and_modifier_network(S, path):
     _parity(S, net, 700, 6.0, 0.25, 17, path)
 
 
+@pytest.mark.parametrize("path", [THREAD, WARP, HALF])
+def test_mini_hiv_parity(S, path):
+    """The HIV reaction list on its finite CME-pinned version (tests/test_oracle_distribution.py:
+    infections with signed infectivity modifiers at F = 2, I+Z clearances, mutation): every
+    reaction fires; bit-exact against the oracle on every path."""
+    from .test_oracle_distribution import _mini_hiv
+    _parity(S, _mini_hiv(), 1500, 3.0, 0.25, 21, path)
+
+
 def test_numeric_error_reported(S):
     """A propensity that overflows to inf (SPEC.md:85 'NaN/inf -> hard error
     naming the reaction'): SSA_ERR_NUMERIC with the id and reaction."""
