@@ -23,7 +23,13 @@
 extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(const ssa_k2_params P)
 {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    const int lane = threadIdx.x & 31;
+    // The lane index and the shared-memory window address of this half's state
+    // are computed once and kept opaque (asm volatile): otherwise, at this
+    // register budget, the compiler re-derives them (S2R of TID / CgaCtaId,
+    // tens of cycles of latency) inside the event loop.
+    int lane_ = threadIdx.x & 31;
+    asm volatile("" : "+r"(lane_));
+    const int lane = lane_;
     const int warp = threadIdx.x >> 5;
     const int h = lane >> 4;                 // which half (trajectory slot) of the warp
     const int hl = lane & 15;                // lane within the half
@@ -34,6 +40,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     k2_rx* rx = (k2_rx*)k2_smem_raw;
     double* x0 = (double*)(rx + (SSA_HAS_M3 ? SSA_R : 0));
     double* x = x0 + SSA_S + (size_t)warp * 2 * (SSA_S + SSA_HL * SSA_P) + (size_t)h * (SSA_S + SSA_HL * SSA_P);
+    {
+        unsigned xs = (unsigned)__cvta_generic_to_shared(x);
+        asm volatile("" : "+r"(xs));
+        x = (double*)__cvta_shared_to_generic(xs);
+    }
     double* a = x + SSA_S;                                     // a[q*16 + l]: reaction l*P + q
     int* nu_off = (int*)(x0 + SSA_S + (size_t)SSA_K2_WARPS * 2 * (SSA_S + SSA_HL * SSA_P));
     int* nu_ent = nu_off + (SSA_R + 1);
