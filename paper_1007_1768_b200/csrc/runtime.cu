@@ -918,6 +918,20 @@ static ssa_u64 next_pow2(ssa_u64 v)
     return p;
 }
 
+template <int N>
+struct Events {   // CUDA events, destroyed on every exit path (including a failed create)
+    cudaEvent_t e[N] = {};
+    ~Events() { for (cudaEvent_t x : e) if (x) cudaEventDestroy(x); }
+    cudaError_t create()
+    {
+        for (cudaEvent_t& x : e) {
+            const cudaError_t r = cudaEventCreate(&x);
+            if (r != cudaSuccess) return r;
+        }
+        return cudaSuccess;
+    }
+};
+
 struct DevBuf {  // stream-ordered device allocation
     void* p = nullptr;
     cudaStream_t st = nullptr;
@@ -1202,13 +1216,9 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         if (!p_sum) { CU(dsum.alloc(sizeof(ssa_dev_summary) * n_dump, st)); p_sum = dsum.as<ssa_dev_summary>(); }
     }
 
-    cudaEvent_t ev0, ev1, evs0, evs1, evr1;
-    CU(cudaEventCreate(&ev0)); CU(cudaEventCreate(&ev1)); CU(cudaEventCreate(&evs0)); CU(cudaEventCreate(&evs1));
-    CU(cudaEventCreate(&evr1));
-    struct EvGuard {
-        cudaEvent_t a, b, c, d, e;
-        ~EvGuard() { cudaEventDestroy(a); cudaEventDestroy(b); cudaEventDestroy(c); cudaEventDestroy(d); cudaEventDestroy(e); }
-    } eg{ev0, ev1, evs0, evs1, evr1};
+    Events<5> eg;
+    CU(eg.create());
+    cudaEvent_t ev0 = eg.e[0], ev1 = eg.e[1], evs0 = eg.e[2], evs1 = eg.e[3], evr1 = eg.e[4];
     CU(cudaEventRecord(ev0, st));
     float ssa_ms_total = 0.f, reduce_ms_total = 0.f;
 
@@ -1304,29 +1314,26 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     CU(cudaEventRecord(ev1, st));
     CU(cudaMemcpyAsync(&info.stats, statsb.p, sizeof(ssa_dev_stats), cudaMemcpyDeviceToHost, st));
     info.d2h += sizeof(ssa_dev_stats);
-    cudaEvent_t evd0 = nullptr, evd1 = nullptr;
+    Events<2> evd;   // the dump copy's events
     if (n_dump) {
         info.dump_bytes = (dump->states ? sizeof(int) * n_dump * cells : 0) + (dump->events_at ? 8 * n_dump * G : 0) +
                           (dump->time_at ? 8 * n_dump * G : 0) + (dump->summary ? sizeof(ssa_dev_summary) * n_dump : 0);
     }
     if (n_dump && !dump_on_device) {
         info.d2h += info.dump_bytes;
-        CU(cudaEventCreate(&evd0));
-        CU(cudaEventCreate(&evd1));
-        CU(cudaEventRecord(evd0, st));
+        CU(evd.create());
+        CU(cudaEventRecord(evd.e[0], st));
         if (dump->states) CU(cudaMemcpyAsync(dump->states, p_states, sizeof(int) * n_dump * cells, cudaMemcpyDeviceToHost, st));
         if (dump->events_at) CU(cudaMemcpyAsync(dump->events_at, p_e, sizeof(ssa_u64) * n_dump * G, cudaMemcpyDeviceToHost, st));
         if (dump->time_at) CU(cudaMemcpyAsync(dump->time_at, p_t, sizeof(double) * n_dump * G, cudaMemcpyDeviceToHost, st));
         if (dump->summary) CU(cudaMemcpyAsync(dump->summary, p_sum, sizeof(ssa_dev_summary) * n_dump, cudaMemcpyDeviceToHost, st));
-        CU(cudaEventRecord(evd1, st));
+        CU(cudaEventRecord(evd.e[1], st));
     }
     CU(cudaStreamSynchronize(st));
     float ms = 0.f;
-    if (evd0) {
-        CU(cudaEventElapsedTime(&ms, evd0, evd1));
+    if (evd.e[0]) {
+        CU(cudaEventElapsedTime(&ms, evd.e[0], evd.e[1]));
         info.dump_ms = ms;
-        cudaEventDestroy(evd0);
-        cudaEventDestroy(evd1);
     }
     CU(cudaEventElapsedTime(&ms, ev0, ev1));
     info.device_ms = ms;
@@ -1591,9 +1598,9 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
         double* b = dout.as<double>();
         a.times = b; a.count = b + capacity; a.mean = b + 2 * capacity; a.var = b + (2 + S) * capacity;
     }
-    cudaEvent_t e0, e1;
-    CU(cudaEventCreate(&e0));
-    CU(cudaEventCreate(&e1));
+    Events<2> ev;
+    CU(ev.create());
+    cudaEvent_t e0 = ev.e[0], e1 = ev.e[1];
     CU(cudaEventRecord(e0, st));
     ssa_u64 np = 0;
     int launches = 0;
@@ -1602,8 +1609,6 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
     CU(cudaEventSynchronize(e1));
     float ums = 0.f;
     cudaEventElapsedTime(&ums, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     *n_points = np;
     r->events = info.stats.events;
     r->near_ties = info.stats.near_ties;
@@ -1696,8 +1701,9 @@ extern "C" ssa_status ssa_run_trajectories(const ssa_model* m, uint64_t n_trajec
         oe = (ssa_u64*)b; otm = (double*)(b + 8 * capacity); ot = (unsigned*)(b + 16 * capacity);
         os = (int*)(b + 20 * capacity);
     }
-    cudaEvent_t e0, e1, e2;
-    CU(cudaEventCreate(&e0)); CU(cudaEventCreate(&e1)); CU(cudaEventCreate(&e2));
+    Events<3> ev;
+    CU(ev.create());
+    cudaEvent_t e0 = ev.e[0], e1 = ev.e[1], e2 = ev.e[2];
     CU(cudaEventRecord(e0, st));
     ssa_u64 np = 0;
     int launches = 0;
@@ -1718,7 +1724,6 @@ extern "C" ssa_status ssa_run_trajectories(const ssa_model* m, uint64_t n_trajec
     float gms = 0.f, cms = 0.f;
     cudaEventElapsedTime(&gms, e0, e1);
     cudaEventElapsedTime(&cms, e1, e2);
-    cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
     r->device_ms = info.device_ms + gms + cms;
     r->ssa_ms = info.ssa_ms;
     r->reduce_ms = gms;                        // sort + gather of the points
