@@ -1806,7 +1806,10 @@ extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, in
 {
     static thread_local std::string s;
     if (!m) return "";
-    s = k1_full_source(*m, block, minb, (dump & 1) != 0, nullptr, seed, (dump >> 1) & 3);   // bits 1-2: record mode
+    // flags: bit 0 dump, bits 1-2 record mode, bit 3 the sweep variant (the model's own rates as one point)
+    PoolLayout L;
+    if (dump & 8) L = make_pool(*m, 1, nullptr, nullptr);
+    s = k1_full_source(*m, block, minb, (dump & 1) != 0, (dump & 8) ? &L : nullptr, seed, (dump >> 1) & 3);
     return s.c_str();
 }
 

@@ -195,11 +195,13 @@ class Model:
     def prepare(self, device: int = -1, path: int = SSA_PATH_AUTO):
         _check(lib().ssa_model_prepare(self.handle, device, path))
 
-    def k1_source(self, block: int = 128, minb: int = 4, dump: bool = False, seed: int = -1, record: int = 0) -> str:
+    def k1_source(self, block: int = 128, minb: int = 4, dump: bool = False, seed: int = -1, record: int = 0,
+                  sweep: bool = False) -> str:
         """Generated K1 source (dump=True: the variant with raw-trajectory dump + hash;
         seed >= 0: the variant with that seed's Philox key schedule compiled in; record 1/2:
         the event-recording / stride-point variants)."""
-        return lib().ssa_debug_k1_source(self.handle, block, minb, int(dump) | (record << 1), seed).decode()
+        flags = int(dump) | (record << 1) | (8 if sweep else 0)
+        return lib().ssa_debug_k1_source(self.handle, block, minb, flags, seed).decode()
 
     def k2_source(self, block: int = 256, dump: bool = False, half: bool = False) -> str:
         """Generated K2 (warp path; half=True: two trajectories per warp) source."""
