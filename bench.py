@@ -497,7 +497,10 @@ def main():
         if net.name != "hiv":
             raise SystemExit("--variant B applies to the HIV configs (2, 4)")
         net = inputs.hiv("B")
-    n_per = args.n_per_gpu or cfg.n_trajectories
+    # config 4 (box scale, 2^24 trajectories over 8 GPUs): one GPU runs one W=8 shard, 2^21
+    # trajectories, and weak scaling keeps that per GPU (N = 8: the full 2^24)
+    default_per_gpu = cfg.n_trajectories // 8 if args.config == 4 else cfg.n_trajectories
+    n_per = args.n_per_gpu or default_per_gpu
     n_total = n_per * world
     t_end = args.t_end or cfg.t_end
     dt = cfg.dt
@@ -604,7 +607,7 @@ def main():
         achieved = per_rank_events * I / (k1_ms / 1e3) / 1e9
     peak = n_sm * 4 * sm_max * 1e6 / 1e9                                  # G warp-instr/s
     workload = f"config{args.config}-{cfg.name}" + ("-variantB" if args.variant == "B" else "")
-    default_size = not args.n_per_gpu and not args.t_end
+    default_size = not args.n_per_gpu and not args.t_end and args.config != 4
     kname = "ssa_k1" if path == 1 else "ssa_k2"
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gwarp-inst/s", "frac": achieved / peak,
                 "traffic": measured_traffic(workload, kname, default_size),
