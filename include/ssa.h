@@ -153,7 +153,7 @@ typedef struct {
 } ssa_dump;
 
 typedef struct {
-    int32_t path;                  /* SSA_PATH_*: AUTO picks THREAD for R <= 64, HALFWARP for R <= 256, else WARP */
+    int32_t path;                  /* SSA_PATH_*: AUTO picks THREAD for R <= 160, HALFWARP for R <= 256, else WARP */
     int32_t device;                /* CUDA device ordinal; -1 = the calling thread's current device */
     void* stream;                  /* cudaStream_t to run on; NULL = a library-owned stream */
     uint64_t chunk;                /* trajectories per chunk (power of two); 0 = auto */

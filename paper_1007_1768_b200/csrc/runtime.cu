@@ -701,9 +701,12 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
 // SSA_PATH_AUTO: the thread path for R <= 64 (registers hold the prefix),
 // two trajectories per warp for R <= 256 (P = ceil(R/16) <= 16), else one
 // trajectory per warp.
+// Thresholds from the path A/B benchmark (scripts/path_ab.py): on synthetic networks
+// the thread path leads up to R = 128 (even with its prefix spilled past R ~ 64) and the half-warp
+// K2 from R = 192; the crossover lies near R = 160.
 static int auto_path(const ssa_model& m)
 {
-    return m.R <= 64 ? SSA_PATH_THREAD : (m.R <= 256 ? SSA_PATH_HALFWARP : SSA_PATH_WARP);
+    return m.R <= 160 ? SSA_PATH_THREAD : (m.R <= 256 ? SSA_PATH_HALFWARP : SSA_PATH_WARP);
 }
 
 // requires: current device == dev, m.mu held.  The K2 tables live in one
