@@ -652,8 +652,10 @@ static std::string k1_key(int block, int minb, bool dump, const PoolLayout* swee
 static int default_minb(const ssa_model& m, int block)
 {
     // target <= 128 registers per thread (512 threads/SM) for small networks;
-    // let large networks spill less by asking for fewer resident blocks.
-    const int threads = m.R <= 64 ? 512 : 256;
+    // let larger networks spill less by asking for fewer resident blocks
+    // (measured on synthetic networks, profiles/r1k_k1_blocks_per_sm.txt:
+    // 4 x 128 threads best up to R = 48, 3 x 128 for R = 56..80, 2 x 128 beyond)
+    const int threads = m.R <= 48 ? 512 : (m.R <= 80 ? 384 : 256);
     return std::max(1, threads / block);
 }
 
