@@ -220,11 +220,13 @@ ssa_status ssa_run_shard(const ssa_model* model, uint64_t id_begin, uint64_t id_
  * The model supplies species, stoichiometry, modifier species and initial
  * counts.  Every point simulates trajectories 0..n_per_point-1 with the same
  * seed (common random numbers across points, R31), so point p's
- * grids are bitwise those of ssa_run on the model with point p's constants.
+ * grids are bitwise those of ssa_run (thread path) on the model with point
+ * p's constants.
  * result->mean/var/m2/count are [n_points][G*S] (host, or device with
  * opts->outputs_on_device); the counters are totals over all points.  Dump ids
- * (opts->dump) are virtual ids p*n_per_point + i.  Thread path only
- * (SSA_ERR_UNSUPPORTED for the warp path); the points whose staging fits the
+ * (opts->dump) are virtual ids p*n_per_point + i.  Runs on the thread path
+ * at any size (AUTO included; an explicit WARP or HALFWARP path is
+ * SSA_ERR_UNSUPPORTED); the points whose staging fits the
  * budget run in one kernel launch.  Errors as ssa_run (first_error_id is the
  * virtual id). */
 ssa_status ssa_run_sweep(const ssa_model* model, int32_t n_points, const double* rates, const double* mod_coefs,

@@ -1490,7 +1490,9 @@ extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const 
     }
     RunInfo info;
     const bool on_dev = o && o->outputs_on_device;
-    TRY(run_range(m, 0, (ssa_u64)n_points * n_per_point, t_end, sample_dt, seed, o, c, sw.roots[0], info,
+    ssa_run_options ro = o ? *o : ssa_run_options{};
+    ro.path = SSA_PATH_THREAD;   // AUTO included: sweeps run on the thread path at any size
+    TRY(run_range(m, 0, (ssa_u64)n_points * n_per_point, t_end, sample_dt, seed, &ro, c, sw.roots[0], info,
                   o ? o->dump : nullptr, on_dev, &sw));
     ssa_status st = fill_result(info, r);
     // finalize every point into its [G*S] slab of the caller's arrays
