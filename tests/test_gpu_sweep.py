@@ -107,3 +107,18 @@ def test_sweep_rejects_warp_path(S):
     with pytest.raises(S.SSAError) as ei:
         S.run_sweep(m, inputs.rate_matrix(net, [1], [0.1, 0.2]), 10, 5.0, 1.0, 1, path=2)
     assert ei.value.status == 8
+
+
+def test_sweep_large_network_auto_runs_thread_path(S):
+    """A network past the thread path's AUTO threshold (R = 192 > 160): the sweep still runs on the
+    thread path under AUTO, and each point equals ssa_run on the thread path bitwise."""
+    net = inputs.synthetic(48, 192, seed=9)
+    base = np.array([r.rate for r in net.reactions])
+    rates = np.stack([base, base * 0.5])
+    N, t_end, dt, seed = 96, 0.2, 0.05, 5
+    m = S.Model(net)
+    sw = S.run_sweep(m, rates, N, t_end, dt, seed)
+    assert sw.status == 0 and sw.path_used == 1
+    for p in range(2):
+        one = S.run(S.Model(inputs.with_rates(net, rates[p])), N, t_end, dt, seed, path=1)
+        assert np.array_equal(sw.mean[p], one.mean) and np.array_equal(sw.var[p], one.var)
