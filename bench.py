@@ -362,7 +362,7 @@ def run_traj_bench(args, rank, world):
     cap = len(first.time)
     for _ in range(max(args.warmup - 1, 0)):
         S.run_trajectories(m, n, t_end, cfg.seed, 10, capacity=cap)
-    dev_ms, events, d2h, red_ms = [], 0, 0, []
+    dev_ms, events, d2h, red_ms, launches = [], 0, 0, [], 0
     with ClockSampler(0) as clk:
         for _ in range(args.steps):
             u = S.run_trajectories(m, n, t_end, cfg.seed, 10, capacity=cap)
@@ -370,6 +370,7 @@ def run_traj_bench(args, rank, world):
             red_ms.append(u.result.reduce_ms)
             d2h = u.result.d2h_bytes
             events += u.result.events
+            launches += u.result.kernel_launches
     ms = sum(dev_ms)
     line = {"metric": "ssa_events_per_s", "value": events / (ms / 1e3), "unit": "events/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -378,7 +379,7 @@ def run_traj_bench(args, rank, world):
                        "t_end": t_end, "stride": 10, "seed": cfg.seed, "points": cap,
                        "timing": "device time of each call incl. the D2H of the points (CUDA events in the library)"},
             "points_per_s": cap * args.steps / (ms / 1e3), "output_bytes_per_step": d2h,
-            "sort_gather_ms": statistics.mean(red_ms), "clocks": clk.summary()}
+            "sort_gather_ms": statistics.mean(red_ms), "gpu_launches": launches, "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     return 0
 
