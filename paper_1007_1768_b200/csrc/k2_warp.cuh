@@ -142,7 +142,11 @@ static __device__ __forceinline__ double k2_propensity(const k2_rx& q, const dou
 extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(const ssa_k2_params P)
 {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    const int lane = threadIdx.x & 31;
+    // lane index and the warp's state address computed once and kept opaque (as
+    // in the half-warp kernel: no S2R re-derivation inside the event loop)
+    int lane_ = threadIdx.x & 31;
+    asm volatile("" : "+r"(lane_));
+    const int lane = lane_;
     const int warp = threadIdx.x >> 5;
     const unsigned FULL = 0xffffffffu;
     // shared: rx[R] | x0[S] | per warp (x[S] | a[P][32]) | nu_off[R+1] | nu_ent | dep_off[R+1] | dep_ent
@@ -150,6 +154,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     k2_rx* rx = (k2_rx*)k2_smem_raw;
     double* x0 = (double*)(rx + (SSA_HAS_M3 ? SSA_R : 0));
     double* x = x0 + SSA_S + (size_t)warp * (SSA_S + 32 * SSA_P);
+    {
+        unsigned xs = (unsigned)__cvta_generic_to_shared(x);
+        asm volatile("" : "+r"(xs));
+        x = (double*)__cvta_shared_to_generic(xs);
+    }
     double* a = x + SSA_S;                                     // a[q*32 + l]: reaction l*P + q
     int* nu_off = (int*)(x0 + SSA_S + (size_t)SSA_K2_WARPS * (SSA_S + 32 * SSA_P));
     int* nu_ent = nu_off + (SSA_R + 1);
