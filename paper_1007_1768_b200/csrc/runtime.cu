@@ -102,6 +102,7 @@ struct K2Dev {
 struct DevCache {
     std::map<std::string, K1Entry> k1;  // k1_key(block, minb, dump, sweep layout)
     K2Dev k2;
+    double* prof = nullptr;             // [R] propensity-share sums of a profiling run (device)
 };
 
 struct ssa_model {
@@ -111,6 +112,12 @@ struct ssa_model {
     mutable std::mutex mu;
     mutable std::map<int, DevCache> dev;
     mutable double* pinned_const = nullptr;  // [constant pool][x0 S], page-locked, for per-run uploads
+    // K1 dispatch profile (results are identical with or without it): the
+    // reactions that dominate the event stream, measured by the first thread-path
+    // run (propensity shares sampled at grid crossings) and applied by predicated
+    // adds ahead of the update's jump table in later runs
+    mutable std::vector<int> hot;
+    mutable bool hot_known = false;
 };
 
 struct PoolLayout;
@@ -226,6 +233,7 @@ extern "C" void ssa_model_destroy(ssa_model* m)
                 if (e.second.lib) cudaLibraryUnload(e.second.lib);
             for (auto& e : kv.second.k1)
                 if (e.second.lib) cudaLibraryUnload(e.second.lib);
+            if (kv.second.prof) cudaFree(kv.second.prof);
         }
         cudaSetDevice(cur);
     }
@@ -361,19 +369,27 @@ static std::string prop_stmts(const RxI& q, int j, const PoolLayout& L, int kh =
 // K1 code-generation variants (tuning; the arithmetic is identical in all of
 // them).  SSA_K1_GEN is read once per process:
 //   upd=brx|switch   a8 as one brx.idx jump table (default) or a C++ switch
-//   hot=a:b:...      the listed reactions are applied by predicated adds and
-//                    only the other lanes take the jump table (HIV with
-//                    hot=26:25, the two clearances that make 98% of its events:
-//                    +1.7%; off by default -- the hot set is model- and
-//                    horizon-dependent and the library does not measure it)
+//   hot=a:b:...      override the measured hot set (K1Spec; run_range measures
+//                    it on a model's first plain thread-path run): the listed
+//                    reactions are applied by predicated adds and only the other
+//                    lanes take the jump table
+//   nospread32       small ensembles run the (128, minb) variant instead of a
+//                    (32, 1) one
 // (Measured and dropped: int64-pattern selection compares on the ALU pipe,
 // species counts in shared memory with a table update, and a warp-vote
 // pruning of the selection compares at static anchors were all slower.)
+// Dispatch specialisation of one K1 variant (the arithmetic is the same in all).
+struct K1Spec {
+    std::vector<int> hot;   // reactions applied by predicated adds ahead of the jump table
+    bool prof = false;      // sample the propensity shares at grid crossings
+};
+
 struct K1Gen {
     bool flat_switch = true;
     bool seed_imm = true;   // keys=imm|param: Philox round keys as instruction immediates (kernel per seed)
     int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
     std::vector<int> hot;   // hot=a:b:...: reactions updated by predicated adds ahead of the jump table
+    bool spread32 = true;   // small-ensemble launches use a (32, 1) launch-bounds variant (nospread32: off)
 };
 
 static K1Gen k1_gen()
@@ -386,6 +402,7 @@ static K1Gen k1_gen()
         if (s.find("keys=param") != std::string::npos) r.seed_imm = false;
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
+        if (s.find("nospread32") != std::string::npos) r.spread32 = false;
         const size_t h = s.find("hot=");
         if (h != std::string::npos) {
             size_t q = h + 4;
@@ -405,7 +422,7 @@ static K1Gen k1_gen()
 // shared memory through kp); L: the constant layout the code indexes.
 // seed >= 0: the run's Philox key schedule is compiled in as immediates.
 static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool dump, bool sweep, const PoolLayout& L,
-                                long long seed_bits, bool use_seed, int record = 0)
+                                long long seed_bits, bool use_seed, int record = 0, const K1Spec* spec = nullptr)
 {
     const int S = m.S, R = m.R;
     const K1Gen g = k1_gen();
@@ -421,6 +438,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
     } else {
         o << "#define SSA_K1_RECORD 0\n";
     }
+    o << "#define SSA_K1_PROF " << (spec && spec->prof ? 1 : 0) << "\n";
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
       << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
       << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
@@ -571,7 +589,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
     o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
     if (use_brx) {
         std::vector<int> hot;
-        for (int hj : g.hot)
+        for (int hj : (!g.hot.empty() ? g.hot : (spec ? spec->hot : std::vector<int>())))
             if (hj >= 0 && hj < R) hot.push_back(hj);
         if (!hot.empty()) {
             // the most frequent reactions as predicated adds; the jump table only
@@ -664,17 +682,23 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
 // seed: the run's seed when the key schedule is compiled in (K1Gen::seed_imm),
 // else -1 (keys from the launch parameters).
 static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep,
-                                  long long seed = -1, int record = 0)
+                                  long long seed = -1, int record = 0, const K1Spec* spec = nullptr)
 {
     const PoolLayout L = sweep ? *sweep : make_pool(m, 1, nullptr, nullptr);
     return std::string(kSsaDeviceSrc) + "\n" +
-           gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1, record) + "\n" + kK1ThreadSrc;
+           gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1, record, spec) + "\n" +
+           kK1ThreadSrc;
 }
 
-static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed, int record)
+static std::string k1_key(int block, int minb, bool dump, const PoolLayout* sweep, long long seed, int record,
+                          const K1Spec* spec = nullptr)
 {
     std::ostringstream o;
     o << block << "/" << minb << "/" << (dump ? 1 : 0) << "/" << seed << "/" << record;
+    if (spec) {
+        o << "/prof:" << (spec->prof ? 1 : 0) << "/hot";
+        for (int h : spec->hot) o << ":" << h;
+    }
     if (sweep) {
         o << "/sweep:" << sweep->n;
         for (size_t j = 0; j < sweep->rate_slot.size(); ++j)
@@ -695,10 +719,11 @@ static int default_minb(const ssa_model& m, int block)
 
 // requires: current device == dev, m.mu held
 static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bool dump, const PoolLayout* sweep,
-                            K1Entry** out, double* jit_ms, long long seed = -1, int record = 0)
+                            K1Entry** out, double* jit_ms, long long seed = -1, int record = 0,
+                            const K1Spec* spec = nullptr)
 {
     DevCache& dc = m.dev[dev];
-    const std::string key = k1_key(block, minb, dump, sweep, seed, record);
+    const std::string key = k1_key(block, minb, dump, sweep, seed, record, spec);
     auto it = dc.k1.find(key);
     if (it != dc.k1.end()) {
         *out = &it->second;
@@ -709,7 +734,7 @@ static ssa_status ensure_k1(const ssa_model& m, int dev, int block, int minb, bo
     e.block = block;
     e.minb = minb;
     std::vector<char> cubin;
-    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep, seed, record), cubin, e.log));
+    TRY(nvrtc_compile(k1_full_source(m, block, minb, dump, sweep, seed, record, spec), cubin, e.log));
     CU(cudaLibraryLoadData(&e.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
     CU(cudaLibraryGetKernel(&e.fn, e.lib, "ssa_k1"));
     // constant pool (plain runs) and x0 into the module's constant memory
@@ -1148,29 +1173,47 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     if (block % 32 || block > 1024) return fail(SSA_ERR_INVALID_ARG, "block %d must be a multiple of 32 <= 1024", block);
     int grid = 0;
     bool spread = false;
+    K1Spec spec;              // K1 dispatch profile: measured on the first plain run, then applied
+    double* prof = nullptr;   // the profiling run's share sums (device, [R])
     {
         std::lock_guard<std::mutex> lk(m->mu);
         if (path == SSA_PATH_THREAD) {
             // blocks_per_sm > 0 also sets the K1 variant's __launch_bounds__ residency
             // target (its register budget is 64K / (block * blocks_per_sm))
-            const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : default_minb(*m, block);
+            // small ensembles (at most one trajectory per SM sub-partition) are spread:
+            // one working lane per block of one warp (knob spread32: a variant JIT'd for
+            // that launch shape, __launch_bounds__(32, 1))
+            const bool spread_n = n_ids <= (ssa_u64)sms * 4 && !(o && o->block > 0);
+            const bool s32 = spread_n && k1_gen().spread32;
+            const int kblock = s32 ? 32 : block;
+            const int minb = (o && o->blocks_per_sm > 0) ? o->blocks_per_sm : (s32 ? 1 : default_minb(*m, block));
             // seed -1 is reserved for "keys from the parameters" (a seed of 2^64-1 takes that path)
             // (kernels per seed are cached; past 32 compiled variants of this model on
             // this device, new seeds take the launch-parameter keys to bound the cache)
+            if (!sw && !(rec && rec->mode == 1)) {
+                if (m->hot_known) {
+                    spec.hot = m->hot;
+                } else if (!rec && k1_gen().hot.empty()) {
+                    spec.prof = true;
+                    DevCache& dc = m->dev[c.device];
+                    if (!dc.prof) CU(cudaMalloc(&dc.prof, sizeof(double) * ((size_t)m->R + 1)));
+                    prof = dc.prof;
+                }
+            }
             long long kseed = k1_gen().seed_imm ? (long long)seed : -1;
             if (kseed != -1 && m->dev[c.device].k1.size() >= 32 &&
-                !m->dev[c.device].k1.count(k1_key(block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, kseed,
-                                                  rec ? rec->mode : 0)))
+                !m->dev[c.device].k1.count(k1_key(kblock, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, kseed,
+                                                  rec ? rec->mode : 0, &spec)))
                 kseed = -1;
-            TRY(ensure_k1(*m, c.device, block, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms,
-                          kseed, rec ? rec->mode : 0));
+            TRY(ensure_k1(*m, c.device, kblock, minb, dump && dump->n > 0, sw ? &sw->L : nullptr, &k1, &info.jit_ms,
+                          kseed, rec ? rec->mode : 0, &spec));
             int bps = k1->blocks_per_sm;
             if (o && o->blocks_per_sm > 0) bps = std::min(bps, o->blocks_per_sm);
             grid = sms * bps;
             grid = (int)std::min<ssa_u64>((ssa_u64)grid, (C + block - 1) / block);
             // small ensembles (at most one trajectory per SM sub-partition): one
             // working lane per block of one warp, spread over the SMs
-            if (n_ids <= (ssa_u64)sms * 4 && !(o && o->block > 0)) {
+            if (spread_n) {
                 spread = true;
                 grid = (int)n_ids;
             }
@@ -1228,6 +1271,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     CU(cudaMemsetAsync(statsb.p, 0, sizeof(ssa_dev_stats), st));
     CU(cudaMemsetAsync((char*)statsb.p + offsetof(ssa_dev_stats, first_err_id), 0xFF, sizeof(ssa_u64), st));
     CU(cudaMemsetAsync(work.p, 0, sizeof(ssa_u64) * n_chunks, st));
+    if (prof) CU(cudaMemsetAsync(prof, 0, sizeof(double) * ((size_t)m->R + 1), st));
 
     // dump
     ssa_u64 n_dump = dump ? dump->n : 0;
@@ -1289,6 +1333,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
                 smem = sizeof(double) * (size_t)p.n_pts * (size_t)p.n_pool;
             }
             p.spread = spread ? 1 : 0;
+            p.prof = prof;
             void* args[] = {&p};
             CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(spread ? 32 : block), args, smem, st));
             info.launches += 1;
@@ -1378,6 +1423,31 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     info.device_ms = ms;
     info.ssa_ms = ssa_ms_total;
     info.reduce_ms = reduce_ms_total;
+    if (prof) {
+        // choose the hot set from the sampled propensity sums (reaction j's share of the
+        // events ~ sum a_j / sum a0): the top reaction if it carries >= 1/2 of the events,
+        // the second too if the two carry >= 80% (more hot reactions measured slower,
+        // DESIGN.md §6); at least 32 samples
+        std::vector<double> h((size_t)m->R + 1);
+        CU(cudaMemcpy(h.data(), prof, sizeof(double) * h.size(), cudaMemcpyDeviceToHost));
+        const double samples = h[(size_t)m->R];
+        h.pop_back();
+        double tot = 0.0;
+        for (double v : h) tot += v;
+        if (samples >= 32.0 && tot > 0.0) {
+            std::vector<int> idx((size_t)m->R);
+            for (int j = 0; j < m->R; ++j) idx[(size_t)j] = j;
+            std::sort(idx.begin(), idx.end(), [&](int a, int b) { return h[(size_t)a] > h[(size_t)b]; });
+            std::vector<int> hot;
+            const double s1 = m->R > 0 ? h[(size_t)idx[0]] / tot : 0.0;
+            const double s2 = m->R > 1 ? h[(size_t)idx[1]] / tot : 0.0;
+            if (s1 >= 0.5) hot.push_back(idx[0]);
+            if (s1 >= 0.5 && s1 + s2 >= 0.8 && s2 > 0.05) hot.push_back(idx[1]);
+            std::lock_guard<std::mutex> lk(m->mu);
+            m->hot = hot;
+            m->hot_known = true;
+        }
+    }
     return SSA_OK;
 }
 
@@ -1843,6 +1913,18 @@ extern "C" int32_t ssa_abi_version(void) { return 1; }
 
 // Test/diagnostic hooks (not part of the stable ABI): the generated K1
 // source for a model, and compiling it without a device (NVRTC only).
+// The model's measured K1 hot set: the number of hot reactions written to out
+// (at most cap), or -1 if no profiling run has completed yet.
+extern "C" int32_t ssa_debug_model_hot(const ssa_model* m, int32_t* out, int32_t cap)
+{
+    if (!m) return -1;
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (!m->hot_known) return -1;
+    const int32_t n = (int32_t)m->hot.size();
+    for (int32_t i = 0; i < n && i < cap; ++i) out[i] = m->hot[(size_t)i];
+    return n;
+}
+
 extern "C" const char* ssa_debug_k1_source(const ssa_model* m, int32_t block, int32_t minb, int32_t dump, int64_t seed)
 {
     static thread_local std::string s;

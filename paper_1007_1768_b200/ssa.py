@@ -131,6 +131,8 @@ def lib():
         L.ssa_abi_version.restype = C.c_int32
         L.ssa_debug_k1_source.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int64]
         L.ssa_debug_k1_source.restype = C.c_char_p
+        L.ssa_debug_model_hot.argtypes = [C.c_void_p, P(C.c_int32), C.c_int32]
+        L.ssa_debug_model_hot.restype = C.c_int32
         L.ssa_debug_k1_compile.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_uint64,
                                            P(C.c_uint64)]
         L.ssa_debug_k1_compile.restype = C.c_int
@@ -202,6 +204,12 @@ class Model:
         the event-recording / stride-point variants)."""
         flags = int(dump) | (record << 1) | (8 if sweep else 0)
         return lib().ssa_debug_k1_source(self.handle, block, minb, flags, seed).decode()
+
+    def hot_set(self):
+        """The K1 hot set measured by this model's first plain thread-path run (None: not yet)."""
+        buf = (C.c_int32 * 8)()
+        n = lib().ssa_debug_model_hot(self.handle, buf, 8)
+        return None if n < 0 else [int(buf[i]) for i in range(min(n, 8))]
 
     def k2_source(self, block: int = 256, dump: bool = False, half: bool = False) -> str:
         """Generated K2 (warp path; half=True: two trajectories per warp) source."""
