@@ -277,8 +277,12 @@ ssa_status ssa_run_trajectories(const ssa_model* model, uint64_t n_trajectories,
 ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, uint64_t cells, const ssa_run_options* opts,
                            ssa_result* result);
 
-/* Compile (NVRTC) and load the model's K1 kernel for a device ahead of time
- * so that a later ssa_run does no JIT work.  path as in ssa_run_options. */
+/* Compile (NVRTC) and load the model's seed-independent kernel for a device
+ * ahead of time (K2, or K1 with the Philox keys as launch parameters) and
+ * check that it builds.  path as in ssa_run_options.  The thread path still
+ * compiles, once per model, device and seed, a variant with the seed's Philox
+ * round keys as instruction immediates, and after a model's first plain run a
+ * variant specialised on its measured dispatch profile; both are cached. */
 ssa_status ssa_model_prepare(const ssa_model* model, int32_t device, int32_t path);
 
 const char* ssa_status_string(ssa_status status);
