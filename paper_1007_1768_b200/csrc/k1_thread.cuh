@@ -154,6 +154,19 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // interleaves them.
         double c[SSA_R > 0 ? SSA_R : 1];
         const double a0 = ssa_prefix(x, kh, c SSA_KP_ARG);
+#if SSA_K1_PROF
+        // dispatch profile (a model's first thread-path run): at every 4096th event of a
+        // trajectory, the propensity shares a_j / a0 of the current state -- their mean
+        // estimates each reaction's share of the events; prof[R] counts the samples
+        if (P.prof && (e & 4095ull) == 4095ull && a0 > 0.0 && a0 < INF) {
+            double prev = 0.0;
+            for (int q = 0; q < SSA_R; ++q) {
+                atomicAdd(&P.prof[q], (c[q] - prev) / a0);
+                prev = c[q];
+            }
+            atomicAdd(&P.prof[SSA_R], 1.0);
+        }
+#endif
         // keep the prefix in registers: without this barrier the compiler
         // recomputes the whole propensity chain for the selection (a7)
 #pragma unroll
@@ -199,24 +212,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                         if (x[s] > 2147483647.0) status = 2;
                         dst[(ssa_u64)s * P.stride] = (int)x[s];
                     }
-#if SSA_K1_PROF
-                    // dispatch profile (first plain run of a model): the propensities a_j of
-                    // the current state at every 4th grid point, one lane per warp; their sums
-                    // estimate each reaction's share of the events (integral of a_j dt over
-                    // integral of a0 dt), and prof[R] counts the samples
-                    if (P.prof && k >= 4 && (k & 3) == 0 && (threadIdx.x & 31) == 0) {
-                        double cp[SSA_R > 0 ? SSA_R : 1];
-                        const double s0 = ssa_prefix(x, kh, cp SSA_KP_ARG);
-                        if (s0 > 0.0 && s0 < INF) {
-                            double prev = 0.0;
-                            for (int q = 0; q < SSA_R; ++q) {
-                                atomicAdd(&P.prof[q], cp[q] - prev);
-                                prev = cp[q];
-                            }
-                            atomicAdd(&P.prof[SSA_R], 1.0);
-                        }
-                    }
-#endif
 #if SSA_K1_DUMP
                     if (slot >= 0) {
                         const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;

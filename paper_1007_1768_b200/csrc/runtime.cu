@@ -586,11 +586,11 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         for (int s2 = 0; s2 < S; ++s2) o << (s2 ? ", " : "") << "\"+d\"(x[" << s2 << "])";
         o << "\n    : \"r\"(j)" << (rec ? ", \"l\"(out)" : "") << (rec ? "\n    : \"memory\"" : "") << ");\n";
     };
+    std::vector<int> hot;   // the dispatch profile's hot reactions (K1Spec, or the knob)
+    for (int hj : (!g.hot.empty() ? g.hot : (spec ? spec->hot : std::vector<int>())))
+        if (hj >= 0 && hj < R) hot.push_back(hj);
     o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
     if (use_brx) {
-        std::vector<int> hot;
-        for (int hj : (!g.hot.empty() ? g.hot : (spec ? spec->hot : std::vector<int>())))
-            if (hj >= 0 && hj < R) hot.push_back(hj);
         if (!hot.empty()) {
             // the most frequent reactions as predicated adds; the jump table only
             // for the lanes whose reaction is not among them
@@ -622,7 +622,26 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         // pre-event counts of the species reaction j changes, in nu order, then x += nu_j
         o << "static __device__ __forceinline__ void ssa_apply_rec(int j, double (&x)[SSA_S], int* out) {\n";
         if (use_brx) {
-            emit_brx(true);
+            if (!hot.empty()) {
+                // hot reactions: the record's stores and the adds predicated, the jump
+                // table only for the other lanes (as ssa_apply)
+                o << "  bool hot = false;\n";
+                for (int hj : hot) {
+                    o << "  if (j == " << hj << ") { hot = true;";
+                    o << " if (out) {";
+                    for (size_t q = 0; q < m.rx[hj].nu.size(); ++q)
+                        o << " out[" << q << "] = (int)x[" << m.rx[hj].nu[q].first << "];";
+                    o << " }";
+                    for (auto& d : m.rx[hj].nu)
+                        o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << (double)d.second << ");";
+                    o << " }\n";
+                }
+                o << "  if (!hot) {\n";
+                emit_brx(true);
+                o << "  }\n";
+            } else {
+                emit_brx(true);
+            }
         } else {
             o << "  if (out) switch (j) {\n";
             for (int jj = 0; jj < R; ++jj) {
@@ -1190,10 +1209,10 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             // seed -1 is reserved for "keys from the parameters" (a seed of 2^64-1 takes that path)
             // (kernels per seed are cached; past 32 compiled variants of this model on
             // this device, new seeds take the launch-parameter keys to bound the cache)
-            if (!sw && !(rec && rec->mode == 1)) {
+            if (!sw) {
                 if (m->hot_known) {
                     spec.hot = m->hot;
-                } else if (!rec && k1_gen().hot.empty()) {
+                } else if (k1_gen().hot.empty()) {
                     spec.prof = true;
                     DevCache& dc = m->dev[c.device];
                     if (!dc.prof) CU(cudaMalloc(&dc.prof, sizeof(double) * ((size_t)m->R + 1)));
@@ -1424,8 +1443,8 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     info.ssa_ms = ssa_ms_total;
     info.reduce_ms = reduce_ms_total;
     if (prof) {
-        // choose the hot set from the sampled propensity sums (reaction j's share of the
-        // events ~ sum a_j / sum a0): the top reaction if it carries >= 1/2 of the events,
+        // choose the hot set from the sampled propensity shares (their mean estimates each
+        // reaction's share of the events): the top reaction if it carries >= 1/2 of them,
         // the second too if the two carry >= 80% (more hot reactions measured slower,
         // DESIGN.md §6); at least 32 samples
         std::vector<double> h((size_t)m->R + 1);

@@ -110,3 +110,16 @@ def test_trajectory_points_hiv_and_rerun(S, monkeypatch):
         k, t, x = O.stride_points(om, i, 3, 0.2, 10)
         assert np.array_equal(got.event[sel], k) and np.array_equal(got.time[sel], t)
         assert np.array_equal(got.states[sel], x.astype(np.int32))
+
+
+def test_union_profiled_dispatch_bitwise(S):
+    """The first recording run of a model measures its K1 hot set (HIV: the clearances); the next
+    run records through the hot variant -- the event streams, and so every union point, are
+    bitwise those of the first run."""
+    m = S.Model(inputs.hiv())
+    a = S.run_union(m, 16, 5.0, 5, 16)
+    assert m.hot_set() is not None
+    b = S.run_union(m, 16, 5.0, 5, 16)
+    assert a.result.events == b.result.events
+    for f in ("times", "mean", "var", "count"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
