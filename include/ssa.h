@@ -78,7 +78,10 @@ typedef struct ssa_model ssa_model;
  * valid: the state is held).  On success *out owns the model;
  * release it with ssa_model_destroy.  Errors: SSA_ERR_INVALID_ARG (null
  * pointers), SSA_ERR_MODEL (with the reason in ssa_last_error()).  The model
- * is immutable and may be used from several threads at once. */
+ * is immutable and may be used from several threads at once.  (The library
+ * caches compiled kernels and a dispatch profile per model -- the reactions
+ * that dominate its event stream, measured by its first thread-path run; they
+ * change speed only, never results.) */
 ssa_status ssa_model_create(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
                             const ssa_reaction* reactions, ssa_model** out);
 /* Gated propensities (the paper's time-triggered
