@@ -76,6 +76,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     long long k = 0, slot = -1;
     int status = 0, absorbed = 0, err_r = -1;
 
+#if SSA_K1_SWEEP
+    ssa_u64 my_ptl = 0;                 // this lane's sweep point (chunk-local)
+#endif
     // a1: take the next trajectory id (atomic counter) and initialise it
     auto start = [&]() -> bool {
 #if SSA_K1_SWEEP
@@ -85,8 +88,17 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             // whole launch; the staging column stays point-major (dense per point)
             const ssa_u64 w = atomicAdd(P.work, 1ull);
             if (w >= P.n_ids) return false;
-            const ssa_u64 ptl = w % (ssa_u64)P.n_pts;
-            id = w / (ssa_u64)P.n_pts;          // trajectory id within its sweep point (RNG key)
+            ssa_u64 ptl;
+            if (P.pt_order) {
+                // points in the given order (costliest first, measured by an earlier run)
+                const ssa_u64 o = w / P.n_per_point;
+                ptl = (ssa_u64)P.pt_order[o];
+                id = w - o * P.n_per_point;
+            } else {
+                ptl = w % (ssa_u64)P.n_pts;
+                id = w / (ssa_u64)P.n_pts;      // trajectory id within its sweep point (RNG key)
+            }
+            my_ptl = ptl;
             rel = ptl * P.n_per_point + id;
             kp = s_k + ptl * (ssa_u64)P.n_pool;
         }
@@ -230,6 +242,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 // trajectory done: per-trajectory records, then refill (a1)
                 my_events += e;
                 my_ties += ties;
+#if SSA_K1_SWEEP
+                if (P.pt_events) atomicAdd(&P.pt_events[my_ptl], e);
+#endif
 #if SSA_K1_DUMP
                 if (slot >= 0) {
                     ssa_dev_summary sm;

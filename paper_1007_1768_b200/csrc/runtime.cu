@@ -118,6 +118,10 @@ struct ssa_model {
     // adds ahead of the update's jump table in later runs
     mutable std::vector<int> hot;
     mutable bool hot_known = false;
+    // parameter sweeps: events per trajectory of each point, from an earlier run of
+    // the same sweep (keyed by its points, sizes and horizon), used to hand out the
+    // costliest points first
+    mutable std::map<std::string, std::vector<double>> sweep_cost;
 };
 
 struct PoolLayout;
@@ -1126,6 +1130,8 @@ struct SweepSpec {
     ssa_u64 N = 0;
     PoolLayout L;
     std::vector<RangeOut> roots;   // per point
+    std::vector<double> cost;      // per point: events per trajectory of an earlier run (empty: unknown)
+    mutable std::vector<ssa_u64> events;   // out: applied events per point in this run
 };
 
 // Event recording (union-time selective memory): every applied event is
@@ -1272,7 +1278,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     }
 
     // buffers
-    DevBuf staging, tiles, croots, statsb, work, dids, dstates, de, dt_, dsum, pconst;
+    DevBuf staging, tiles, croots, statsb, work, dids, dstates, de, dt_, dsum, pconst, ptev, ptord;
     const ssa_u64 stride = sw ? (C + 3) / 4 * 4 : C;     // rows 16-byte aligned for the vector loads of K3
     CU(staging.alloc(sizeof(int) * stride * cells, st));
     const ssa_u64 seg = sw ? sw->N : C;                   // ids per reduced segment (a point, or the chunk)
@@ -1284,6 +1290,27 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         CU(cudaMemcpyAsync(pconst.p, sw->L.values.data(), sizeof(double) * sw->L.values.size(),
                            cudaMemcpyHostToDevice, st));
         info.h2d += sizeof(double) * sw->L.values.size();
+        CU(ptev.alloc(sizeof(ssa_u64) * (size_t)sw->P, st));
+        CU(cudaMemsetAsync(ptev.p, 0, sizeof(ssa_u64) * (size_t)sw->P, st));
+        if ((int)sw->cost.size() == sw->P) {
+            // longest-processing-time order within each chunk: the costliest points' trajectories
+            // are handed out first, so the end of the launch is not one long trajectory started late
+            const ssa_u64 ppc = C / sw->N;   // points per chunk
+            std::vector<int> ord((size_t)sw->P);
+            for (ssa_u64 p0 = 0; p0 < (ssa_u64)sw->P; p0 += ppc) {
+                const ssa_u64 p1 = std::min<ssa_u64>((ssa_u64)sw->P, p0 + ppc);
+                std::vector<int> loc;
+                for (ssa_u64 q = p0; q < p1; ++q) loc.push_back((int)(q - p0));
+                std::stable_sort(loc.begin(), loc.end(), [&](int a, int b) {
+                    return sw->cost[(size_t)(p0 + a)] > sw->cost[(size_t)(p0 + b)];
+                });
+                for (size_t q = 0; q < loc.size(); ++q) ord[(size_t)(p0 + q)] = loc[q];
+            }
+            CU(ptord.alloc(sizeof(int) * ord.size(), st));
+            CU(cudaMemcpyAsync(ptord.p, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice, st));
+            CU(cudaStreamSynchronize(st));   // ord is a local
+            info.h2d += sizeof(int) * ord.size();
+        }
     }
     CU(statsb.alloc(sizeof(ssa_dev_stats), st));
     CU(work.alloc(sizeof(ssa_u64) * n_chunks, st));
@@ -1350,6 +1377,8 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
                 p.n_pool = sw->L.n;
                 p.pconst = pconst.as<double>() + (cb / sw->N) * (ssa_u64)sw->L.n;
                 smem = sizeof(double) * (size_t)p.n_pts * (size_t)p.n_pool;
+                p.pt_events = ptev.as<ssa_u64>() + cb / sw->N;
+                p.pt_order = ptord.p ? (const int*)ptord.p + cb / sw->N : nullptr;
             }
             p.spread = spread ? 1 : 0;
             p.prof = prof;
@@ -1442,6 +1471,10 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
     info.device_ms = ms;
     info.ssa_ms = ssa_ms_total;
     info.reduce_ms = reduce_ms_total;
+    if (sw) {
+        sw->events.assign((size_t)sw->P, 0);
+        CU(cudaMemcpy(sw->events.data(), ptev.p, sizeof(ssa_u64) * (size_t)sw->P, cudaMemcpyDeviceToHost));
+    }
     if (prof) {
         // choose the hot set from the sampled propensity shares (their mean estimates each
         // reaction's share of the events): the top reaction if it carries >= 1/2 of them,
@@ -1604,6 +1637,19 @@ extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const 
     sw.P = n_points;
     sw.N = n_per_point;
     sw.L = make_pool(*m, n_points, rates, mod_coefs);
+    std::string skey;   // this sweep's identity for the point-cost cache
+    {
+        auto put = [&](const void* q, size_t n) { skey.append((const char*)q, n); };
+        put(&n_points, sizeof n_points);
+        put(&n_per_point, sizeof n_per_point);
+        put(&t_end, sizeof t_end);
+        put(&sample_dt, sizeof sample_dt);
+        put(rates, sizeof(double) * (size_t)n_points * R);
+        if (mod_coefs) put(mod_coefs, sizeof(double) * (size_t)n_points * R);
+        std::lock_guard<std::mutex> lk(m->mu);
+        auto it = m->sweep_cost.find(skey);
+        if (it != m->sweep_cost.end()) sw.cost = it->second;
+    }
     DevBuf rootb;
     CU(rootb.alloc(sizeof(double) * 3 * cells * (size_t)n_points, c.st));
     double* rb = rootb.as<double>();
@@ -1617,6 +1663,13 @@ extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const 
     ro.path = SSA_PATH_THREAD;   // AUTO included: sweeps run on the thread path at any size
     TRY(run_range(m, 0, (ssa_u64)n_points * n_per_point, t_end, sample_dt, seed, &ro, c, sw.roots[0], info,
                   o ? o->dump : nullptr, on_dev, &sw));
+    if ((int)sw.events.size() == n_points) {
+        std::vector<double> cost((size_t)n_points);
+        for (int q = 0; q < n_points; ++q) cost[(size_t)q] = (double)sw.events[(size_t)q] / (double)n_per_point;
+        std::lock_guard<std::mutex> lk(m->mu);
+        if (m->sweep_cost.size() >= 64) m->sweep_cost.clear();   // bound the cache
+        m->sweep_cost[skey] = cost;
+    }
     ssa_status st = fill_result(info, r);
     // finalize every point into its [G*S] slab of the caller's arrays
     for (int p = 0; p < n_points; ++p) {

@@ -122,3 +122,21 @@ def test_sweep_large_network_auto_runs_thread_path(S):
     for p in range(2):
         one = S.run(S.Model(inputs.with_rates(net, rates[p])), N, t_end, dt, seed, path=1)
         assert np.array_equal(sw.mean[p], one.mean) and np.array_equal(sw.var[p], one.var)
+
+
+def test_sweep_rerun_costliest_first_is_bitwise(S):
+    """The first run of a sweep records each point's events per trajectory; a re-run hands out the
+    costliest point's trajectories first.  Scheduling never changes results: grids, counters and
+    dumps are bitwise those of the first run."""
+    net = inputs.immigration_death()
+    rates = inputs.rate_matrix(net, [0], [2.0, 40.0, 10.0])     # immigration 2 / 40 / 10: unequal costs
+    N, t_end, dt, seed = 3000, 20.0, 0.5, 13
+    ids = np.array([0, 1, 2999, 3000, 4500, 8999], dtype=np.uint64)
+    m = S.Model(net)
+    a = S.run_sweep(m, rates, N, t_end, dt, seed, dump_ids=ids)
+    b = S.run_sweep(m, rates, N, t_end, dt, seed, dump_ids=ids)
+    assert a.events == b.events
+    assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var)
+    for f in ("states", "events_at", "time_at"):
+        assert np.array_equal(getattr(a.dump, f), getattr(b.dump, f)), f
+    assert a.dump.summary.tobytes() == b.dump.summary.tobytes()
