@@ -180,15 +180,34 @@ def _oracle_worker(args):
     return int(r.summaries["events"].sum()), len(ids)
 
 
+def sample_ids(cfg_index: int, n_traj: int):
+    """The CPU sample: n_traj ids drawn uniformly from the config's whole id range
+    (inputs.dump_ids' generator), so early die-outs appear at their ensemble rate."""
+    import inputs
+    cfg = inputs.config(cfg_index)
+    return [int(v) for v in inputs.dump_ids(cfg.n_trajectories, n_traj, cfg.seed + 0xC0)]
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(cfg_index: int, n_traj: int, cores: int, t_end=None):
-    """Time the unmodified CPU oracle on `n_traj` trajectories of the config,
-    spread over `cores` worker processes.  Returns (events, trajectories, seconds)."""
+    """Time the unmodified CPU oracle on `n_traj` trajectories of the config
+    (sample_ids), spread over `cores` worker processes.  Returns (events,
+    trajectories, seconds)."""
     import multiprocessing as mp
 
     import inputs
     cfg = inputs.config(cfg_index)
     t_end = t_end or cfg.t_end
-    ids = list(range(n_traj))
+    ids = sample_ids(cfg_index, n_traj)
     parts = [ids[i::cores] for i in range(cores) if ids[i::cores]]
     t0 = time.perf_counter()
     with mp.get_context("fork").Pool(len(parts)) as pool:
@@ -214,7 +233,7 @@ def run_reference(args, rank, world):
     O.build()
     cfg = inputs.config(args.config)
     cores = host_cores()
-    per_step = max(cores, 8)      # one ~1 s HIV trajectory per core per step
+    per_step = 3 * max(cores, 8)  # three ~0.4 s HIV trajectories per core per step (~15-20 s of CPU work)
     for _ in range(args.warmup):
         oracle_sample(args.config, per_step, cores)
     ev = tr = 0
@@ -231,8 +250,9 @@ def run_reference(args, rank, world):
                    "seed": cfg.seed, "trajectories_per_step": per_step, "parallelism": "cpu-processes"},
         "trajectories_per_s": tr / secs,
         "cpu_baseline": {"value": value, "unit": "events/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{per_step} full {cfg.name} trajectories per step (ids 0..{per_step - 1}) "
-                                   f"over {cores} processes"},
+                         "cpu_model": cpu_model(),
+                         "sample": f"{per_step} full {cfg.name} trajectories per step (ids drawn uniformly from "
+                                   f"the {cfg.n_trajectories}-id ensemble) over {cores} processes"},
         "e2e": {"value": value, "unit": "events/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -542,20 +562,21 @@ def main():
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
-            res = step()
-            if res is not None:
-                events += res.events
-                ssa_ms.append(res.ssa_ms)
-                red_ms.append(res.reduce_ms)
-                red_bytes = res.reduce_bytes
-                launches += res.kernel_launches
+            res = step()                       # job-wide StepResult, the same on every rank
+            events += res.events
+            loc = res.local                    # this rank's ssa_run_shard result
+            if loc is not None:
+                ssa_ms.append(loc.ssa_ms)
+                red_ms.append(loc.reduce_ms)
+                red_bytes = loc.reduce_bytes
+                launches += loc.kernel_launches
             launches += 2      # merge + finalize of ssa_merge_roots
         ev1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    ms, events, launches = D.max_and_sum([ms, events, launches], dev)   # max-over-ranks time, summed counters
+    ms, launches = D.max_and_sum([ms, launches], dev)   # max-over-ranks time, launches summed over ranks
     events, launches = int(events), int(launches)
     value = events / (ms / 1e3)
     traj_per_s = n_total * args.steps / (ms / 1e3)
@@ -563,7 +584,7 @@ def main():
     # end to end through the public API with host buffers (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
-        e2e_steps = max(1, min(args.steps, 2))
+        e2e_steps = args.steps                 # the same number of steps as `value`
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -577,13 +598,13 @@ def main():
                 h2d, d2h = r.h2d_bytes, r.d2h_bytes
             else:
                 res = step()
-                e2e_events += res.events if res else 0
+                e2e_events += res.events               # job-wide
                 merged = ens.out.cpu()                 # D2H of this step's mean/var/M2/n grids
-                h2d = res.h2d_bytes if res else 0
+                h2d = res.local.h2d_bytes if res.local is not None else 0
                 d2h = merged.numel() * merged.element_size()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        wall, e2e_events = D.max_and_sum([wall, e2e_events], dev)
+        wall, _ = D.max_and_sum([wall, 0], dev)
         e2e = {"value": e2e_events / wall, "unit": "events/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                "note": "ssa_run with host result buffers; wall clock incl. per-run model upload and D2H"}
@@ -641,11 +662,12 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         cores = host_cores()
-        n_cpu = max(cores, 8)
+        n_cpu = 3 * max(cores, 8)
         ce, ct, cs = oracle_sample(args.config, n_cpu, cores, t_end)
-        cpu = {"value": ce / cs, "unit": "events/s", "cores": cores, "kind": "oracle",
-               "sample": f"{n_cpu} full trajectories (ids 0..{n_cpu - 1}) of {cfg.name} over {cores} processes, "
-                         f"{cs:.1f} s wall", "trajectories_per_s": ct / cs}
+        cpu = {"value": ce / cs, "unit": "events/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+               "sample": f"{n_cpu} full trajectories of {cfg.name} (ids drawn uniformly from the "
+                         f"{cfg.n_trajectories}-id ensemble) over {cores} processes, {cs:.1f} s wall",
+               "trajectories_per_s": ct / cs}
 
     line = {
         "metric": "ssa_events_per_s", "value": value, "unit": "events/s", "n_gpus": world, "steps": args.steps,

@@ -201,16 +201,24 @@ typedef struct {
  * any trajectory is reproducible in isolation.  reducers: SSA_REDUCE_MEAN |
  * SSA_REDUCE_VAR (both are always computed; the flags only gate the copies).
  * Returns the first error by trajectory id: SSA_ERR_NUMERIC/OVERFLOW (detail
- * in result->first_error_*), or an argument/CUDA/JIT error. */
+ * in result->first_error_*), or an argument/CUDA/JIT error.  When any
+ * trajectory ends in SSA_ERR_NUMERIC/OVERFLOW the whole ensemble has no
+ * defined moments: mean, var and m2 are written as NaN (count is still
+ * written, the counters and the dump are valid). */
 ssa_status ssa_run(const ssa_model* model, uint64_t n_trajectories, double t_end, double sample_dt,
                    uint64_t seed, uint32_t reducers, const ssa_run_options* opts, ssa_result* result);
 
-/* Multi-process form (one process per GPU): simulate ids [id_begin, id_end)
- * and write their subtree root of the canonical reduction tree to d_root
- * (DEVICE memory, [3][G*S] doubles: n, mean, M2).  (id_end - id_begin) must
- * be >= 1 and id_begin a multiple of the next power of two >= (id_end -
- * id_begin), so the shard is an aligned subtree (R26).  result's
- * output arrays are ignored; its counters are filled. */
+/* Multi-process form (one process per GPU; the workers of the paper's
+ * two-level "systolic" reduction, §3.2 -- each reduces its
+ * own simulations before the collector merges the partials): simulate ids
+ * [id_begin, id_end) and write their subtree root of the canonical reduction
+ * tree to d_root (DEVICE memory, caller-owned, [3][G*S] doubles: n, mean,
+ * M2).  (id_end - id_begin) must be >= 1 and id_begin a multiple of the next
+ * power of two >= (id_end - id_begin), so the shard is an aligned subtree
+ * (R26).  result's output arrays are ignored; its counters are
+ * filled (this shard's only: the caller exchanges them, paper_1007_1768_b200/
+ * dist.py).  Errors as ssa_run; on SSA_ERR_NUMERIC/OVERFLOW the root's mean
+ * and M2 rows are NaN, so any merge that includes it is NaN. */
 ssa_status ssa_run_shard(const ssa_model* model, uint64_t id_begin, uint64_t id_end, double t_end,
                          double sample_dt, uint64_t seed, double* d_root, const ssa_run_options* opts,
                          ssa_result* result);
@@ -272,11 +280,16 @@ ssa_status ssa_run_trajectories(const ssa_model* model, uint64_t n_trajectories,
                                 int32_t* states, uint64_t* n_points, const ssa_run_options* opts,
                                 ssa_result* result);
 
-/* Merge n_roots shard roots (DEVICE memory, contiguous [n_roots][3][cells],
- * in rank order, each an aligned subtree of equal span) as the top levels of
- * the canonical tree, then finalize into result->mean/var/m2/count (host or
- * device per opts->outputs_on_device).  Every rank obtains bitwise identical
- * output. */
+/* The collector of the paper's two-level reduction (§3.2: "a
+ * systolic reduction of partial results"), made deterministic: merge n_roots
+ * shard roots (DEVICE memory, contiguous [n_roots][3][cells], in rank order,
+ * each an aligned subtree of equal span) as the top levels of the canonical
+ * tree, then finalize into result->mean/var/m2/count (host or device per
+ * opts->outputs_on_device).  Every rank obtains bitwise identical output.
+ * Reads d_roots only during the call, on opts->stream (NULL: a library
+ * stream, synchronised with the device before reading -- pass the stream the
+ * all-gather was ordered on).  Errors: SSA_ERR_INVALID_ARG (null pointer,
+ * n_roots < 1, cells == 0), SSA_ERR_CUDA. */
 ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, uint64_t cells, const ssa_run_options* opts,
                            ssa_result* result);
 

@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <map>
 #include <tuple>
 #include <memory>
@@ -601,8 +602,8 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
             o << "  bool hot = false;\n";
             for (int hj : hot) {
                 o << "  if (j == " << hj << ") { hot = true;";
-                for (auto& d : m.rx[hj].nu)
-                    o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << (double)d.second << ");";
+                for (auto& d : m.rx[hj].nu)   // exact integer literal (as the switch path)
+                    o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
                 o << " }\n";
             }
             o << "  if (!hot) {\n";
@@ -637,7 +638,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
                         o << " out[" << q << "] = (int)x[" << m.rx[hj].nu[q].first << "];";
                     o << " }";
                     for (auto& d : m.rx[hj].nu)
-                        o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << (double)d.second << ");";
+                        o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
                     o << " }\n";
                 }
                 o << "  if (!hot) {\n";
@@ -1096,6 +1097,7 @@ struct RunInfo {
     double device_ms = 0, ssa_ms = 0, jit_ms = 0, reduce_ms = 0, dump_ms = 0;
     uint64_t h2d = 0, d2h = 0, reduce_bytes = 0, dump_bytes = 0;
     int launches = 0;
+    uint64_t lanes = 0;   // SSA lanes launched (K1 threads that take trajectories)
 };
 
 // Reduce `count` elements per row from `in` down to one, writing the final
@@ -1385,6 +1387,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             void* args[] = {&p};
             CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(spread ? 32 : block), args, smem, st));
             info.launches += 1;
+            info.lanes = std::max<uint64_t>(info.lanes, (uint64_t)grid * (spread ? 1 : block));
         } else {
             ssa_k2_params p{};
             p.n_ent = k2->n_ent; p.n_dep = k2->n_dep;
@@ -1422,7 +1425,11 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
                 double* b = tiles.as<double>();
                 ssa_tree_out to{b, b + cells * n_tiles, b + 2 * cells * n_tiles, n_tiles, 1, 0};
                 CU(ssa_tree_leaf_launch(src, stride, sn, cells, to, st, &info.launches));
-                TRY(reduce_partials(ssa_tree_in{to.n, to.mean, to.m2, n_tiles, 1}, n_tiles, cells, seg_out, st,
+                // only the tiles holding this segment's ids were written (a ragged chunk
+                // has fewer than n_tiles): the merge treats positions >= count as empty
+                // leaves, the identity, so the tree keeps its shape and its bits
+                const ssa_u64 written = (sn + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
+                TRY(reduce_partials(ssa_tree_in{to.n, to.mean, to.m2, n_tiles, 1}, written, cells, seg_out, st,
                                     &info.launches));
             } else {
                 CU(ssa_tree_leaf_launch(src, stride, sn, cells, seg_out, st, &info.launches));
@@ -1545,8 +1552,11 @@ static ssa_status check_common(const ssa_model* m, double t_end, double dt, ssa_
     return SSA_OK;
 }
 
+// poisoned: the run had trajectories that ended in an error (their grid rows past
+// the error are not samples of the method), so mean, var and M2 are NaN; count
+// is still written
 static ssa_status finalize_to(const double* rn, const double* rmean, const double* rm2, ssa_u64 cells, uint32_t reducers,
-                              ssa_result* r, bool on_device, cudaStream_t st)
+                              ssa_result* r, bool on_device, cudaStream_t st, bool poisoned = false)
 {
     double* om = (reducers & SSA_REDUCE_MEAN) ? r->mean : nullptr;
     double* ov = (reducers & SSA_REDUCE_VAR) ? r->var : nullptr;
@@ -1555,6 +1565,9 @@ static ssa_status finalize_to(const double* rn, const double* rmean, const doubl
     r->kernel_launches += 1;
     if (on_device) {
         CU(ssa_finalize_launch(rn, rmean, rm2, cells, om, ov, o2, oc, st));
+        if (poisoned)   // all-ones bytes are a quiet NaN
+            for (double* q : {om, ov, o2})
+                if (q) CU(cudaMemsetAsync(q, 0xFF, sizeof(double) * cells, st));
         CU(cudaStreamSynchronize(st));
         return SSA_OK;
     }
@@ -1568,6 +1581,9 @@ static ssa_status finalize_to(const double* rn, const double* rmean, const doubl
     if (o2) CU(cudaMemcpyAsync(o2, d + 2 * cells, sizeof(double) * cells, cudaMemcpyDeviceToHost, st));
     if (oc) CU(cudaMemcpyAsync(oc, d + 3 * cells, sizeof(double) * cells, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (poisoned)
+        for (double* q : {om, ov, o2})
+            if (q) std::fill(q, q + cells, std::numeric_limits<double>::quiet_NaN());
     return SSA_OK;
 }
 
@@ -1589,7 +1605,7 @@ extern "C" ssa_status ssa_run(const ssa_model* m, uint64_t n_trajectories, doubl
                   o ? o->dump : nullptr, on_dev));
     ssa_status st = fill_result(info, r);
     TRY(finalize_to(rb, rb + cells, rb + 2 * cells, cells, reducers ? reducers : (SSA_REDUCE_MEAN | SSA_REDUCE_VAR), r,
-                    on_dev, c.st));
+                    on_dev, c.st, info.stats.n_errors > 0));
     return st;
 }
 
@@ -1609,6 +1625,12 @@ extern "C" ssa_status ssa_run_shard(const ssa_model* m, uint64_t id_begin, uint6
     RunInfo info;
     TRY(run_range(m, id_begin, id_end, t_end, sample_dt, seed, o, c, RangeOut{d_root, d_root + cells, d_root + 2 * cells},
                   info, o ? o->dump : nullptr, o && o->outputs_on_device));
+    if (info.stats.n_errors > 0) {
+        // a shard with erroring trajectories has no defined moments: NaN mean and M2
+        // (n kept), so every merge that includes this root is NaN as well
+        CU(cudaMemsetAsync(d_root + cells, 0xFF, sizeof(double) * 2 * cells, c.st));
+        CU(cudaStreamSynchronize(c.st));
+    }
     return fill_result(info, r);
 }
 
@@ -1683,7 +1705,7 @@ extern "C" ssa_status ssa_run_sweep(const ssa_model* m, int32_t n_points, const 
         rp.d2h_bytes = 0;
         const RangeOut& pr = sw.roots[p];
         TRY(finalize_to(pr.n, pr.mean, pr.m2, cells, reducers ? reducers : (SSA_REDUCE_MEAN | SSA_REDUCE_VAR), &rp,
-                        on_dev, c.st));
+                        on_dev, c.st, info.stats.n_errors > 0));
         r->kernel_launches += rp.kernel_launches;
         r->d2h_bytes += rp.d2h_bytes;
     }
@@ -1744,8 +1766,14 @@ extern "C" ssa_status ssa_run_union(const ssa_model* m, uint64_t n_trajectories,
             if (attempt == 1) info = info1;
             break;
         }
-        cap = rows;   // rare: the reserved size for the second run
+        // rare: size the second run.  Which trajectories a lane gets depends on the
+        // schedule, so its reserved rows can differ from this run's; each lane leaves
+        // at most one partly used block, so rows + lanes * block bounds any run.
+        cap = rows + ri.lanes * 256ull;
     }
+    if (rows > cap)
+        return fail(SSA_ERR_OOM, "event record overflow (%llu rows reserved, capacity %llu)", (unsigned long long)rows,
+                    (unsigned long long)cap);
     E = info.stats.events;   // valid rows: the first E after sorting by time (unused rows are +inf)
     // model tables for the reduction: changed species and net changes, ensemble sums of x0, x0^2
     const int R1 = std::max(m->R, 1);
@@ -1868,8 +1896,11 @@ extern "C" ssa_status ssa_run_trajectories(const ssa_model* m, uint64_t n_trajec
             if (attempt == 1) info = info1;
             break;
         }
-        cap = rows;
+        cap = rows + ri.lanes * 32ull;   // as ssa_run_union: any schedule fits (blocks of 32 points)
     }
+    if (rows > cap)
+        return fail(SSA_ERR_OOM, "point record overflow (%llu rows reserved, capacity %llu)", (unsigned long long)rows,
+                    (unsigned long long)cap);
     const bool on_dev = o && o->outputs_on_device;
     DevBuf dout;
     unsigned* ot = nullptr;
@@ -1927,6 +1958,8 @@ extern "C" ssa_status ssa_merge_roots(const double* d_roots, int32_t n_roots, ui
     if (!d_roots || n_roots < 1 || cells == 0 || !r) return fail(SSA_ERR_INVALID_ARG, "bad merge arguments");
     Ctx c;
     TRY(setup_ctx(o, c));
+    // a library stream is not ordered after the caller's all-gather: wait for the device first
+    if (c.own_stream) CU(cudaDeviceSynchronize());
     DevBuf rootb;
     CU(rootb.alloc(sizeof(double) * 3 * cells, c.st));
     double* rb = rootb.as<double>();

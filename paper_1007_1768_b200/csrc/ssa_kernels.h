@@ -1,4 +1,4 @@
-// ssa_kernels.h -- internal interface between the runtime (ssa_api.cpp) and
+// ssa_kernels.h -- internal interface between the runtime (runtime.cu) and
 // the nvcc-compiled kernels (kernels.cu).  Not part of the public C ABI.
 #pragma once
 #include <cuda_runtime.h>

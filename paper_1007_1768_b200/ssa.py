@@ -454,8 +454,11 @@ def run_device(model: Model, n_trajectories: int, t_end: float, sample_dt: float
 
 
 def run_shard(model: Model, id_begin: int, id_end: int, t_end: float, sample_dt: float, seed: int, d_root, *,
-              path: int = SSA_PATH_AUTO, stream=None, dump_ids=None, **opts) -> RunResult:
-    """ssa_run_shard: d_root is a torch CUDA float64 tensor [3, G*S] (n, mean, M2)."""
+              path: int = SSA_PATH_AUTO, stream=None, dump_ids=None, raise_on_error: bool = True,
+              **opts) -> RunResult:
+    """ssa_run_shard: d_root is a torch CUDA float64 tensor [3, G*S] (n, mean, M2).  With
+    raise_on_error=False a trajectory error (SSA_ERR_NUMERIC / OVERFLOW) is returned in
+    .status instead of raised (the root's mean and M2 are then NaN)."""
     G = grid_size(t_end, sample_dt)
     dump = cdump = None
     if dump_ids is not None and len(dump_ids):
@@ -464,7 +467,8 @@ def run_shard(model: Model, id_begin: int, id_end: int, t_end: float, sample_dt:
     r = ssa_result()
     st = lib().ssa_run_shard(model.handle, id_begin, id_end, t_end, sample_dt, seed, C.c_void_p(d_root.data_ptr()),
                              C.byref(o), C.byref(r))
-    _check(st)
+    if st != SSA_OK and (raise_on_error or st not in (3, 4)):
+        _check(st)
     return _result_from(r, st, None, None, None, None, dump)
 
 

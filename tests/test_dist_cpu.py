@@ -62,7 +62,9 @@ def _worker(rank, world, port, outdir):
         G = int(np.floor(T_END / DT + 1e-9)) + 1
         ens = D.ShardedEnsemble(N_TOTAL, G * 1, torch.device("cpu"), _shard_sums, _sum_merge)
         res = ens.step()
-        t_ms, events = D.max_and_sum([10.0 * (rank + 1), res["events"] if res else 0], torch.device("cpu"))
+        t_ms, events = D.max_and_sum([10.0 * (rank + 1), res.local["events"] if res.local else 0],
+                                     torch.device("cpu"))
+        assert res.events == events and res.status == 0 and res.n_errors == 0
         np.savez(os.path.join(outdir, f"rank{rank}.npz"), roots=ens.roots.numpy(), out=ens.out.numpy(),
                  bounds=np.array([ens.begin, ens.end]), t_ms=t_ms, events=events)
     finally:
@@ -106,3 +108,94 @@ def test_shard_bounds_rejects_bad_world():
         D.shard_bounds(100, 3, 0)
     with pytest.raises(ValueError):
         D.shard_bounds(100, 4, 4)
+
+
+# ------------------------------------------------------------ fail-safe exchange
+def _fail_worker(rank, world, port, outdir):
+    """Rank 1's shard fails outright (a library error raised before any
+    collective) and rank 2's shard reports trajectory errors; every rank must
+    still reach the root all-gather and raise the same error afterwards."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    from paper_1007_1768_b200 import dist as D
+    from paper_1007_1768_b200.ssa import SSAError
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        def run_shard(b, e, root):
+            root[0] = float(e - b)
+            root[1:] = 1.0
+            if rank == 1:
+                raise SSAError(6, "injected CUDA failure")
+            n_err = 5 if rank == 2 else 0
+            return {"events": 100 + rank, "near_ties": rank, "n_errors": n_err, "status": 3 if n_err else 0,
+                    "first_error_id": b + 7 if n_err else 0, "first_error_reaction": 4 if n_err else -1}
+
+        ens = D.ShardedEnsemble(64, 3, torch.device("cpu"), run_shard, _sum_merge)
+        try:
+            ens.step()
+            raised = None
+        except SSAError as ex:
+            raised = (ex.status, str(ex))
+        res = ens.last
+        np.savez(os.path.join(outdir, f"rank{rank}.npz"), raised=np.array(raised is not None),
+                 status=raised[0] if raised else 0, msg=raised[1] if raised else "",
+                 word=np.array([res.status, res.events, res.near_ties, res.n_errors, res.first_error_id,
+                                res.first_error_reaction, res.error_rank]), out=ens.out.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_error_on_one_rank_reaches_every_rank(tmp_path):
+    world = 4
+    tmp.start_processes(_fail_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="fork")
+    outs = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
+    w0 = outs[0]["word"]
+    for o in outs:
+        assert bool(o["raised"]) and int(o["status"]) == 6          # the non-trajectory failure wins
+        assert np.array_equal(o["word"], w0)                      # identical job-wide result on every rank
+    # events/ties summed over the ranks that ran; the trajectory errors of rank 2 are still counted
+    assert list(w0[:4]) == [6, 100 + 0 + 102 + 103, 0 + 2 + 3, 5]
+    assert int(w0[4]) == 32 + 7 and int(w0[5]) == 4 and int(w0[6]) == 1
+    # the failed rank's root is NaN (n = 0), so the merged moments are NaN everywhere
+    assert np.all(np.isnan(outs[0]["out"][1]))
+
+
+def _dump_worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    from paper_1007_1768_b200 import dist as D
+    from paper_1007_1768_b200.ssa import SUMMARY_DTYPE, Dump
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        G, S = 5, 3
+        n = [3, 0, 1, 4][rank]            # uneven, one rank with nothing dumped
+        d = None
+        if n:
+            ids = np.arange(n, dtype=np.uint64) + 100 * rank
+            st = (ids[:, None, None] * 1000 + np.arange(G * S).reshape(1, G, S)).astype(np.int32)
+            ev = (ids[:, None] + np.arange(G)).astype(np.uint64)
+            tm = ev.astype(np.float64) * 0.5
+            sm = np.zeros(n, SUMMARY_DTYPE)
+            sm["events"] = ids * 3
+            sm["hash"] = ids ^ 0xABCDEF
+            d = Dump(ids, st, ev, tm, sm)
+        for dst in (0, None):
+            g = D.gather_dump(d, torch.device("cpu"), dst=dst)
+            if g is not None:
+                np.savez(os.path.join(outdir, f"rank{rank}_{dst}.npz"), ids=g.ids, states=g.states,
+                         events_at=g.events_at, time_at=g.time_at, ev=g.summary["events"], hash=g.summary["hash"])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_dump_rank_order(tmp_path):
+    world = 4
+    tmp.start_processes(_dump_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="fork")
+    ids = np.concatenate([np.arange(n, dtype=np.uint64) + 100 * r for r, n in enumerate([3, 0, 1, 4])])
+    files = sorted(os.listdir(tmp_path))
+    assert files == ["rank0_0.npz", "rank0_None.npz", "rank1_None.npz", "rank2_None.npz", "rank3_None.npz"]
+    for f in files:
+        g = np.load(tmp_path / f)
+        assert np.array_equal(g["ids"], ids)
+        assert np.array_equal(g["states"][:, 2, 1], (ids * 1000 + 7).astype(np.int32))
+        assert np.array_equal(g["events_at"][:, 4], ids + 4)
+        assert np.array_equal(g["time_at"], g["events_at"].astype(np.float64) * 0.5)
+        assert np.array_equal(g["ev"], ids * 3) and np.array_equal(g["hash"], ids ^ 0xABCDEF)

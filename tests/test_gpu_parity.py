@@ -206,6 +206,29 @@ def test_chunk_block_and_schedule_invariance(S):
             assert np.array_equal(a.mean, b.mean) and np.array_equal(a.var, b.var), (path, opts)
 
 
+@pytest.mark.parametrize("path", [THREAD, HALF])
+def test_ragged_chunks_reduce_only_written_tiles(S, path):
+    """A ragged chunk holds fewer reduction tiles than the chunk span: 5000 ids
+    in chunks of 4096 (the last chunk has 904 ids, one tile of its two), and
+    5000 ids in one 8192 chunk (3 tiles of 4), each run right after a larger
+    run that leaves other data in the pooled buffers.  Counts, moments and M2
+    must be those of the exact sums over the 5000 trajectories."""
+    cfg = inputs.config(1)
+    m = S.Model(cfg.network)
+    n = 5000
+    ids = np.arange(n, dtype=np.uint64)
+    ref = None
+    for big, opts in ((8192, dict(chunk=4096)), (8192, dict()), (16384, dict(chunk=8192))):
+        S.run(m, big, cfg.t_end, cfg.dt, cfg.seed + 1, path=path, **opts)    # dirty the pool
+        r = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=path, dump_ids=ids, **opts)
+        assert np.all(r.count == n), opts
+        if ref is None:
+            ref = exact_moments(r.dump.states)
+            first = r
+        assert_moments_close(r.mean, r.var, *ref)
+        assert np.array_equal(r.mean, first.mean) and np.array_equal(r.m2, first.m2), opts
+
+
 def test_reduction_paths_bitwise_equal(S):
     """K3's full-tile kernel takes an integer fast path for 8-leaf groups below
     2^20 and the fp64 Chan merges otherwise; both must give the canonical

@@ -283,44 +283,149 @@ def test_hiv_variant_b_structure(oracle_lib):
         assert bool(np.any(gx[:, :, 7] > 0)) == expect_v4
 
 
+def _linear_moments(net, times):
+    """Exact mean and covariance of a network whose propensities are affine in
+    the counts (zero- and first-order reactions, coefficient 1), written from
+    the reaction list alone: with a_j(x) = c_j + w_j.x and net change nu_j,
+      m'     = J m + nu c,                     J = sum_j nu_j w_j^T
+      Sigma' = J Sigma + Sigma J^T + sum_j nu_j nu_j^T (c_j + w_j.m)
+    (the moment equations of a linear network close exactly).  Solved as one
+    linear system z' = M z on z = [m, vec(Sigma), 1] with expm(M t) from
+    m = x0, Sigma = 0.  Returns [(mean[S], var[S])] per time."""
+    S, R = net.S, net.R
+    nu = np.zeros((S, R)); c = np.zeros(R); W = np.zeros((R, S))
+    for j, rx in enumerate(net.reactions):
+        if rx.rate == 0.0 and rx.modifier_coef == 0.0:
+            continue                                    # a switched-off reaction never fires
+        assert rx.modifier_species < 0 and rx.mass_action and not rx.gates
+        assert len(rx.reactants) <= 1 and all(mm == 1 for _, mm in rx.reactants), "not first order"
+        if rx.reactants:
+            W[j, rx.reactants[0][0]] = rx.rate
+        else:
+            c[j] = rx.rate
+        for sp, mm in rx.reactants:
+            nu[sp, j] -= mm
+        for sp, mm in rx.products:
+            nu[sp, j] += mm
+    J = nu @ W
+    n = S + S * S + 1
+    M = np.zeros((n, n))
+    M[:S, :S] = J
+    M[:S, -1] = nu @ c
+    I = np.eye(S)
+    M[S:S + S * S, S:S + S * S] = np.kron(I, J) + np.kron(J, I)
+    for j in range(R):
+        v = np.outer(nu[:, j], nu[:, j]).reshape(-1)
+        M[S:S + S * S, -1] += v * c[j]
+        M[S:S + S * S, :S] += np.outer(v, W[j])
+    z0 = np.zeros(n)
+    z0[:S] = net.x0
+    z0[-1] = 1.0
+    out = []
+    for t in times:
+        z = scipy.linalg.expm(M * t) @ z0
+        out.append((z[:S], np.diag(z[S:S + S * S].reshape(S, S)).copy()))
+    return out
+
+
+def _check_linear(O, net, n, t_end, dt, seed, must_move):
+    """z < 4 for every species' mean at every grid point, against the closed
+    form's own variance (SE = sqrt(Var/n)); constants must be exact.  The
+    sample variance is checked against the closed form with the standard error
+    of a variance estimate, sqrt((m4 - s^4)/n), m4 from the sample."""
+    res = O.run(O.OracleModel(net), np.arange(n), seed, t_end, dt)
+    assert res.status == 0
+    G = O.grid_size(t_end, dt)
+    ref = _linear_moments(net, [k * dt for k in range(G)])
+    x = res.grid_x.astype(np.float64)
+    for k, (mu, var) in enumerate(ref):
+        for s in range(net.S):
+            assert _zmean(res.mean[k, s], mu[s], var[s], n) < Z, (k, s, res.mean[k, s], mu[s])
+            if var[s] * n > 20:      # enough spread for the normal approximation of the estimator
+                m4 = np.mean((x[:, k, s] - x[:, k, s].mean()) ** 4)
+                assert _zvar(res.var[k, s], var[s], m4, n) < Z, (k, s, res.var[k, s], var[s])
+            elif var[s] < 1e-12:
+                assert res.var[k, s] == 0.0, (k, s)
+    for s in must_move:   # the pin has power: the species actually changes
+        assert abs(ref[-1][0][s] - net.x0[s]) > 10 * math.sqrt(max(ref[-1][1][s], 0.0) / n) + 1e-3, s
+    return res, ref
+
+
+def test_linear_moments_closed_form_self_check():
+    """The helper itself against textbook cases: immigration-death is Poisson
+    (mean = var = k1/k2 (1 - e^{-k2 t})); pure death is Binomial."""
+    ref = _linear_moments(inputs.immigration_death(10.0, 0.1, 0), [0.0, 5.0, 50.0])
+    for t, (m, v) in zip([0.0, 5.0, 50.0], ref):
+        lam = 100.0 * (1 - math.exp(-0.1 * t))
+        assert abs(m[0] - lam) < 1e-9 and abs(v[0] - lam) < 1e-9
+    ref = _linear_moments(inputs.pure_death(0.7, 12), [1.3])
+    p = math.exp(-0.7 * 1.3)
+    assert abs(ref[0][0][0] - 12 * p) < 1e-12 and abs(ref[0][1][0] - 12 * p * (1 - p)) < 1e-12
+
+
 def test_hiv_linear_subnetwork_closed_form(oracle_lib):
     """HIV network (Table 1) with the infection, mutation and infectivity rates set to
     zero (beta = gamma = mu = K = 0): no cell is infected, so I4 = I5 = V4 = F = 0 and what remains is
     first order -- U0 -> U0 + U (lambda), U -> T (d_ut), U -> Z4 and U -> Z5 (d_uz each), T, Z4, Z5
-    and V5 clearance.  For a first-order network the means solve the linear rate equations exactly:
-      U(t)  = A + B e^{-a t},  a = d_ut + 2 d_uz, A = lambda / a, B = U(0) - A
-      T(t)  = T0 e^{-d_t t} + d_ut [A (1 - e^{-d_t t}) / d_t + B (e^{-a t} - e^{-d_t t}) / (d_t - a)]
-      Zi(t) = Z0 e^{-d_z t} + d_uz [A (1 - e^{-d_z t}) / d_z + B (e^{-a t} - e^{-d_z t}) / (d_z - a)]
-    and V5 is a pure death: Binomial(100, e^{-d_v t}).  Pins the oracle's reading of Table 1's
+    and V5 clearance.  Means and variances against the exact linear moment equations
+    (_linear_moments), z < 4 with the closed form's variance.  Pins the oracle's reading of Table 1's
     reaction list (which species each reaction consumes and produces, and at which rate)."""
     O = oracle_lib
-    p = inputs.networks.HIV_PARAMS
-    net = inputs.hiv(beta=0.0, gamma=0.0, mu=0.0, K=0.0)
-    n, t_end = 2000, 20.0
-    res = O.run(O.OracleModel(net), np.arange(n), 3, t_end, 1.0, keep=False)
-    assert res.status == 0
-    lam, d_ut, d_uz, d_t, d_z, d_v = p["lam"], p["d_ut"], p["d_uz"], p["d_t"], p["d_z"], p["d_v"]
-    x0 = net.x0
-    a = d_ut + 2 * d_uz
-    A = lam / a
-    B = x0[1] - A
+    net = inputs.hiv(beta=0.0, gamma=0.0, mu=0.0, K=0.0, s1=0.0, d_iz=0.0, d_uf=0.0, d_tf=0.0)
+    res, _ = _check_linear(O, net, 2000, 20.0, 1.0, 3, must_move=(1, 2, 3, 4, 8))
+    for s in (5, 6, 7, 9):
+        assert np.all(res.mean[:, s] == 0) and np.all(res.var[:, s] == 0)
+    assert np.all(res.mean[:, 0] == 1) and np.all(res.var[:, 0] == 0)
 
-    def conv(rate_in, d, y0, t):
-        return y0 * math.exp(-d * t) + rate_in * (A * (1 - math.exp(-d * t)) / d
-                                                  + B * (math.exp(-a * t) - math.exp(-d * t)) / (d - a))
 
-    for k in range(1, int(t_end) + 1):
-        t = float(k)
-        mu = {1: A + B * math.exp(-a * t), 2: conv(d_ut, d_t, x0[2], t),
-              3: conv(d_uz, d_z, x0[3], t), 4: conv(d_uz, d_z, x0[4], t)}
-        for s, m_s in mu.items():
-            assert _zmean(res.mean[k, s], m_s, res.var[k, s], n) < 4.5, (k, s, res.mean[k, s], m_s)
-        q = math.exp(-d_v * t)
-        v5 = 100 * q
-        assert _zmean(res.mean[k, 8], v5, 100 * q * (1 - q), n) < 4.5, (k, res.mean[k, 8], v5)
-        for s in (5, 6, 7, 9):
-            assert res.mean[k, s] == 0 and res.var[k, s] == 0
-        assert res.mean[k, 0] == 1 and res.var[k, 0] == 0
+@pytest.mark.parametrize("raised", [False, True])
+def test_hiv_bursts_and_productions_closed_form(oracle_lib, raised):
+    """Table 1's bursts "I5 -> V5 x 200" and "I4 -> V4 x 200" (reactions 19-20, PAPER.md:63-64 with
+    PAPER.md:91 "I4 x pi") and the productions that consume nothing -- sigma_2 (I -> I + Z, reactions
+    12-13), sigma_3 (V4 -> F + V4, reaction 21) -- plus the mutation V5 -> V4 (mu) and the I, V
+    clearances, on the first-order sub-network that remains when every bimolecular rate is 0
+    (beta = gamma = K = sigma_1 = delta_iz = delta_uf = delta_tf = 0) and I4 = I5 = 5 at t = 0.  The
+    means and variances solve the linear moment equations exactly (_linear_moments).  raised=False
+    keeps Table 1's own rates (the bursts dominate: ~1000 virions of each strain); raised=True raises
+    sigma_2, sigma_3 and lowers pi so every production moves its species by many standard errors --
+    a dropped product, a burst multiplicity other than 200, or a burst that keeps its infected cell
+    fails the z-tests."""
+    O = oracle_lib
+    zero = dict(beta=0.0, gamma=0.0, K=0.0, s1=0.0, d_iz=0.0, d_uf=0.0, d_tf=0.0)
+    if raised:
+        zero.update(s2=0.8, s3=0.05, pi=1.5, mu=0.4, d_v=1.0)
+    net = inputs.hiv(**zero)
+    x0 = list(net.x0)
+    x0[5] = x0[6] = 5                                   # I4 = I5 = 5
+    net = Network(net.species, tuple(x0), net.reactions, "hiv-linear-bursts")
+    move = (1, 2, 3, 4, 5, 6, 7, 8) + ((9,) if raised else ())
+    res, ref = _check_linear(O, net, 3000, 3.0, 0.25, 31, must_move=move)
+    # the bursts' multiplicity is visible directly: with Table 1's pi the five I5 burst almost at once
+    if not raised:
+        assert ref[1][0][8] > 500 and res.mean[1, 8] > 500     # ~60 without the bursts
+    # the same data reject the plausible misreadings of reactions 12, 13, 19, 20 and 21 (z > 10)
+    from inputs.networks import Reaction
+    G = O.grid_size(3.0, 0.25)
+
+    def alt(j, products):
+        rx = list(net.reactions)
+        r = rx[j]
+        rx[j] = Reaction(r.reactants, tuple(products), r.rate, r.modifier_species, r.modifier_coef, r.name,
+                         r.mass_action, r.gates)
+        return Network(net.species, net.x0, tuple(rx))
+
+    U0, U, T, Z4, Z5, I4, I5, V4, V5, F = range(10)
+    wrong = {"burst keeps its cell": alt(18, [(I5, 1), (V5, 200)]),
+             "burst of 100": alt(18, [(V5, 100)]),
+             "X4 burst into V5": alt(19, [(V5, 200)])}
+    if raised:
+        wrong.update({"sigma2 consumes I": alt(11, [(Z5, 1)]), "sigma2 into Z4": alt(11, [(I5, 1), (Z4, 1)]),
+                      "sigma3 consumes V4": alt(20, [(F, 1)])})
+    for name, w in wrong.items():
+        ra = _linear_moments(w, [k * 0.25 for k in range(G)])
+        worst = max(_zmean(res.mean[k, s], ra[k][0][s], max(ra[k][1][s], 1e-30), 3000)
+                    for k in range(1, G) for s in range(10))
+        assert worst > 10, (name, worst)
 
 
 def _mini_hiv(swap_modifier_signs: bool = False):

@@ -216,6 +216,46 @@ def test_grid_alignment_edge_cases(oracle_lib):
     assert O.grid_size(400.0, 1.0) == 401
 
 
+def test_near_tie_counter_constructed_streams(oracle_lib):
+    """The near-tie counter (north_star: "any trajectory whose event time lies
+    within 1e-9 relative of a sample time flagged and counted"; R22)
+    on event streams with known counts.  It counts grid points, not
+    trajectories: a crossing of s_k is flagged when the candidate that crosses
+    it or the last applied event lies within 1e-9 * s_k of s_k, once per grid
+    point.  Each case pins one reading against its plausible misreadings
+    (per trajectory instead of per grid point, an absolute 1e-9 tolerance,
+    counting only the candidate or only the applied event, counting a point
+    twice)."""
+    O = oracle_lib
+
+    def ties(times, t_end, dt):
+        n = len(times)
+        states = np.arange(1, n + 1, dtype=np.int64).reshape(n, 1)
+        _, _, _, nt = O.align_events([0], times, states, t_end, dt)
+        return int(nt)
+
+    # relative: 5e-10 s_k away is near, 2e-9 s_k away is not (both sides of s_k)
+    assert ties([2.0 * (1 + 5e-10), 4.5], 5.0, 1.0) == 1            # candidate just past s_2
+    assert ties([2.0 * (1 - 5e-10), 4.5], 5.0, 1.0) == 1            # applied event just before s_2
+    assert ties([2.0 * (1 + 2e-9), 4.5], 5.0, 1.0) == 0
+    assert ties([2.0 * (1 - 2e-9), 4.5], 5.0, 1.0) == 0
+    # an event exactly at s_k is applied (right-continuous hold) and flagged when s_k is crossed
+    assert ties([3.0, 4.5], 5.0, 1.0) == 1
+    # per grid point: three near ties in one trajectory count 3 (a per-trajectory flag gives 1)
+    assert ties([1.0 * (1 + 4e-10), 2.0 * (1 - 4e-10), 2.5, 4.0, 4.7], 5.0, 1.0) == 3
+    # applied event and candidate both near the same s_k: one flag for that grid point, not two
+    assert ties([5.0 * (1 - 3e-10), 5.0 * (1 + 3e-10)], 5.0, 1.0) == 1
+    # relative, not absolute: at s_k = 1000 an offset of 5e-7 (5e-10 relative) is near ...
+    assert ties([1000.0 + 5e-7, 2500.0], 3000.0, 1000.0) == 1
+    # ... and at s_k = 1e-3 an offset of 5e-10 (5e-7 relative) is not
+    assert ties([1e-3 + 5e-10, 2.5e-3], 3e-3, 1e-3) == 0
+    # s_0 = 0 is never a near tie (tolerance 0 and no applied event), nor the hold after the last event
+    assert ties([1e-300, 0.5], 1.0, 1.0) == 0
+    assert ties([], 5.0, 1.0) == 0
+    # a candidate that crosses several grid points is compared with each of them
+    assert ties([0.5, 3.0 * (1 + 1e-10)], 5.0, 1.0) == 1
+
+
 # ------------------------------------------------------------------ moments
 def test_moments_printed_example(oracle_lib):
     O = oracle_lib
