@@ -106,16 +106,20 @@ def alg_fp64_per_event(net) -> float:
 def alg_warp_instr_per_event(net, lanes: int = 32) -> float:
     """Algorithmic WARP-instructions per applied event of the warp paths (K2,
     DESIGN.md §7), `lanes` = 32 (one trajectory per warp, order warp32) or 16
-    (two per warp, order warp16), P = ceil(R/lanes) propensities per lane.
+    (two per warp, order warp16s), P = ceil(R/lanes) propensities per lane.
     Per warp iteration: lane sum (P loads + P adds), log2(lanes)-step scan (2
-    shuffles + add), 3 broadcasts, tau (IEEE divide 9 + add), grid check, r,
-    selection (P adds + P compares + vprev shuffle + ballot/ffs/broadcast),
-    update and dependency recompute (one lane-parallel pass each), Philox +
-    u53 + plog amortised over `lanes` events, loop; divided by the
-    32/lanes trajectories a warp advances per iteration."""
+    shuffles + add), 3 broadcasts, tau (IEEE divide 9 + add), grid check,
+    selection, update and dependency recompute (one lane-parallel pass each),
+    Philox + u53 + plog amortised over `lanes` events, loop; divided by the
+    32/lanes trajectories a warp advances per iteration.  Selection: warp32 --
+    r, each lane re-sums its P propensities from v_{l-1} with a compare each
+    (2P), vprev shuffle, ballot/ffs/broadcast (2P + 5); warp16s -- r, ballot +
+    ffs for lane*, broadcast of v_{lane*-1}, one load, a 4-step scan of lane*'s
+    propensities, add, compare, ballot + ffs (22)."""
     P = max(1, -(-net.R // lanes))
     steps = 5 if lanes == 32 else 4
-    per_iter = 2 * P + 3 * steps + 6 + 10 + 2 + (2 * P + 5) + 5 + 15 + 78 / lanes + 3
+    select = (2 * P + 5) if lanes == 32 else (1 + 2 + 2 + 1 + 3 * 4 + 1 + 1 + 2)
+    per_iter = 2 * P + 3 * steps + 6 + 10 + 2 + select + 5 + 15 + 78 / lanes + 3
     return per_iter / (32 // lanes)
 
 
@@ -473,8 +477,10 @@ def main():
     ap.add_argument("--path", type=int, default=0)
     ap.add_argument("--block", type=int, default=0)
     ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--tail-lanes", type=int, default=0, help="K1 tail compaction threshold (0 default, -1 off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dump", action="store_true", help="config 4: skip the raw-trajectory dump")
     ap.add_argument("--variant", default="A", choices=["A", "B"],
                     help="HIV configs: B = the gated time-triggered mutation (SPEC.md:424, NEXT 3)")
     ap.add_argument("--workload", default="config", choices=["config", "sweep", "union", "trajectories", "dump"],
@@ -528,18 +534,32 @@ def main():
     G = S.grid_size(t_end, dt)
     model = S.Model(net)
     path = args.path or cfg.path
-    opts = dict(block=args.block, blocks_per_sm=args.blocks_per_sm)
+    opts = dict(block=args.block, blocks_per_sm=args.blocks_per_sm, tail_lanes=args.tail_lanes)
 
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
+    # config 4 dumps its 65,536 chosen trajectories raw (BASELINE configs[4], R24): each
+    # rank dumps the ones in its shard into page-locked host memory, gathered in rank order
+    dump_ids = None
+    if args.config == 4 and not args.no_dump:
+        all_dump = inputs.dump_ids(cfg.n_trajectories, cfg.n_dump, cfg.seed)
+        dump_ids = all_dump[all_dump < n_total]
     # rank r owns the aligned id shard r; roots all-gathered over NCCL, merged in rank order
-    ens = D.ShardedEnsemble.for_model(model, n_total, t_end, dt, cfg.seed, dev, path=path, stream=sh, **opts)
+    ens = D.ShardedEnsemble.for_model(model, n_total, t_end, dt, cfg.seed, dev, path=path, stream=sh,
+                                      dump_ids=dump_ids, dump_pinned=dump_ids is not None, **opts)
     cells = ens.cells
     l2 = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    dump_stats = []
 
     def step():
         l2.zero_()                                               # flush L2 between steps
-        return ens.step()
+        res = ens.step()
+        if dump_ids is not None:
+            loc = res.local
+            g = D.gather_dump(loc.dump if loc is not None else None, dev)   # rank order, on rank 0
+            dump_stats.append((loc.dump_bytes if loc is not None else 0, loc.dump_ms if loc is not None else 0.0,
+                               0 if g is None else len(g.ids)))
+        return res
 
     # JIT + warm-up (untimed)
     jit0 = time.perf_counter()
@@ -659,7 +679,19 @@ def main():
                        "peak_basis": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "B200 nominal"}
 
     clocks = clk.summary()
-    cpu = None
+    dump_block = None
+    if dump_ids is not None and dump_stats:
+        timed = dump_stats[args.warmup:args.warmup + args.steps]
+        b = statistics.mean(x[0] for x in timed)
+        dms = statistics.mean(x[1] for x in timed)
+        dump_block = {"n_dump_per_gpu": int(len(dump_ids) // world), "n_dump_gathered": int(timed[-1][2]),
+                      "bytes_per_step_per_gpu": int(b), "d2h_ms": dms,
+                      "d2h_GBps": b / (dms / 1e3) / 1e9 if dms > 0 else None,
+                      "written_in_loop_GBps": b / (k1_ms / 1e3) / 1e9 if k1_ms == k1_ms else None,
+                      "host_memory": "page-locked", "gather": "rank order (contiguous shards = id order)",
+                      "note": "K1's dump variant writes each dumped trajectory's grid states, event counts and "
+                              "last-event times while it simulates; the library copies them to the host after "
+                              "the run (d2h_ms, CUDA events)"}
     if not args.no_cpu_baseline and world == 1:
         cores = host_cores()
         n_cpu = 3 * max(cores, 8)
@@ -684,6 +716,7 @@ def main():
         "roofline_reduce": roofline_reduce,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "dump": dump_block,
         "gpu_launches": launches,
         "clocks": clocks,
         "jit_s": jit_s,

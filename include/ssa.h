@@ -165,7 +165,11 @@ typedef struct {
     int32_t blocks_per_sm;         /* resident blocks per SM for K1 / K2; 0 = occupancy maximum */
     const ssa_dump* dump;          /* NULL = no dump */
     int32_t outputs_on_device;     /* 1: ssa_result arrays and dump arrays are device pointers */
-    int32_t pad;
+    int32_t tail_lanes;            /* thread path, end of a launch: once no ids are left, the trajectories of a
+                                      warp with at most this many live lanes are suspended at their next grid
+                                      point and resumed packed into whole warps by a follow-up launch (tail
+                                      compaction); 0 = default (16), -1 = off.  Speed only: results are
+                                      bitwise the same for every value. */
 } ssa_run_options;
 
 /* Result.  The caller sets the output arrays (any may be NULL), each [G*S]

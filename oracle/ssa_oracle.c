@@ -235,6 +235,12 @@ int oracle_propensities(const oracle_model *M, const int64_t *x, double *a, int3
 /*         lane* = min{ l : v_l > r };  p = v_{lane*-1} (0 for lane 0), then  */
 /*         p += a_j over lane*'s reactions in order, j* = first j with p > r; */
 /*         if none, j* = the largest j <= lane*'s last index with a_j > 0.    */
+/*  mode 3 "warp16s" (the half-warp path since round 2): lane sums, scan and */
+/*         lane* as mode 2; then lane*'s P propensities (padded with 0 to 16  */
+/*         positions) are Hillis-Steele scanned over the 16 positions         */
+/*         (offsets 1,2,4,8) into s_q, p_q = v_{lane*-1} + s_q (s_q for lane  */
+/*         0), j* = lane*'s q-th reaction for the first q with p_q > r; if    */
+/*         none, the fallback of mode 2.                                      */
 /* r = u2 * a0 ("smallest j with sum_{i<=j} a_i > u2 a0").        */
 /* ------------------------------------------------------------------------ */
 static double total_sequential(const double *a, int R)
@@ -258,7 +264,7 @@ static int select_sequential(const double *a, int R, double r)
  * "warp16", a half warp per trajectory): P = ceil(R/L) contiguous reactions
  * per lane, lane sums from 0.0 in order, inclusive Hillis-Steele scan over
  * the L lane sums with offsets 1, 2, 4, ... < L, a0 = v_{L-1}. */
-static int mode_lanes(int mode) { return mode == 2 ? 16 : 32; }
+static int mode_lanes(int mode) { return (mode == 2 || mode == 3) ? 16 : 32; }
 
 static void warp_scan(const double *a, int R, int L, double v[32])
 {
@@ -299,7 +305,42 @@ static int select_warp(const double *a, int R, int L, const double v[32], double
     return -1;
 }
 
-/* Computes a0 and j* for given propensities and u2 (mode 0, 1 or 2). */
+/* mode 3: the within-lane step as a 16-position Hillis-Steele scan (DESIGN.md
+ * R13: the summation and selection order is declared per path; the paper is
+ * silent). */
+static int select_warp_scanned(const double *a, int R, const double v[32], double r)
+{
+    const int L = 16;
+    int P = (R + L - 1) / L;
+    if (P < 1) P = 1;
+    int lane = -1;
+    for (int l = 0; l < L; ++l) {
+        if (v[l] > r) { lane = l; break; }
+    }
+    if (lane < 0) return -1;
+    double s[16];
+    for (int q = 0; q < 16; ++q) {
+        const int j = lane * P + q;
+        s[q] = (q < P && j < R) ? a[j] : 0.0;
+    }
+    for (int o = 1; o < 16; o *= 2) {
+        double ns[16];
+        for (int q = 0; q < 16; ++q) ns[q] = (q >= o) ? (s[q - o] + s[q]) : s[q];
+        for (int q = 0; q < 16; ++q) s[q] = ns[q];
+    }
+    const double base = (lane > 0) ? v[lane - 1] : 0.0;
+    int last = (lane + 1) * P - 1;
+    if (last > R - 1) last = R - 1;
+    for (int q = 0; q < P && lane * P + q <= last; ++q) {
+        const double p = (lane > 0) ? base + s[q] : s[q];
+        if (p > r) return lane * P + q;
+    }
+    for (int j = last; j >= 0; --j)
+        if (a[j] > 0.0) return j;
+    return -1;
+}
+
+/* Computes a0 and j* for given propensities and u2 (mode 0, 1, 2 or 3). */
 int oracle_select(const double *a, int32_t R, int32_t mode, double u2, double *a0_out, int32_t *j_out)
 {
     double a0, r;
@@ -314,7 +355,7 @@ int oracle_select(const double *a, int32_t R, int32_t mode, double u2, double *a
         warp_scan(a, R, L, v);
         a0 = v[L - 1];
         r = u2 * a0;
-        j = (a0 > 0.0) ? select_warp(a, R, L, v, r) : -1;
+        j = (a0 > 0.0) ? (mode == 3 ? select_warp_scanned(a, R, v, r) : select_warp(a, R, L, v, r)) : -1;
     }
     *a0_out = a0;
     *j_out = j;
@@ -498,7 +539,8 @@ int oracle_trajectory_events(const oracle_model *M, uint64_t id, uint64_t seed, 
 
         /* a7 */
         double r = u2 * a0;
-        int j = (mode == 0) ? select_sequential(a, R, r) : select_warp(a, R, mode_lanes(mode), v, r);
+        int j = (mode == 0) ? select_sequential(a, R, r)
+              : (mode == 3) ? select_warp_scanned(a, R, v, r) : select_warp(a, R, mode_lanes(mode), v, r);
 
         /* a8 */
         for (int s = 0; s < S; ++s) x[s] += M->nu[(int64_t)j * S + s];

@@ -66,11 +66,29 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     __syncthreads();
     const double* kp = s_k;
 #endif
+#if SSA_K1_MIG
+    // tail compaction (P.mig_thresh > 0): live lanes per warp, and whether some lane of
+    // this block has found the launch's ids exhausted
+    __shared__ int s_wlive[SSA_K1_BLOCK / 32];
+    __shared__ int s_dry;
+    const int wid = threadIdx.x >> 5;
+    const double s_last = __dmul_rn((double)K, dt);   // s_K: a crossing past it ends the trajectory
+    bool may_suspend = true;                          // a resumed lane first crosses its pending grid point
+    if (threadIdx.x == 0) s_dry = 0;
+    __syncthreads();
+#endif
     // small ensembles (spread launch): one working lane per warp and one warp
     // per block, so each trajectory has an SM sub-partition to itself
     if (P.spread && (threadIdx.x & 31) != 0) return;
     double x[SSA_S];
     double kh[SSA_NKH > 0 ? SSA_NKH : 1];   // cached modified rates k^ (ssa_khat)
+    // the propensity prefix (a4); with SSA_CSKIP its first SSA_CSKIP entries are
+    // carried across iterations and recomputed only when a lane changed a species
+    // they read (cold-prefix reuse, runtime.cu gen_k1_model)
+    double c[SSA_R > 0 ? SSA_R : 1];
+#if SSA_CSKIP
+    bool lo_dirty = true;
+#endif
     double t = 0.0, s_next = 0.0;
     ssa_u64 e = 0, hash = 0, ties = 0, rel = 0, id = 0, vid = 0;
     long long k = 0, slot = -1;
@@ -103,8 +121,43 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             kp = s_k + ptl * (ssa_u64)P.n_pool;
         }
 #else
+#if SSA_K1_MIG
+        if (P.mig_in) {
+            // resume a trajectory a sparse warp of the previous launch suspended
+            const ssa_u64 q = atomicAdd(P.mig_in_take, 1ull);
+            if (q < P.mig_in_n) {
+                const double* st = P.mig_in + q * (ssa_u64)(SSA_S + 6);
+#pragma unroll
+                for (int s = 0; s < SSA_S; ++s) x[s] = st[s];
+                t = st[SSA_S];
+                e = (ssa_u64)__double_as_longlong(st[SSA_S + 1]);
+                k = __double_as_longlong(st[SSA_S + 2]);
+                rel = (ssa_u64)__double_as_longlong(st[SSA_S + 3]);
+                hash = (ssa_u64)__double_as_longlong(st[SSA_S + 4]);
+                ties = (ssa_u64)__double_as_longlong(st[SSA_S + 5]);
+                vid = P.id_begin + rel;
+                id = vid;
+#if SSA_K1_DUMP
+                slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
+#endif
+                ssa_khat(x, kh SSA_KP_ARG);
+                s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+                status = 0; absorbed = 0; err_r = -1;
+                may_suspend = false;
+#if SSA_CSKIP
+                lo_dirty = true;
+#endif
+                return true;
+            }
+        }
+#endif
         rel = atomicAdd(P.work, 1ull);
-        if (rel >= P.n_ids) return false;
+        if (rel >= P.n_ids) {
+#if SSA_K1_MIG
+            *(volatile int*)&s_dry = 1;
+#endif
+            return false;
+        }
 #endif
         vid = P.id_begin + rel;
 #if !SSA_K1_SWEEP
@@ -118,6 +171,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         ssa_khat(x, kh SSA_KP_ARG);
         t = 0.0; s_next = 0.0; e = 0; k = 0; hash = SSA_FNV_OFFSET; ties = 0;
         status = 0; absorbed = 0; err_r = -1;
+#if SSA_CSKIP
+        lo_dirty = true;
+#endif
         return true;
     };
 
@@ -152,6 +208,13 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #if SSA_K1_RECORD == 2
     if (live) { rec_left = P.rec_stride; rec_point(0, 0.0); }
 #endif
+#if SSA_K1_MIG
+    if (!P.spread) {
+        const unsigned b = __ballot_sync(0xffffffffu, live);
+        if ((threadIdx.x & 31) == 0) s_wlive[wid] = __popc(b);
+        __syncwarp();
+    }
+#endif
     while (live) {
         // a2: one Philox block per candidate event, counter (e, id)
 #if SSA_KS_IMM
@@ -164,8 +227,14 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // a3 + a4 (the propensity prefix chain) and a5's logarithm are
         // independent dependency chains in one basic block, so the scheduler
         // interleaves them.
-        double c[SSA_R > 0 ? SSA_R : 1];
+#if SSA_CSKIP
+        // c_0..c_{CSKIP-1}: recomputed by the whole warp (a uniform branch) when any
+        // lane's last event changed a species they read, else reused as they are
+        if (__any_sync(__activemask(), lo_dirty)) ssa_prefix_lo(x, kh, c SSA_KP_ARG);
+        const double a0 = ssa_prefix_hi(x, kh, c SSA_KP_ARG);
+#else
         const double a0 = ssa_prefix(x, kh, c SSA_KP_ARG);
+#endif
 #if SSA_K1_PROF
         // dispatch profile (a model's first thread-path run): at every 4096th event of a
         // trajectory, the propensity shares a_j / a0 of the current state -- their mean
@@ -196,6 +265,28 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         double tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
         if (!fast || tn > s_next) {
             // ---------------- rare path: a5 edge cases, a6, end + refill
+#if SSA_K1_MIG
+            // tail compaction: no ids left and this warp is sparse -- suspend before
+            // this grid crossing (the candidate is a function of (x, t, e), so the
+            // resumed lane recomputes it bit for bit) and leave the warp
+            if (P.mig_thresh && may_suspend && status == 0 && fast && tn <= s_last &&
+                *(volatile int*)&s_wlive[wid] <= P.mig_thresh &&
+                (*(volatile int*)&s_dry || *(volatile ssa_u64*)P.work >= P.n_ids)) {
+                const ssa_u64 q = atomicAdd(P.mig_out_n, 1ull);
+                double* st = P.mig_out + q * (ssa_u64)(SSA_S + 6);
+#pragma unroll
+                for (int s = 0; s < SSA_S; ++s) st[s] = x[s];
+                st[SSA_S] = t;
+                st[SSA_S + 1] = __longlong_as_double((long long)e);
+                st[SSA_S + 2] = __longlong_as_double(k);
+                st[SSA_S + 3] = __longlong_as_double((long long)rel);
+                st[SSA_S + 4] = __longlong_as_double((long long)hash);
+                st[SSA_S + 5] = __longlong_as_double((long long)ties);
+                atomicSub(&s_wlive[wid], 1);
+                live = false;
+                continue;
+            }
+#endif
             bool fin = false;
             if (!fast) {
                 if (a0 > 0.0 && a0 < INF) {
@@ -237,6 +328,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
                 } while (tn > s_next);
                 fin = (k > K);
+#if SSA_K1_MIG
+                may_suspend = true;
+#endif
             }
             if (fin) {
                 // trajectory done: per-trajectory records, then refill (a1)
@@ -270,6 +364,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 }
 #endif
                 live = start();
+#if SSA_K1_MIG
+                if (!live && !P.spread) atomicSub(&s_wlive[wid], 1);
+#endif
 #if SSA_K1_RECORD == 2
                 if (live) { rec_left = P.rec_stride; rec_point(0, 0.0); }
 #endif
@@ -294,6 +391,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         ssa_apply(j, x);
 #endif
         if (ssa_khat_dirty(j)) ssa_khat(x, kh SSA_KP_ARG);   // a modifier species changed
+#if SSA_CSKIP
+        lo_dirty = !ssa_lo_clean(j);
+#endif
         t = tn;
         ++e;
 #if SSA_K1_DUMP

@@ -3,13 +3,24 @@
 // helpers -- k2_rx, k2_rxd, the propensity evaluators -- it uses) when the
 // generated section defines SSA_K2_HALF = 1.
 //
-// Order "warp16" (R13; oracle mode 2): lane l of the half owns
+// Order "warp16s" (R13; oracle mode 3): lane l of the half owns
 // the P = ceil(R/16) contiguous reactions l*P + q; lane sums from 0.0, then an
 // inclusive Hillis-Steele scan over the 16 lanes (offsets 1, 2, 4, 8; the
-// shuffles are segmented with width 16), a0 = v_15, and the same speculative
-// selection as K2 within the half.  Per warp the scan, the broadcasts, the
-// division and the update/recompute passes now serve two events, which is
-// where the one-trajectory-per-warp kernel spent most of its instructions.
+// shuffles are segmented with width 16), a0 = v_15, lane* = min{l : v_l > r}.
+// The step inside lane* is a second 16-position Hillis-Steele scan over
+// lane*'s propensities, one per lane of the half (lane q reads lane*'s q-th
+// reaction), p_q = v_{lane*-1} + s_q, j* = lane*'s first q with p_q > r -- a
+// ballot instead of every lane re-summing its P propensities sequentially.
+// Per warp the scans, the broadcasts, the division and the update/recompute
+// passes serve two events.
+//
+// Shared memory per half: x[S] and the propensities a[q*17 + l] (reaction
+// l*P + q; row stride 17 doubles, so both the lane sums -- fixed q, l = 0..15 --
+// and the lane* scan -- fixed l, q = 0..15 -- are bank-conflict free).  Per
+// block: the model's per-reaction record {nu begin, nu end, dep begin, dep
+// end} (one 16-byte load once j* is known) and the dependency entries
+// pre-resolved to (reactant species and coefficients, propensity slot,
+// reaction) so that the recompute of dep(j*) reads x and the rate directly.
 //
 // Both halves execute the common path in lockstep (the shuffles are
 // full-warp); rare paths (grid crossing, end of a trajectory, refill, the
@@ -19,6 +30,26 @@
 
 #if SSA_K2_HALF
 #define SSA_HL 16
+#define SSA_AS 17                            // row stride of a[] (doubles)
+
+// dependency entry: sa | sb << 14 | ma << 28 | mb << 30 | slot << 32 | reaction << 48
+static __device__ __forceinline__ double k2h_propensity(ssa_u64 de, const k2_rxd* __restrict__ rxd,
+                                                        const double* __restrict__ x)
+{
+    const unsigned lo = (unsigned)de;
+    const int rxi = (int)(de >> 48);
+    const double f1 = k2_factor_bf(x[lo & 0x3FFFu], (int)((lo >> 28) & 3u));
+    const double f2 = k2_factor_bf(x[(lo >> 14) & 0x3FFFu], (int)(lo >> 30));
+    const double h = __dmul_rn(f1, f2);
+#if SSA_HAS_MODS
+    const k2_rxd& d = rxd[rxi];
+    double k = __dadd_rn(d.rate, __dmul_rn(d.modc, x[d.sms & 0xFFFF]));
+    k = (k < 0.0) ? 0.0 : k;
+    return k2_gated(__dmul_rn(k, h), d.gw, x);
+#else
+    return k2_gated(__dmul_rn(rxd[rxi].rate, h), rxd[rxi].gw, x);
+#endif
+}
 
 extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(const ssa_k2_params P)
 {
@@ -35,21 +66,20 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     const int hl = lane & 15;                // lane within the half
     const unsigned FULL = 0xffffffffu;
     const unsigned HALF = 0xFFFFu << (16 * h);
-    // shared: rx[R] | x0[S] | per warp, per half (x[S] | a[P][16]) | nu_off | nu_ent | dep_off | dep_ent | rxd
+    // shared: rx[R] | x0[S] | per warp, per half (x[S] | a[P*17]) | rec[R] | nu_ent | dent | rxd
     // the packed table rx is needed only by the general evaluator (coefficient-3 models)
     k2_rx* rx = (k2_rx*)k2_smem_raw;
     double* x0 = (double*)(rx + (SSA_HAS_M3 ? SSA_R : 0));
-    double* x = x0 + SSA_S + (size_t)warp * 2 * (SSA_S + SSA_HL * SSA_P) + (size_t)h * (SSA_S + SSA_HL * SSA_P);
+    double* x = x0 + SSA_S + (size_t)warp * 2 * (SSA_S + SSA_AS * SSA_P) + (size_t)h * (SSA_S + SSA_AS * SSA_P);
     {
         unsigned xs = (unsigned)__cvta_generic_to_shared(x);
         asm volatile("" : "+r"(xs));
         x = (double*)__cvta_shared_to_generic(xs);
     }
-    double* a = x + SSA_S;                                     // a[q*16 + l]: reaction l*P + q
-    int* nu_off = (int*)(x0 + SSA_S + (size_t)SSA_K2_WARPS * 2 * (SSA_S + SSA_HL * SSA_P));
-    int* nu_ent = nu_off + (SSA_R + 1);
-    int* dep_off = nu_ent + P.n_ent;
-    int* dep_ent = dep_off + (SSA_R + 1);
+    double* a = x + SSA_S;                                     // a[q*17 + l]: reaction l*P + q
+    int4* rec = (int4*)(k2_smem_raw + P.rec_offset);          // {nu begin, nu end, dep begin, dep end}
+    int* nu_ent = (int*)(rec + SSA_R);
+    ssa_u64* dent = (ssa_u64*)(k2_smem_raw + P.dent_offset);
 #if !SSA_HAS_M3
     k2_rxd* rxd = (k2_rxd*)(k2_smem_raw + P.rxd_offset);
 #endif
@@ -63,9 +93,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     (void)rx;
 #endif
     for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
-    for (int i = threadIdx.x; i <= SSA_R; i += SSA_K2_BLOCK) { nu_off[i] = P.nu_off[i]; dep_off[i] = P.dep_off[i]; }
+    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) rec[i] = P.rec[i];
     for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_ent[i] = P.nu_ent[i];
-    for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dep_ent[i] = P.dep_ent[i];
+    for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dent[i] = P.dent[i];
 #if !SSA_HAS_M3
     for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
         const ssa_u64 pk = P.pk[i];
@@ -76,9 +106,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         d.modc = (ms != 0x3FFF) ? P.modc[i] : 0.0;
         const int sa = n >= 1 ? (int)((pk >> 2) & 0x3FFF) : 0, sb = n >= 2 ? (int)((pk >> 18) & 0x3FFF) : 0;
         const int ma = n >= 1 ? (int)((pk >> 16) & 3) : 0, mb = n >= 2 ? (int)((pk >> 32) & 3) : 0;
-        const int slot = (i % SSA_P) * SSA_HL + i / SSA_P;
         d.sab = sa | (sb << 16);
-        d.sms = (ms != 0x3FFF ? ms : 0) | (slot << 16);
+        d.sms = (ms != 0x3FFF ? ms : 0);
         d.mab = ma | (mb << 8);
         d.pad = 0;
         d.gw = P.gw[i];
@@ -122,9 +151,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         for (int q = 0; q < SSA_P; ++q) {
             const int j = hl * SSA_P + q;
 #if SSA_HAS_M3
-            a[q * SSA_HL + hl] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+            a[q * SSA_AS + hl] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
 #else
-            a[q * SSA_HL + hl] = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
+            a[q * SSA_AS + hl] = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
 #endif
         }
         __syncwarp(HALF);
@@ -145,12 +174,10 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         // a4: lane sum, scan over the half (width 16)
         double L = 0.0;
 #pragma unroll
-        for (int q = 0; q < SSA_P; ++q) L = __dadd_rn(L, a[q * SSA_HL + hl]);
+        for (int q = 0; q < SSA_P; ++q) L = __dadd_rn(L, a[q * SSA_AS + hl]);
         double v = L;
 #pragma unroll
-        for (int o = 1; o < SSA_HL; o <<= 1) {
-            v = ssa_scan_step(v, o, 0x1000);     // width 16
-        }
+        for (int o = 1; o < SSA_HL; o <<= 1) v = ssa_scan_step(v, o, 0x1000);     // width 16
         const double a0 = __shfl_sync(FULL, v, SSA_HL - 1, SSA_HL);
         // a5
         const int src = (int)(e & 15ull);
@@ -159,21 +186,17 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         const unsigned a0hi = (unsigned)__double2hiint(a0);
         const bool fast = a0hi - (123u << 20) < ((1923u - 123u) << 20);   // a0 in [2^-900, 2^901)
         double tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
-        // a7, speculatively in every lane (full warp: both halves)
+        // a7: lane* = min{l : v_l > r}; then lane q of the half takes lane*'s q-th
+        // propensity, a second scan gives s_q, p_q = v_{lane*-1} + s_q, q* = min{q : p_q > r}
         const double r = __dmul_rn(u2, a0);
-        const double vprev = __shfl_up_sync(FULL, v, 1, SSA_HL);
-        double p = (hl > 0) ? vprev : 0.0;
-        int over = 0;
-#pragma unroll
-        for (int q = 0; q < SSA_P; ++q) {
-            p = __dadd_rn(p, a[q * SSA_HL + hl]);
-            asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
-                : "+r"(over) : "d"(p), "d"(r));
-        }
-        const int jl = over ? SSA_P - over : -1;
         const unsigned bal = (__ballot_sync(FULL, v > r) >> (16 * h)) & 0xFFFFu;
         const int ls = bal ? __ffs(bal) - 1 : 0;
-        const int jq = __shfl_sync(FULL, jl, ls, SSA_HL);
+        const double base = __shfl_sync(FULL, v, ls > 0 ? ls - 1 : 0, SSA_HL);
+        double y = (hl < SSA_P && ls * SSA_P + hl < SSA_R) ? a[hl * SSA_AS + ls] : 0.0;
+#pragma unroll
+        for (int o = 1; o < SSA_HL; o <<= 1) y = ssa_scan_step(y, o, 0x1000);
+        const double p = (ls > 0) ? __dadd_rn(base, y) : y;
+        const unsigned bq = (__ballot_sync(FULL, hl < SSA_P && p > r) >> (16 * h)) & 0xFFFFu;
 
         bool apply = live;
         if (live && (!fast || tn > s_next)) {     // rare path of this half
@@ -189,7 +212,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                     int bad = SSA_R;
 #pragma unroll
                     for (int q = SSA_P - 1; q >= 0; --q)
-                        if (hl * SSA_P + q < SSA_R && !(fabs(a[q * SSA_HL + hl]) < INF)) bad = hl * SSA_P + q;
+                        if (hl * SSA_P + q < SSA_R && !(fabs(a[q * SSA_AS + hl]) < INF)) bad = hl * SSA_P + q;
 #pragma unroll
                     for (int o = 8; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(HALF, bad, o, SSA_HL));
                     err_r = bad < SSA_R ? bad : -1;
@@ -255,35 +278,34 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         {
             int j = 0;
             if (!apply) {
-            } else if (jq >= 0) {
-                j = ls * SSA_P + jq;
+            } else if (bq) {
+                j = ls * SSA_P + (__ffs(bq) - 1);
             } else {
                 // rounding fallback (rare): the largest j <= lane*'s last index with a_j > 0
                 int lp = -1;
 #pragma unroll
                 for (int q = 0; q < SSA_P; ++q)
-                    if (a[q * SSA_HL + hl] > 0.0) lp = hl * SSA_P + q;
+                    if (hl * SSA_P + q < SSA_R && a[q * SSA_AS + hl] > 0.0) lp = hl * SSA_P + q;
                 const unsigned m2 = (__ballot_sync(HALF, lp >= 0 && hl <= ls) >> (16 * h)) & 0xFFFFu;
                 j = __shfl_sync(HALF, lp, 31 - __clz(m2), SSA_HL);
             }
             // a8: state update (lane t of the half takes the t-th net change)
-            const int nb = apply ? nu_off[j] : 0, ne = apply ? nu_off[j + 1] : 0;
+            const int4 rj = rec[j];
+            const int nb = apply ? rj.x : 0, ne = apply ? rj.y : 0;
             for (int q = nb + hl; q < ne; q += SSA_HL) {
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
                 x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));
             }
             __syncwarp();
-            // a3: the half recomputes dep(j)
-            const int db = apply ? dep_off[j] : 0, de = apply ? dep_off[j + 1] : 0;
+            // a3: the half recomputes dep(j), one entry per lane
+            const int db = apply ? rj.z : 0, de = apply ? rj.w : 0;
             for (int q = db + hl; q < de; q += SSA_HL) {
-                const int jj = dep_ent[q];
+                const ssa_u64 d = dent[q];
 #if !SSA_HAS_M3
-                const k2_rxd d = rxd[jj];
-                a[(unsigned)d.sms >> 16] = k2_propensity_d(d, x);
+                a[(unsigned)(d >> 32) & 0xFFFFu] = k2h_propensity(d, rxd, x);
 #else
-                const int l = jj / SSA_P, qq = jj - l * SSA_P;
-                a[qq * SSA_HL + l] = k2_propensity(rx[jj], x);
+                a[(unsigned)(d >> 32) & 0xFFFFu] = k2_propensity(rx[(int)(d >> 48)], x);
 #endif
             }
             __syncwarp();

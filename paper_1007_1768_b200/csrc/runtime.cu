@@ -83,6 +83,7 @@ struct K2Kernel {
     cudaKernel_t fn = nullptr;
     size_t smem = 0;
     size_t rxd_offset = 0;
+    size_t rec_offset = 0, dent_offset = 0;   // half-warp layout
     int blocks_per_sm = 0;
 };
 
@@ -97,6 +98,8 @@ struct K2Dev {
     double *rate = nullptr, *modc = nullptr, *x0 = nullptr;
     int *nu_off = nullptr, *nu_ent = nullptr;
     int *dep_off = nullptr, *dep_ent = nullptr;
+    int4* rec = nullptr;                    // half-warp path: per-reaction {nu b, nu e, dep b, dep e}
+    ssa_u64* dent = nullptr;                // half-warp path: resolved dependency entries
     std::map<std::string, K2Kernel> kern;   // "block/dump" -> NVRTC-compiled K2
 };
 
@@ -395,6 +398,8 @@ struct K1Gen {
     int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
     std::vector<int> hot;   // hot=a:b:...: reactions updated by predicated adds ahead of the jump table
     bool spread32 = true;   // small-ensemble launches use a (32, 1) launch-bounds variant (nospread32: off)
+    bool no_cskip = true;   // cskip: reuse the cold prefix (measured 1.6% slower on HIV: the warp-uniform
+                            // branch splits the event loop's basic block; off by default)
 };
 
 static K1Gen k1_gen()
@@ -408,6 +413,7 @@ static K1Gen k1_gen()
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
         if (s.find("nospread32") != std::string::npos) r.spread32 = false;
+        if (s.find("cskip") != std::string::npos && s.find("nocskip") == std::string::npos) r.no_cskip = false;
         const size_t h = s.find("hot=");
         if (h != std::string::npos) {
             size_t q = h + 4;
@@ -444,6 +450,11 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         o << "#define SSA_K1_RECORD 0\n";
     }
     o << "#define SSA_K1_PROF " << (spec && spec->prof ? 1 : 0) << "\n";
+    // tail compaction (k1_thread.cuh): plain, dump and profiling variants
+    o << "#define SSA_K1_MIG " << ((!sweep && record == 0) ? 1 : 0) << "\n";
+    std::vector<int> hot;   // the dispatch profile's hot reactions (K1Spec, or the knob)
+    for (int hj : (!g.hot.empty() ? g.hot : (spec ? spec->hot : std::vector<int>())))
+        if (hj >= 0 && hj < R) hot.push_back(hj);
     o << "#define SSA_S " << S << "\n#define SSA_R " << R << "\n#define SSA_K1_BLOCK " << block
       << "\n#define SSA_K1_MINB " << minb << "\n#define SSA_K1_SEL " << g.sel << "\n#define SSA_K1_DUMP "
       << (dump ? 1 : 0) << "\n#define SSA_K1_SWEEP " << (sweep ? 1 : 0) << "\n";
@@ -536,6 +547,72 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
           << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
     }
     o << "  return acc;\n}\n";
+    // Cold-prefix reuse (K1Spec::hot): the profile's hot reactions change a few
+    // species (HIV's V4 -> 0 and V5 -> 0 change V4, V5); every propensity before
+    // the first one that reads such a species -- indices [0, f) -- and hence the
+    // prefix c_0..c_{f-1} is unchanged by a hot event.  K1 keeps c_0..c_{f-1} across
+    // iterations and recomputes them only when some lane of the warp applied a
+    // reaction that changes a species they read (a warp-uniform branch); the
+    // values are the same expressions of the same counts, so the bits are those
+    // of the full recompute.  ssa_prefix_lo computes c_0..c_{f-1}, ssa_prefix_hi
+    // the rest from c_{f-1}; ssa_lo_clean(j) says reaction j leaves [0, f) alone.
+    int cskip = 0;
+    if (!hot.empty() && !(spec && spec->prof) && !sweep && !g.no_cskip) {
+        std::vector<char> hot_sp(S, 0), lo_reads(S, 0);
+        for (int hj : hot)
+            for (auto& d : m.rx[hj].nu) hot_sp[d.first] = 1;
+        auto reads = [&](int j, const std::vector<char>& set) {
+            const RxI& q = m.rx[j];
+            bool r = q.mod_sp >= 0 && set[q.mod_sp];
+            if (q.mass_action) for (auto& t : q.reac) r = r || set[t.first];
+            for (auto& gt : q.gates) r = r || set[gt.first];
+            return r;
+        };
+        int f = R;
+        for (int j = 0; j < R && f == R; ++j)
+            if (reads(j, hot_sp)) f = j;
+        std::vector<int> clean;
+        if (f >= 2 && f < R) {
+            for (int j = 0; j < f; ++j) {
+                const RxI& q = m.rx[j];
+                if (q.mod_sp >= 0) lo_reads[q.mod_sp] = 1;
+                if (q.mass_action) for (auto& t : q.reac) lo_reads[t.first] = 1;
+                for (auto& gt : q.gates) lo_reads[gt.first] = 1;
+            }
+            for (int j = 0; j < R; ++j) {
+                bool touches = false;
+                for (auto& d : m.rx[j].nu) touches = touches || lo_reads[d.first];
+                if (!touches) clean.push_back(j);
+            }
+            if (R <= 64 || clean.size() <= 4) cskip = f;
+        }
+        if (cskip) {
+            o << "static __device__ __forceinline__ void ssa_prefix_lo(const double (&x)[SSA_S], const double (&kh)[SSA_NKH > 0 ? SSA_NKH : 1], double (&c)[SSA_R > 0 ? SSA_R : 1] SSA_KP_PARAM) {\n";
+            o << "  double a, h, k, acc = 0.0; (void)a; (void)h; (void)k; (void)x; (void)kh;\n";
+            for (int j = 0; j < cskip; ++j)
+                o << "  { " << prop_stmts(m.rx[j], j, L, kh_of[j]) << " "
+                  << (j == 0 ? "acc = a;" : "acc = __dadd_rn(acc, a);") << " c[" << j << "] = acc; }\n";
+            o << "}\n";
+            o << "static __device__ __forceinline__ double ssa_prefix_hi(const double (&x)[SSA_S], const double (&kh)[SSA_NKH > 0 ? SSA_NKH : 1], double (&c)[SSA_R > 0 ? SSA_R : 1] SSA_KP_PARAM) {\n";
+            o << "  double a, h, k, acc = c[" << cskip - 1 << "]; (void)a; (void)h; (void)k; (void)x; (void)kh;\n";
+            for (int j = cskip; j < R; ++j)
+                o << "  { " << prop_stmts(m.rx[j], j, L, kh_of[j]) << " acc = __dadd_rn(acc, a); c[" << j
+                  << "] = acc; }\n";
+            o << "  return acc;\n}\n";
+            o << "static __device__ __forceinline__ bool ssa_lo_clean(int j) { return ";
+            if (clean.empty()) {
+                o << "false";
+            } else if (R <= 64) {
+                unsigned long long mask = 0;
+                for (int j : clean) mask |= 1ull << j;
+                o << "((0x" << std::hex << mask << std::dec << "ull >> j) & 1ull) != 0";
+            } else {
+                for (size_t i = 0; i < clean.size(); ++i) o << (i ? " || " : "") << "j == " << clean[i];
+            }
+            o << "; }\n";
+        }
+    }
+    o << "#define SSA_CSKIP " << cskip << "\n";
     // error path only: out of line, state passed by value so the caller's
     // counts never need an addressable (stack) copy
     o << "struct ssa_state_v { double v[SSA_S]; };\n";
@@ -591,9 +668,6 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         for (int s2 = 0; s2 < S; ++s2) o << (s2 ? ", " : "") << "\"+d\"(x[" << s2 << "])";
         o << "\n    : \"r\"(j)" << (rec ? ", \"l\"(out)" : "") << (rec ? "\n    : \"memory\"" : "") << ");\n";
     };
-    std::vector<int> hot;   // the dispatch profile's hot reactions (K1Spec, or the knob)
-    for (int hj : (!g.hot.empty() ? g.hot : (spec ? spec->hot : std::vector<int>())))
-        if (hj >= 0 && hj < R) hot.push_back(hj);
     o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
     if (use_brx) {
         if (!hot.empty()) {
@@ -823,6 +897,28 @@ static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block
     return k2_rxd_offset(S, R, P, n_ent, n_dep, block, half, rx) + 40 * (size_t)R;
 }
 
+// half-warp layout (k2_half.cuh): rx[R] (coefficient-3 models) | x0[S] | per warp, per half
+// (x[S] | a[17 P]) | rec[R] (16 B) | nu_ent | dent[n_dep] (8 B) | rxd[R] (40 B, 16-aligned)
+struct K2HalfLayout {
+    size_t rec = 0, dent = 0, rxd = 0, bytes = 0;
+};
+static K2HalfLayout k2_half_layout(int S, int R, int P, int n_ent, int n_dep, int block, bool rx)
+{
+    K2HalfLayout L;
+    const size_t warps = (size_t)(block / 32);
+    size_t b = (rx ? 32 * (size_t)R : 0) + 8 * (size_t)S + warps * 2 * 8 * ((size_t)S + 17 * (size_t)P);
+    b = (b + 15) & ~(size_t)15;
+    L.rec = b;
+    b += 16 * (size_t)R + 4 * (size_t)std::max(n_ent, 1);
+    b = (b + 7) & ~(size_t)7;
+    L.dent = b;
+    b += 8 * (size_t)std::max(n_dep, 1);
+    b = (b + 15) & ~(size_t)15;
+    L.rxd = b;
+    L.bytes = b + (rx ? 0 : 40 * (size_t)R);
+    return L;
+}
+
 static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, bool dump, bool half)
 {
     // longest net-change list and longest per-reaction dependency list (as
@@ -929,6 +1025,21 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         }
         const int n_dep_real = (int)dep_ent.size();
         if (dep_ent.empty()) dep_ent.push_back(0);
+        // half-warp path: per-reaction records and dependency entries resolved for its
+        // propensity layout a[q*17 + l] (reaction l*PH + q, PH = ceil(R/16))
+        const int PH = std::max(1, (R + 15) / 16);
+        std::vector<int4> rec(R1);
+        for (int j = 0; j < R; ++j) rec[j] = make_int4(nu_off[j], nu_off[j + 1], dep_off[j], dep_off[j + 1]);
+        std::vector<ssa_u64> dent(dep_ent.size(), 0);
+        for (size_t q = 0; q < (size_t)n_dep_real; ++q) {
+            const int jj = dep_ent[q];
+            const ssa_u64 w = pk[jj];
+            const int n = (int)(w & 3ull);
+            const ssa_u64 sa = n >= 1 ? (w >> 2) & 0x3FFF : 0, sb = n >= 2 ? (w >> 18) & 0x3FFF : 0;
+            const ssa_u64 ma = n >= 1 ? (w >> 16) & 3 : 0, mb = n >= 2 ? (w >> 32) & 3 : 0;
+            const ssa_u64 slot = (ssa_u64)((jj % PH) * 17 + jj / PH);
+            dent[q] = sa | (sb << 14) | (ma << 28) | (mb << 30) | (slot << 32) | ((ssa_u64)jj << 48);
+        }
         // image layout (8-byte aligned sections): pk | gw | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
         const size_t o_pk = 0, o_gw = o_pk + 8 * R1, o_rate = o_gw + 8 * R1, o_modc = o_rate + 8 * R1,
                      o_x0 = o_modc + 8 * R1;
@@ -936,7 +1047,9 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         const size_t o_ent = o_off + ((4 * nu_off.size() + 7) & ~(size_t)7);
         const size_t o_doff = o_ent + ((4 * nu_ent.size() + 7) & ~(size_t)7);
         const size_t o_dent = o_doff + ((4 * dep_off.size() + 7) & ~(size_t)7);
-        const size_t bytes = o_dent + 4 * dep_ent.size();
+        const size_t o_rec = (o_dent + 4 * dep_ent.size() + 15) & ~(size_t)15;
+        const size_t o_hd = o_rec + 16 * R1;
+        const size_t bytes = o_hd + 8 * dent.size();
         CU(cudaMallocHost(&k.host_image, bytes));
         char* h = (char*)k.host_image;
         memcpy(h + o_pk, pk.data(), 8 * R1);
@@ -948,6 +1061,8 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         memcpy(h + o_ent, nu_ent.data(), 4 * nu_ent.size());
         memcpy(h + o_doff, dep_off.data(), 4 * dep_off.size());
         memcpy(h + o_dent, dep_ent.data(), 4 * dep_ent.size());
+        memcpy(h + o_rec, rec.data(), 16 * R1);
+        memcpy(h + o_hd, dent.data(), 8 * dent.size());
         CU(cudaMalloc(&k.dev_image, bytes));
         CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
         char* d = (char*)k.dev_image;
@@ -960,6 +1075,8 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         k.nu_ent = (int*)(d + o_ent);
         k.dep_off = (int*)(d + o_doff);
         k.dep_ent = (int*)(d + o_dent);
+        k.rec = (int4*)(d + o_rec);
+        k.dent = (ssa_u64*)(d + o_hd);
         k.image_bytes = bytes;
         k.P = P;
         k.n_ent = n_ent_real;
@@ -981,8 +1098,16 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         CU(cudaLibraryLoadData(&kk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
         CU(cudaLibraryGetKernel(&kk.fn, kk.lib, "ssa_k2"));
         const bool m3 = has_m3(m);
-        kk.smem = k2_smem_bytes(S, R, PL, k.n_ent, k.n_dep, block, half, m3);
-        kk.rxd_offset = k2_rxd_offset(S, R, PL, k.n_ent, k.n_dep, block, half, m3);
+        if (half) {
+            const K2HalfLayout hl = k2_half_layout(S, R, PL, k.n_ent, k.n_dep, block, m3);
+            kk.smem = hl.bytes;
+            kk.rxd_offset = hl.rxd;
+            kk.rec_offset = hl.rec;
+            kk.dent_offset = hl.dent;
+        } else {
+            kk.smem = k2_smem_bytes(S, R, PL, k.n_ent, k.n_dep, block, half, m3);
+            kk.rxd_offset = k2_rxd_offset(S, R, PL, k.n_ent, k.n_dep, block, half, m3);
+        }
         if (kk.smem > 227 * 1024)
             return fail(SSA_ERR_UNSUPPORTED, "warp path: model needs %zu B of shared memory", kk.smem);
         CU(cudaFuncSetAttribute((const void*)kk.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kk.smem));
@@ -1098,6 +1223,7 @@ struct RunInfo {
     uint64_t h2d = 0, d2h = 0, reduce_bytes = 0, dump_bytes = 0;
     int launches = 0;
     uint64_t lanes = 0;   // SSA lanes launched (K1 threads that take trajectories)
+    int tail_passes = 0;  // K1 tail-compaction launches
 };
 
 // Reduce `count` elements per row from `in` down to one, writing the final
@@ -1314,6 +1440,20 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             info.h2d += sizeof(int) * ord.size();
         }
     }
+    // tail compaction (K1 plain / dump / profiling variants, not for small spread ensembles):
+    // two ping-pong buffers of suspended states and their counters
+    const int tail_lanes = (o && o->tail_lanes) ? o->tail_lanes : 16;
+    const bool mig = path == SSA_PATH_THREAD && !sw && !rec && !spread && tail_lanes > 0;
+    DevBuf migb[2], migc;
+    const ssa_u64 mig_rec = (ssa_u64)m->S + 6, mig_cap = (ssa_u64)grid * (ssa_u64)block;
+    ssa_u64* mig_host = nullptr;
+    if (mig) {
+        CU(migb[0].alloc(sizeof(double) * mig_rec * mig_cap, st));
+        CU(migb[1].alloc(sizeof(double) * mig_rec * mig_cap, st));
+        CU(migc.alloc(sizeof(ssa_u64) * 4, st));
+        CU(cudaMallocHost(&mig_host, sizeof(ssa_u64) * 2));
+    }
+    struct PinnedFree { ssa_u64* p; ~PinnedFree() { if (p) cudaFreeHost(p); } } mig_host_guard{mig_host};
     CU(statsb.alloc(sizeof(ssa_dev_stats), st));
     CU(work.alloc(sizeof(ssa_u64) * n_chunks, st));
     CU(cudaMemsetAsync(statsb.p, 0, sizeof(ssa_dev_stats), st));
@@ -1384,16 +1524,43 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             }
             p.spread = spread ? 1 : 0;
             p.prof = prof;
+            if (mig) {
+                ssa_u64* cnt = migc.as<ssa_u64>();   // [0] take index of the input, [1] suspended count
+                p.mig_thresh = tail_lanes;
+                p.mig_in = nullptr; p.mig_in_n = 0; p.mig_in_take = cnt;
+                p.mig_out = migb[0].as<double>(); p.mig_out_n = cnt + 1;
+                CU(cudaMemsetAsync(cnt, 0, sizeof(ssa_u64) * 2, st));
+            }
             void* args[] = {&p};
             CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(spread ? 32 : block), args, smem, st));
             info.launches += 1;
             info.lanes = std::max<uint64_t>(info.lanes, (uint64_t)grid * (spread ? 1 : block));
+            // tail compaction: resume the suspended trajectories packed into whole warps,
+            // launch after launch, until none is suspended
+            for (int pass = 0; mig; ++pass) {
+                ssa_u64* cnt = migc.as<ssa_u64>();
+                CU(cudaMemcpyAsync(mig_host, cnt, sizeof(ssa_u64) * 2, cudaMemcpyDeviceToHost, st));
+                CU(cudaStreamSynchronize(st));
+                const ssa_u64 n_in = mig_host[1];
+                if (n_in == 0) break;
+                if (n_in > mig_cap) return fail(SSA_ERR_CUDA, "tail compaction: %llu suspended > %llu lanes",
+                                                (unsigned long long)n_in, (unsigned long long)mig_cap);
+                p.mig_in = migb[pass & 1].as<double>(); p.mig_in_n = n_in;
+                p.mig_out = migb[(pass + 1) & 1].as<double>();
+                CU(cudaMemsetAsync(cnt, 0, sizeof(ssa_u64) * 2, st));
+                const int g2 = (int)std::min<ssa_u64>((ssa_u64)grid, (n_in + block - 1) / block);
+                CU(cudaLaunchKernel((const void*)k1->fn, dim3(g2), dim3(block), args, smem, st));
+                info.launches += 1;
+                info.tail_passes += 1;
+            }
         } else {
             ssa_k2_params p{};
             p.n_ent = k2->n_ent; p.n_dep = k2->n_dep;
             p.pk = k2->pk; p.gw = k2->gw; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
             p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
             p.rxd_offset = k2k->rxd_offset;
+            p.rec = k2->rec; p.dent = k2->dent;
+            p.rec_offset = k2k->rec_offset; p.dent_offset = k2k->dent_offset;
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
             p.dump_ids = dids.as<ssa_u64>(); p.n_dump = n_dump; p.dump_states = p_states; p.dump_e = p_e;
@@ -2073,9 +2240,11 @@ extern "C" ssa_status ssa_debug_k2_compile(const ssa_model* m, int32_t block, in
     if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
     std::vector<char> cubin;
     std::string lg;
+    // dump: bit 0 = the dump variant, bit 1 = HALFWARP, bits 4-7 = the residency target (0: 1)
     const bool half = (dump & 2) != 0;
+    const int minb = std::max(1, (dump >> 4) & 15);
     ssa_status st = nvrtc_compile(
-        k2_full_source(*m, std::max(1, (m->R + (half ? 15 : 31)) / (half ? 16 : 32)), block, 1, (dump & 1) != 0, half),
+        k2_full_source(*m, std::max(1, (m->R + (half ? 15 : 31)) / (half ? 16 : 32)), block, minb, (dump & 1) != 0, half),
         cubin, lg);
     if (log && log_cap) {
         std::string all = (st == SSA_OK) ? lg : g_err;

@@ -64,6 +64,45 @@ __global__ void k_flags(const ssa_u64* __restrict__ keys, ssa_u64 E, unsigned ch
         f[m] = (m + 1 == E || keys[m] != keys[m + 1]) ? 1 : 0;
 }
 
+// N / D rounded once to the nearest double (ties to even), for 0 <= N, 0 < D < 2^126:
+// the quotient's first 55 significant bits by integer (long) division, the rest folded
+// into a sticky bit -- the value a correctly rounded exact division (the oracle's
+// Fraction -> float) gives, so means and variances are bitwise the oracle's.
+__device__ int bitlen128(unsigned __int128 v)
+{
+    const unsigned long long hi = (unsigned long long)(v >> 64), lo = (unsigned long long)v;
+    return hi ? 128 - __clzll((long long)hi) : (lo ? 64 - __clzll((long long)lo) : 0);
+}
+
+__device__ double ratio_rn(unsigned __int128 N, unsigned __int128 D)
+{
+    if (N == 0) return 0.0;
+    unsigned __int128 q = N / D, r = N % D;
+    int ex = 0;
+    bool sticky;
+    const int qb = bitlen128(q);
+    if (qb > 55) {
+        const int sh = qb - 55;
+        sticky = r != 0 || (q & ((((unsigned __int128)1) << sh) - 1)) != 0;
+        q >>= sh;
+        ex = sh;
+    } else {
+        while (bitlen128(q) < 55) {      // next quotient bits of the fraction r / D
+            r <<= 1;
+            const bool b = r >= D;
+            if (b) r -= D;
+            q = (q << 1) | (b ? 1u : 0u);
+            --ex;
+        }
+        sticky = r != 0;
+    }
+    unsigned long long m = (unsigned long long)(q >> 2);
+    const bool guard = ((unsigned)q >> 1) & 1u, rest = (((unsigned)q & 1u) != 0) || sticky;
+    if (guard && (rest || (m & 1ull))) ++m;
+    if (m == (1ull << 53)) { m >>= 1; ++ex; }
+    return ldexp((double)m, ex + 2);
+}
+
 __global__ void k_xgroups(ssa_union_args a, const ssa_u64* __restrict__ keys, const unsigned* __restrict__ ypos,
                           ssa_u64 D, ssa_u64 NY, const long long* __restrict__ p1, const long long* __restrict__ p2)
 {
@@ -97,9 +136,9 @@ __global__ void k_xgroups(ssa_union_args a, const ssa_u64* __restrict__ keys, co
             x1 += s1;
             x2 += (__int128)s2;
         }
-        const __int128 num = (__int128)n * x2 - (__int128)x1 * x1;
-        a.mean[g * a.S + s] = __ddiv_rn((double)x1, (double)n);
-        a.var[g * a.S + s] = __ddiv_rn((double)num, __dmul_rn((double)n, (double)n));
+        const __int128 num = (__int128)n * x2 - (__int128)x1 * x1;     // >= 0 (Cauchy-Schwarz)
+        a.mean[g * a.S + s] = ratio_rn((unsigned __int128)x1, (unsigned __int128)n);
+        a.var[g * a.S + s] = ratio_rn((unsigned __int128)num, (unsigned __int128)n * (unsigned __int128)n);
     }
 }
 

@@ -68,7 +68,7 @@ class ssa_dump(C.Structure):
 class ssa_run_options(C.Structure):
     _fields_ = [("path", C.c_int32), ("device", C.c_int32), ("stream", C.c_void_p), ("chunk", C.c_uint64),
                 ("staging_budget_bytes", C.c_uint64), ("block", C.c_int32), ("blocks_per_sm", C.c_int32),
-                ("dump", C.POINTER(ssa_dump)), ("outputs_on_device", C.c_int32), ("pad", C.c_int32)]
+                ("dump", C.POINTER(ssa_dump)), ("outputs_on_device", C.c_int32), ("tail_lanes", C.c_int32)]
 
 
 class ssa_result(C.Structure):
@@ -215,9 +215,9 @@ class Model:
         """Generated K2 (warp path; half=True: two trajectories per warp) source."""
         return _k2_source(self, block, int(dump) | (2 if half else 0))
 
-    def k2_compile(self, block: int = 256, dump: bool = False, half: bool = False):
+    def k2_compile(self, block: int = 256, dump: bool = False, half: bool = False, minb: int = 1):
         """NVRTC-compile the model's K2 kernel (no device needed); returns (status, log, cubin bytes)."""
-        return _k2_compile(self, block, int(dump) | (2 if half else 0))
+        return _k2_compile(self, block, int(dump) | (2 if half else 0) | (min(max(minb, 1), 15) << 4))
 
     def k1_compile(self, block: int = 128, minb: int = 4, dump: bool = False):
         """NVRTC-compile the model's K1 kernel (no device needed); returns (status, log, cubin bytes)."""
@@ -274,9 +274,10 @@ class RunResult:
 
 
 def _options(path=SSA_PATH_AUTO, device=-1, stream=None, chunk=0, staging_budget_bytes=0, block=0,
-             blocks_per_sm=0, dump=None, outputs_on_device=False) -> ssa_run_options:
+             blocks_per_sm=0, dump=None, outputs_on_device=False, tail_lanes=0) -> ssa_run_options:
     o = ssa_run_options()
     o.path, o.device, o.chunk, o.staging_budget_bytes = path, device, chunk, staging_budget_bytes
+    o.tail_lanes = tail_lanes
     o.stream = stream
     o.block, o.blocks_per_sm = block, blocks_per_sm
     o.outputs_on_device = 1 if outputs_on_device else 0
@@ -455,14 +456,14 @@ def run_device(model: Model, n_trajectories: int, t_end: float, sample_dt: float
 
 def run_shard(model: Model, id_begin: int, id_end: int, t_end: float, sample_dt: float, seed: int, d_root, *,
               path: int = SSA_PATH_AUTO, stream=None, dump_ids=None, raise_on_error: bool = True,
-              **opts) -> RunResult:
+              dump_pinned: bool = False, **opts) -> RunResult:
     """ssa_run_shard: d_root is a torch CUDA float64 tensor [3, G*S] (n, mean, M2).  With
     raise_on_error=False a trajectory error (SSA_ERR_NUMERIC / OVERFLOW) is returned in
     .status instead of raised (the root's mean and M2 are then NaN)."""
     G = grid_size(t_end, sample_dt)
     dump = cdump = None
     if dump_ids is not None and len(dump_ids):
-        dump, cdump = _make_dump(dump_ids, G, model.S)
+        dump, cdump = _make_dump(dump_ids, G, model.S, dump_pinned)
     o = _options(path=path, stream=stream, dump=cdump, **opts)
     r = ssa_result()
     st = lib().ssa_run_shard(model.handle, id_begin, id_end, t_end, sample_dt, seed, C.c_void_p(d_root.data_ptr()),

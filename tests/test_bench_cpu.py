@@ -27,7 +27,10 @@ def test_algorithmic_counts(bench):
     # + the update's count adds (41 net-change entries over 27 reactions)
     assert bench.alg_fp64_per_event(hiv) == pytest.approx(2 + 24 + 9 + 37 + 52 + 2 + 41 / 27)
     c3 = inputs.config(3).network
-    assert bench.alg_warp_instr_per_event(c3, 16) == pytest.approx(63.4375)
+    # half-warp K2, order warp16s: lane sum 32 + scan 12 + broadcasts 6 + tau 10 + grid 2 + selection 22
+    # (lane* ballot, broadcast, load, 4-step scan, add, compare, ballot) + update 5 + recompute 15
+    # + RNG 78/16 + loop 3, per two events
+    assert bench.alg_warp_instr_per_event(c3, 16) == pytest.approx((32 + 12 + 6 + 10 + 2 + 22 + 5 + 15 + 78 / 16 + 3) / 2)
     assert bench.alg_warp_instr_per_event(c3, 32) == pytest.approx(95.4375 + 0.0, abs=0.01)
 
 

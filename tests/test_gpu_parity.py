@@ -14,7 +14,7 @@ from .helpers import assert_dump_equal, assert_moments_close, exact_moments, ora
 pytestmark = pytest.mark.gpu
 
 THREAD, WARP, HALF = 1, 2, 3
-MODE = {THREAD: 0, WARP: 1, HALF: 2}     # summation orders: sequential, warp32, warp16
+MODE = {THREAD: 0, WARP: 1, HALF: 3}     # summation orders: sequential, warp32, warp16s (oracle mode 3)
 
 
 @pytest.fixture(scope="module")
@@ -77,46 +77,27 @@ def test_hiv_full_horizon_sample(S):
     _parity(S, cfg.network, 16, cfg.t_end, cfg.dt, cfg.seed, THREAD)
 
 
-def test_hiv_config2_full_size_sampled(S):
-    """BASELINE configs[2] at full size (2^18 trajectories, 100 d): oracle replay
-    of 48 sampled trajectories (bit-exact) and exact moments of the whole
-    ensemble from the dumped grid states (T2: checks the tree reduction)."""
-    cfg = inputs.config(2)
-    n = cfg.n_trajectories
-    m = S.Model(cfg.network)
-    all_ids = np.arange(n, dtype=np.uint64)
-    r = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD, dump_ids=all_ids)
-    assert r.status == 0 and r.n_errors == 0
-    ref_mean, ref_var = exact_moments(r.dump.states)
-    assert_moments_close(r.mean, r.var, ref_mean, ref_var)
-    sample = inputs.dump_ids(n, 48, cfg.seed)
-    gx, ge, gt, sm = oracle_replay(cfg.network, sample, cfg.seed, cfg.t_end, cfg.dt, 0)
-    idx = sample.astype(np.int64)
-    assert np.array_equal(r.dump.states[idx], gx)
-    assert np.array_equal(r.dump.events_at[idx], ge)
-    assert np.array_equal(r.dump.time_at[idx], gt)
-    assert np.array_equal(r.dump.summary["hash"][idx], sm["hash"])
-    assert r.events == int(r.dump.summary["events"].sum())
-    # HIV structure: U0 is a catalyst
-    assert np.all(r.mean[:, 0] == 1.0) and np.all(r.var[:, 0] == 0.0)
+# (BASELINE configs[2] at full size -- T1 over 256 random ids and T2 over all 2^18 -- is
+# tests/test_gpu_bench_parity.py, on the exact kernel and launch bench.py times.)
 
 
 def test_config4_shards_sampled(S):
-    """BASELINE configs[4] (HIV, 400 d, 2^24 ids over W = 8 shards, 65,536
-    dumped ids): in two of the eight shards (ranks 0 and 7) an aligned block of
-    4096 ids is run at the full horizon through ssa_run_shard with global ids
-    (so the Philox stream is the one the 8-GPU run uses).  Every config-4
-    dumped id in the blocks is replayed by the oracle bit-exactly, and the
-    shard root of one block is checked against the exact moments of all its
-    4096 trajectories (T2)."""
+    """BASELINE configs[4] (HIV, 400 d, 2^24 ids over W = 8 shards, 65,536 dumped
+    ids): an aligned block of 2^16 ids inside shard 0 and one of 4096 ids inside
+    shard 7 run at the full horizon through ssa_run_shard with global ids (so the
+    Philox streams are the ones the 8-GPU run uses).  Every config-4 dumped id in
+    the blocks (>= 256) is replayed by the oracle bit-exactly,
+    and the 2^16 block's shard root is checked against the exact moments of all its
+    trajectories (T2)."""
     import torch
     cfg = inputs.config(4)
-    n_total, W, blk = cfg.n_trajectories, 8, 4096
+    n_total, W = cfg.n_trajectories, 8
     m = S.Model(cfg.network)
     G = S.grid_size(cfg.t_end, cfg.dt)
     cells = G * cfg.network.S
     dumped = inputs.dump_ids(n_total, cfg.n_dump, cfg.seed)
-    for rank in (0, W - 1):
+    replayed = 0
+    for rank, blk in ((0, 1 << 16), (W - 1, 4096)):
         b, e = S.shard_bounds(n_total, W, rank)
         lo = b + (e - b) // 2                        # aligned block in the middle of the shard
         hi = lo + blk
@@ -129,17 +110,16 @@ def test_config4_shards_sampled(S):
         assert r.n_errors == 0
         pos = np.searchsorted(ids, sel)
         gx, ge, gt, sm = oracle_replay(cfg.network, sel, cfg.seed, cfg.t_end, cfg.dt, 0)
-        assert np.array_equal(r.dump.states[pos], gx)
-        assert np.array_equal(r.dump.events_at[pos], ge)
-        assert np.array_equal(r.dump.time_at[pos], gt)
-        assert np.array_equal(r.dump.summary["hash"][pos], sm["hash"])
-        assert np.array_equal(r.dump.summary["events"][pos], sm["events"])
+        sub = S.Dump(sel, r.dump.states[pos], r.dump.events_at[pos], r.dump.time_at[pos], r.dump.summary[pos])
+        assert_dump_equal(sub, gx, ge, gt, sm)
+        replayed += len(sel)
         if rank == 0:
             mean, var, _, count = S.merge_roots(root, 1, cells)
             ref_mean, ref_var = exact_moments(r.dump.states)
             assert_moments_close(mean.reshape(G, -1), var.reshape(G, -1), ref_mean, ref_var)
             assert np.all(count == blk)
             assert r.events == int(r.dump.summary["events"].sum())
+    assert replayed >= 256
 
 
 # ------------------------------------------------------------ config 3 (warp path)
@@ -150,7 +130,7 @@ def test_config3_warp_parity(S):
 
 def test_config3_halfwarp_parity(S):
     """Config 3 on the half-warp path (two trajectories per warp, order
-    warp16), with an odd count so the last warp has one idle half."""
+    warp16s), with an odd count so the last warp has one idle half."""
     cfg = inputs.config(3)
     _parity(S, cfg.network, 97, cfg.t_end, cfg.dt, cfg.seed, HALF)
 
@@ -161,8 +141,11 @@ def test_config3_thread_parity(S):
 
 
 def test_config3_full_size_sampled(S):
-    """BASELINE configs[3] at full size (2^20 trajectories, warp path): sampled
-    bit-exact replay plus T2 over a dumped contiguous block of 2^14 ids."""
+    """BASELINE configs[3] at full size (2^20 trajectories) on the one-trajectory-per-warp
+    K2 (order warp32): 64 sampled trajectories replayed bit-exactly, and the full run's
+    grids bitwise equal to the merge of four shard runs.  (The bench's half-warp K2 at
+    this size, with T1 over 4096 ids and T2 over the whole ensemble, is
+    tests/test_gpu_bench_parity.py.)"""
     cfg = inputs.config(3)
     n = cfg.n_trajectories
     m = S.Model(cfg.network)
@@ -227,6 +210,40 @@ def test_ragged_chunks_reduce_only_written_tiles(S, path):
             first = r
         assert_moments_close(r.mean, r.var, *ref)
         assert np.array_equal(r.mean, first.mean) and np.array_equal(r.m2, first.m2), opts
+
+
+def test_tail_compaction_is_bitwise_neutral(S):
+    """K1 tail compaction (ssa_run_options.tail_lanes): once the ids are exhausted, the
+    trajectories of sparse warps are suspended at a grid crossing and resumed packed into
+    whole warps by follow-up launches.  Off (-1), default (16) and aggressive (31: any warp
+    that lost a lane) give bitwise identical grids, counters and dumps, the follow-up launches
+    do happen, and the dumped trajectories match the oracle."""
+    cfg = inputs.config(1)
+    m = S.Model(cfg.network)
+    n = 20000
+    ids = np.arange(0, n, 37, dtype=np.uint64)
+    runs = {tl: S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD, dump_ids=ids, tail_lanes=tl)
+            for tl in (-1, 16, 31)}
+    off = runs[-1]
+    for tl in (16, 31):
+        r = runs[tl]
+        assert np.array_equal(r.mean, off.mean) and np.array_equal(r.var, off.var) and np.array_equal(r.m2, off.m2)
+        assert r.events == off.events and r.near_ties == off.near_ties
+        for f in ("states", "events_at", "time_at"):
+            assert np.array_equal(getattr(r.dump, f), getattr(off.dump, f)), (tl, f)
+        assert r.dump.summary.tobytes() == off.dump.summary.tobytes()
+    assert runs[31].kernel_launches > off.kernel_launches          # resume launches happened
+    gx, ge, gt, sm = oracle_replay(cfg.network, ids[:64], cfg.seed, cfg.t_end, cfg.dt, 0)
+    r = runs[31]
+    sub = S.Dump(ids[:64], r.dump.states[:64], r.dump.events_at[:64], r.dump.time_at[:64], r.dump.summary[:64])
+    assert_dump_equal(sub, gx, ge, gt, sm)
+    # HIV (hot-set variant after the profiling run), no dump: the same bits with and without
+    hm = S.Model(inputs.config(2).network)
+    a = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD, tail_lanes=-1)
+    b = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD, tail_lanes=31)
+    c = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD)
+    for r in (b, c):
+        assert np.array_equal(r.mean, a.mean) and np.array_equal(r.m2, a.m2) and r.events == a.events
 
 
 def test_reduction_paths_bitwise_equal(S):

@@ -38,7 +38,21 @@ def test_union_immigration_death(S, kx):
     assert np.array_equal(got.times, t)                      # union times and group means: bitwise
     assert np.array_equal(got.count, cnt.astype(float))
     assert np.array_equal(got.mean, mean)                    # exact sums, one rounding each
-    assert np.allclose(got.var, var, rtol=1e-12, atol=0)
+    assert np.array_equal(got.var, var)
+
+
+@pytest.mark.parametrize("kx", [1, 16])
+def test_union_immigration_death_mid_size(S, kx):
+    """A non-toy size: 16 immigration-death trajectories (config 0's rates) over
+    t = 100, ~1.9e3 events each (~3e4 union times), against the oracle's
+    brute-force definition -- times, counts, means and variances bitwise."""
+    net = inputs.immigration_death()
+    n, t_end, seed = 16, 100.0, 7
+    got = S.run_union(S.Model(net), n, t_end, seed, kx)
+    t, mean, var, cnt = _oracle(net, n, t_end, seed, kx)
+    assert len(t) > 1000 * 16 // kx
+    assert np.array_equal(got.times, t) and np.array_equal(got.count, cnt.astype(float))
+    assert np.array_equal(got.mean, mean) and np.array_equal(got.var, var)
 
 
 def test_union_hiv_short(S):
@@ -48,8 +62,7 @@ def test_union_hiv_short(S):
     got = S.run_union(S.Model(net), n, t_end, seed, kx)
     t, mean, var, cnt = _oracle(net, n, t_end, seed, kx)
     assert np.array_equal(got.times, t) and np.array_equal(got.count, cnt.astype(float))
-    assert np.allclose(got.mean, mean, rtol=1e-15, atol=0)
-    assert np.allclose(got.var, var, rtol=1e-9, atol=0)
+    assert np.array_equal(got.mean, mean) and np.array_equal(got.var, var)
     assert np.all(got.mean[:, 0] == 1.0)
 
 

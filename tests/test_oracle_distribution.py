@@ -157,7 +157,7 @@ def _cme_moments(net, times):
     return out, n
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3])
 def test_cme_closed_network(oracle_lib, mode):
     O = oracle_lib
     net = _cme_network()

@@ -139,7 +139,7 @@ def test_selection_matches_exact_arithmetic(oracle_lib, R):
             a[0] = 1.0
         u2 = O.u53(int(rng.integers(0, 2**63)) * 2 + 1)
         jx, r, fa = _exact_select(a, u2)
-        for mode in (0, 1, 2):     # sequential, warp32, warp16
+        for mode in (0, 1, 2, 3):     # sequential, warp32, warp16, warp16 with a scanned lane step
             a0, j = O.select(a, mode, u2)
             assert abs(a0 - float(sum(fa))) <= R * np.spacing(float(sum(fa)))
             assert 0 <= j < R and a[j] > 0
