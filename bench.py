@@ -692,6 +692,7 @@ def main():
                       "note": "K1's dump variant writes each dumped trajectory's grid states, event counts and "
                               "last-event times while it simulates; the library copies them to the host after "
                               "the run (d2h_ms, CUDA events)"}
+    cpu = None
     if not args.no_cpu_baseline and world == 1:
         cores = host_cores()
         n_cpu = 3 * max(cores, 8)

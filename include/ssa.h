@@ -168,7 +168,7 @@ typedef struct {
     int32_t tail_lanes;            /* thread path, end of a launch: once no ids are left, the trajectories of a
                                       warp with at most this many live lanes are suspended at their next grid
                                       point and resumed packed into whole warps by a follow-up launch (tail
-                                      compaction); 0 = default (16), -1 = off.  Speed only: results are
+                                      compaction); 0 = default (off), -1 = off.  Speed only: results are
                                       bitwise the same for every value. */
 } ssa_run_options;
 

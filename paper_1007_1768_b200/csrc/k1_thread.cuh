@@ -67,15 +67,13 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     const double* kp = s_k;
 #endif
 #if SSA_K1_MIG
-    // tail compaction (P.mig_thresh > 0): live lanes per warp, and whether some lane of
-    // this block has found the launch's ids exhausted
+    // tail compaction (P.mig_thresh > 0): live lanes per warp
     __shared__ int s_wlive[SSA_K1_BLOCK / 32];
-    __shared__ int s_dry;
-    const int wid = threadIdx.x >> 5;
+    const int wid = threadIdx.x >> 5, wl = threadIdx.x & 31;
     const double s_last = __dmul_rn((double)K, dt);   // s_K: a crossing past it ends the trajectory
     bool may_suspend = true;                          // a resumed lane first crosses its pending grid point
-    if (threadIdx.x == 0) s_dry = 0;
-    __syncthreads();
+    const bool mig = P.mig_thresh > 0 && !P.spread;
+    volatile ssa_u64* const mctl = P.mig_ctl;
 #endif
     // small ensembles (spread launch): one working lane per warp and one warp
     // per block, so each trajectory has an SM sub-partition to itself
@@ -121,43 +119,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             kp = s_k + ptl * (ssa_u64)P.n_pool;
         }
 #else
-#if SSA_K1_MIG
-        if (P.mig_in) {
-            // resume a trajectory a sparse warp of the previous launch suspended
-            const ssa_u64 q = atomicAdd(P.mig_in_take, 1ull);
-            if (q < P.mig_in_n) {
-                const double* st = P.mig_in + q * (ssa_u64)(SSA_S + 6);
-#pragma unroll
-                for (int s = 0; s < SSA_S; ++s) x[s] = st[s];
-                t = st[SSA_S];
-                e = (ssa_u64)__double_as_longlong(st[SSA_S + 1]);
-                k = __double_as_longlong(st[SSA_S + 2]);
-                rel = (ssa_u64)__double_as_longlong(st[SSA_S + 3]);
-                hash = (ssa_u64)__double_as_longlong(st[SSA_S + 4]);
-                ties = (ssa_u64)__double_as_longlong(st[SSA_S + 5]);
-                vid = P.id_begin + rel;
-                id = vid;
-#if SSA_K1_DUMP
-                slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
-#endif
-                ssa_khat(x, kh SSA_KP_ARG);
-                s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
-                status = 0; absorbed = 0; err_r = -1;
-                may_suspend = false;
-#if SSA_CSKIP
-                lo_dirty = true;
-#endif
-                return true;
-            }
-        }
-#endif
         rel = atomicAdd(P.work, 1ull);
-        if (rel >= P.n_ids) {
-#if SSA_K1_MIG
-            *(volatile int*)&s_dry = 1;
-#endif
-            return false;
-        }
+        if (rel >= P.n_ids) return false;
 #endif
         vid = P.id_begin + rel;
 #if !SSA_K1_SWEEP
@@ -204,16 +167,84 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         rec_last_t = tp;
     };
 #endif
+#if SSA_K1_MIG
+    // suspended trajectory slot q: (x[S], t, e, k, rel, hash, ties) as S + 6 doubles
+    auto mig_restore = [&](ssa_u64 q) {
+        while (((volatile unsigned*)P.mig_ready)[q] == 0u) __nanosleep(32);   // the pusher has reserved it
+        __threadfence();
+        const double* st = P.mig_buf + q * (ssa_u64)(SSA_S + 6);
+#pragma unroll
+        for (int s = 0; s < SSA_S; ++s) x[s] = __ldcg(st + s);     // L2: written by another SM
+        t = __ldcg(st + SSA_S);
+        e = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 1));
+        k = __double_as_longlong(__ldcg(st + SSA_S + 2));
+        rel = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 3));
+        hash = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 4));
+        ties = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 5));
+        vid = P.id_begin + rel;
+        id = vid;
+#if SSA_K1_DUMP
+        slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
+#endif
+        ssa_khat(x, kh SSA_KP_ARG);
+        s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+        status = 0; absorbed = 0; err_r = -1;
+        may_suspend = false;
+#if SSA_CSKIP
+        lo_dirty = true;
+#endif
+    };
+    // push this lane's trajectory (false: the buffer is full)
+    auto mig_push = [&]() -> bool {
+        ssa_u64 pt = mctl[0];
+        for (;;) {
+            if (pt >= P.mig_cap) return false;
+            const ssa_u64 o = atomicCAS((ssa_u64*)&P.mig_ctl[0], pt, pt + 1);
+            if (o == pt) break;
+            pt = o;
+        }
+        double* st = P.mig_buf + pt * (ssa_u64)(SSA_S + 6);
+#pragma unroll
+        for (int s = 0; s < SSA_S; ++s) __stcg(st + s, x[s]);
+        __stcg(st + SSA_S, t);
+        __stcg(st + SSA_S + 1, __longlong_as_double((long long)e));
+        __stcg(st + SSA_S + 2, __longlong_as_double(k));
+        __stcg(st + SSA_S + 3, __longlong_as_double((long long)rel));
+        __stcg(st + SSA_S + 4, __longlong_as_double((long long)hash));
+        __stcg(st + SSA_S + 5, __longlong_as_double((long long)ties));
+        __threadfence();
+        atomicExch(&P.mig_ready[pt], 1u);
+        return true;
+    };
+    // take one suspended trajectory (false: none)
+    auto mig_pop1 = [&]() -> bool {
+        ssa_u64 pb = mctl[1];
+        for (;;) {
+            if (pb >= mctl[0]) return false;
+            const ssa_u64 o = atomicCAS((ssa_u64*)&P.mig_ctl[1], pb, pb + 1);
+            if (o == pb) break;
+            pb = o;
+        }
+        mig_restore(pb);
+        return true;
+    };
+#endif
     bool live = start();
 #if SSA_K1_RECORD == 2
     if (live) { rec_left = P.rec_stride; rec_point(0, 0.0); }
 #endif
 #if SSA_K1_MIG
-    if (!P.spread) {
+    bool running = false;      // this warp is counted in mig_ctl[3] (warp-uniform)
+    if (mig) {
         const unsigned b = __ballot_sync(0xffffffffu, live);
-        if ((threadIdx.x & 31) == 0) s_wlive[wid] = __popc(b);
+        if (wl == 0) {
+            s_wlive[wid] = __popc(b);
+            if (b) atomicAdd((ssa_u64*)&P.mig_ctl[3], 1ull);
+        }
+        running = b != 0;
         __syncwarp();
     }
+    for (;;) {
 #endif
     while (live) {
         // a2: one Philox block per candidate event, counter (e, id)
@@ -266,22 +297,12 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         if (!fast || tn > s_next) {
             // ---------------- rare path: a5 edge cases, a6, end + refill
 #if SSA_K1_MIG
-            // tail compaction: no ids left and this warp is sparse -- suspend before
-            // this grid crossing (the candidate is a function of (x, t, e), so the
-            // resumed lane recomputes it bit for bit) and leave the warp
-            if (P.mig_thresh && may_suspend && status == 0 && fast && tn <= s_last &&
-                *(volatile int*)&s_wlive[wid] <= P.mig_thresh &&
-                (*(volatile int*)&s_dry || *(volatile ssa_u64*)P.work >= P.n_ids)) {
-                const ssa_u64 q = atomicAdd(P.mig_out_n, 1ull);
-                double* st = P.mig_out + q * (ssa_u64)(SSA_S + 6);
-#pragma unroll
-                for (int s = 0; s < SSA_S; ++s) st[s] = x[s];
-                st[SSA_S] = t;
-                st[SSA_S + 1] = __longlong_as_double((long long)e);
-                st[SSA_S + 2] = __longlong_as_double(k);
-                st[SSA_S + 3] = __longlong_as_double((long long)rel);
-                st[SSA_S + 4] = __longlong_as_double((long long)hash);
-                st[SSA_S + 5] = __longlong_as_double((long long)ties);
+            // tail compaction: no ids left, this warp is sparse and another warp runs --
+            // suspend before this grid crossing (the candidate is a function of (x, t, e),
+            // so the resumed lane recomputes it bit for bit) and leave the warp
+            if (mig && may_suspend && status == 0 && fast && tn <= s_last &&
+                *(volatile int*)&s_wlive[wid] <= P.mig_thresh && *(volatile ssa_u64*)P.work >= P.n_ids &&
+                mctl[3] > 1 && mig_push()) {
                 atomicSub(&s_wlive[wid], 1);
                 live = false;
                 continue;
@@ -363,9 +384,14 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     if (rec_last_t < hz) rec_point(2 * e + 1, hz);
                 }
 #endif
+#if SSA_K1_MIG
+                if (mig) atomicAdd((ssa_u64*)&P.mig_ctl[2], ~0ull);   // one trajectory fewer to finish
+#endif
                 live = start();
 #if SSA_K1_MIG
-                if (!live && !P.spread) atomicSub(&s_wlive[wid], 1);
+                // no ids left: a lane of a dense warp takes a suspended trajectory
+                if (!live && mig && *(volatile int*)&s_wlive[wid] > P.mig_thresh) live = mig_pop1();
+                if (!live && mig) atomicSub(&s_wlive[wid], 1);
 #endif
 #if SSA_K1_RECORD == 2
                 if (live) { rec_left = P.rec_stride; rec_point(0, 0.0); }
@@ -406,6 +432,52 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         }
 #endif
     }
+#if SSA_K1_MIG
+        // every lane of this warp is idle: take up to 32 suspended trajectories at once
+        // (a full warp's worth, or what is left once no warp runs), or stop when every
+        // trajectory of the launch has finished
+        if (!mig) break;
+        __syncwarp();
+        if (running && wl == 0) atomicAdd((ssa_u64*)&P.mig_ctl[3], ~0ull);
+        running = false;
+        long long got = 0;
+        ssa_u64 base = 0;
+        ssa_u64 seen = ~0ull, since = 0;   // safety: stop after 30 s without any progress of the launch
+        for (;;) {
+            if (wl == 0) {
+                got = 0;
+                const ssa_u64 pt = mctl[0], pb = mctl[1];
+                const ssa_u64 avail = pt > pb ? pt - pb : 0;
+                if (avail >= 32 || (avail > 0 && mctl[3] == 0)) {
+                    const ssa_u64 n = avail < 32 ? avail : 32;
+                    if (atomicCAS((ssa_u64*)&P.mig_ctl[1], pb, pb + n) == pb) {
+                        base = pb;
+                        got = (long long)n;
+                        atomicAdd((ssa_u64*)&P.mig_ctl[3], 1ull);
+                        s_wlive[wid] = (int)n;
+                    }
+                } else if (mctl[2] == 0) {
+                    got = -1;                   // every trajectory has finished
+                } else {
+                    ssa_u64 now;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                    const ssa_u64 prog = mctl[2] * 0x9E3779B97F4A7C15ull + pt * 31 + pb;
+                    if (prog != seen) { seen = prog; since = now; }
+                    else if (now - since > 30000000000ull) got = -1;   // the host reports what is left
+                }
+            }
+            got = __shfl_sync(0xffffffffu, got, 0);
+            if (got != 0) break;
+            __nanosleep(2000);
+        }
+        if (got < 0) break;
+        base = __shfl_sync(0xffffffffu, base, 0);
+        running = true;
+        __syncwarp();
+        live = (long long)wl < got;
+        if (live) mig_restore(base + (ssa_u64)wl);
+    }
+#endif
 #if SSA_K1_RECORD
     // unused reserved rows sort last: time +inf
     for (; rec_cur < rec_end; ++rec_cur)

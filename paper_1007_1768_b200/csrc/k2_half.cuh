@@ -4,23 +4,32 @@
 // generated section defines SSA_K2_HALF = 1.
 //
 // Order "warp16s" (R13; oracle mode 3): lane l of the half owns
-// the P = ceil(R/16) contiguous reactions l*P + q; lane sums from 0.0, then an
-// inclusive Hillis-Steele scan over the 16 lanes (offsets 1, 2, 4, 8; the
-// shuffles are segmented with width 16), a0 = v_15, lane* = min{l : v_l > r}.
-// The step inside lane* is a second 16-position Hillis-Steele scan over
-// lane*'s propensities, one per lane of the half (lane q reads lane*'s q-th
-// reaction), p_q = v_{lane*-1} + s_q, j* = lane*'s first q with p_q > r -- a
-// ballot instead of every lane re-summing its P propensities sequentially.
+// the P = ceil(R/16) contiguous reactions l*P + q; lane sums from 0.0 in q
+// order, then an inclusive Hillis-Steele scan over the 16 lanes (offsets 1, 2,
+// 4, 8; the shuffles are segmented with width 16), a0 = v_15, lane* = min{l :
+// v_l > r}.  The step inside lane* is a second 16-position Hillis-Steele scan
+// over lane*'s propensities, one per lane of the half (lane q reads lane*'s
+// q-th reaction), p_q = v_{lane*-1} + s_q, j* = lane*'s first q with p_q > r --
+// a ballot instead of every lane re-summing its P propensities sequentially.
 // Per warp the scans, the broadcasts, the division and the update/recompute
 // passes serve two events.
 //
-// Shared memory per half: x[S] and the propensities a[q*17 + l] (reaction
-// l*P + q; row stride 17 doubles, so both the lane sums -- fixed q, l = 0..15 --
-// and the lane* scan -- fixed l, q = 0..15 -- are bank-conflict free).  Per
-// block: the model's per-reaction record {nu begin, nu end, dep begin, dep
-// end} (one 16-byte load once j* is known) and the dependency entries
-// pre-resolved to (reactant species and coefficients, propensity slot,
-// reaction) so that the recompute of dep(j*) reads x and the rate directly.
+// Shared memory per half (16-byte aligned window): the propensities a[l*18 + q]
+// (reaction l*P + q; row stride 18 doubles: the lane sums read their row two
+// doubles at a time with 2 wavefronts per half, the lane* scan reads one row
+// with 1) and then x[S].  Per block: the model's per-reaction record {nu begin,
+// nu end, dep begin, dep end} (one 16-byte load once j* is known) and the
+// dependency entries pre-resolved to (reactant species and coefficients,
+// propensity slot, reaction), so the recompute of dep(j*) reads x and the rate
+// directly.  The shared-memory addresses are computed once and kept opaque:
+// otherwise the compiler re-derives the shared window base (S2R of the CTA id
+// + LEA) inside the event loop.
+//
+// Random numbers: each lane of a half holds (E, u2) of event base + lane for
+// 16 events.  Both halves refill at the same iteration (when either has used
+// its 16): they then stay in step, so the Philox + plog pass -- a divergent
+// branch when only one half takes it -- runs once per 16 iterations, not twice.
+// A half's early refill re-draws the same counter-based values.
 //
 // Both halves execute the common path in lockstep (the shuffles are
 // full-warp); rare paths (grid crossing, end of a trajectory, refill, the
@@ -30,8 +39,10 @@
 
 #if SSA_K2_HALF
 #define SSA_HL 16
-#define SSA_AS 17                            // row stride of a[] (doubles)
+#define SSA_AR 18                            // row stride of a[] (doubles)
+#define SSA_AWIN (SSA_HL * SSA_AR + ((SSA_S + 1) & ~1))   // per-half window (doubles, even)
 
+#if !SSA_HAS_M3
 // dependency entry: sa | sb << 14 | ma << 28 | mb << 30 | slot << 32 | reaction << 48
 static __device__ __forceinline__ double k2h_propensity(ssa_u64 de, const k2_rxd* __restrict__ rxd,
                                                         const double* __restrict__ x)
@@ -50,14 +61,34 @@ static __device__ __forceinline__ double k2h_propensity(ssa_u64 de, const k2_rxd
     return k2_gated(__dmul_rn(rxd[rxi].rate, h), rxd[rxi].gw, x);
 #endif
 }
+#endif
+
+// one inclusive-scan step over the half with a precomputed mask (hi word 0x3ff00000 where the
+// source lane exists, 0 where it does not): v <- fma(y, m, v), fma(y, 1, v) = fl(y + v)
+static __device__ __forceinline__ double ssa_scan_step_m(double v, int o, unsigned mh)
+{
+    asm("{\n\t.reg .b32 lo, hi, z;\n\t.reg .f64 y, m;\n\t"
+        "mov.b64 {lo, hi}, %0;\n\t"
+        "shfl.sync.up.b32 lo, lo, %1, 0x1000, -1;\n\t"
+        "shfl.sync.up.b32 hi, hi, %1, 0x1000, -1;\n\t"
+        "mov.b64 y, {lo, hi};\n\t"
+        "mov.b32 z, 0;\n\t"
+        "mov.b64 m, {z, %2};\n\t"
+        "fma.rn.f64 %0, y, m, %0;\n\t}"
+        : "+d"(v) : "r"(o), "r"(mh));
+    return v;
+}
+
+template <class T> static __device__ __forceinline__ T* k2h_opaque(T* p)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(p);
+    asm volatile("" : "+r"(s));
+    return (T*)__cvta_shared_to_generic(s);
+}
 
 extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(const ssa_k2_params P)
 {
     extern __shared__ __align__(16) unsigned char k2_smem_raw[];
-    // The lane index and the shared-memory window address of this half's state
-    // are computed once and kept opaque (asm volatile): otherwise, at this
-    // register budget, the compiler re-derives them (S2R of TID / CgaCtaId,
-    // tens of cycles of latency) inside the event loop.
     int lane_ = threadIdx.x & 31;
     asm volatile("" : "+r"(lane_));
     const int lane = lane_;
@@ -66,54 +97,61 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     const int hl = lane & 15;                // lane within the half
     const unsigned FULL = 0xffffffffu;
     const unsigned HALF = 0xFFFFu << (16 * h);
-    // shared: rx[R] | x0[S] | per warp, per half (x[S] | a[P*17]) | rec[R] | nu_ent | dent | rxd
+    // shared: rx[R] | x0[S] | (16-aligned) per warp, per half (a[16*18] | x[S]) | rec[R] | nu_ent | dent | rxd
     // the packed table rx is needed only by the general evaluator (coefficient-3 models)
     k2_rx* rx = (k2_rx*)k2_smem_raw;
     double* x0 = (double*)(rx + (SSA_HAS_M3 ? SSA_R : 0));
-    double* x = x0 + SSA_S + (size_t)warp * 2 * (SSA_S + SSA_AS * SSA_P) + (size_t)h * (SSA_S + SSA_AS * SSA_P);
+    double* win0 = (double*)(((unsigned long long)(x0 + SSA_S) + 15ull) & ~15ull);
+    double* a = k2h_opaque(win0 + ((size_t)warp * 2 + h) * SSA_AWIN);   // a[l*18 + q]: reaction l*P + q
+    double* x = k2h_opaque(win0 + ((size_t)warp * 2 + h) * SSA_AWIN + SSA_HL * SSA_AR);
+    const int4* rec = k2h_opaque((const int4*)(k2_smem_raw + P.rec_offset));   // {nu b, nu e, dep b, dep e}
+    const int* nu_ent = k2h_opaque((const int*)(k2_smem_raw + P.rec_offset + 16 * SSA_R));
+    const ssa_u64* dent = k2h_opaque((const ssa_u64*)(k2_smem_raw + P.dent_offset));
+#if !SSA_HAS_M3
+    const k2_rxd* rxd = k2h_opaque((const k2_rxd*)(k2_smem_raw + P.rxd_offset));
+#endif
     {
-        unsigned xs = (unsigned)__cvta_generic_to_shared(x);
-        asm volatile("" : "+r"(xs));
-        x = (double*)__cvta_shared_to_generic(xs);
-    }
-    double* a = x + SSA_S;                                     // a[q*17 + l]: reaction l*P + q
-    int4* rec = (int4*)(k2_smem_raw + P.rec_offset);          // {nu begin, nu end, dep begin, dep end}
-    int* nu_ent = (int*)(rec + SSA_R);
-    ssa_u64* dent = (ssa_u64*)(k2_smem_raw + P.dent_offset);
-#if !SSA_HAS_M3
-    k2_rxd* rxd = (k2_rxd*)(k2_smem_raw + P.rxd_offset);
-#endif
+        int4* rec_w = (int4*)(k2_smem_raw + P.rec_offset);
+        int* nu_w = (int*)(k2_smem_raw + P.rec_offset + 16 * SSA_R);
+        ssa_u64* dent_w = (ssa_u64*)(k2_smem_raw + P.dent_offset);
 #if SSA_HAS_M3
-    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
-        k2_rx q;
-        q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i]; q.gw = P.gw[i];
-        rx[i] = q;
-    }
+        for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
+            k2_rx q;
+            q.pk = P.pk[i]; q.rate = P.rate[i]; q.modc = P.modc[i]; q.gw = P.gw[i];
+            rx[i] = q;
+        }
 #else
-    (void)rx;
+        (void)rx;
 #endif
-    for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
-    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) rec[i] = P.rec[i];
-    for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_ent[i] = P.nu_ent[i];
-    for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dent[i] = P.dent[i];
+        for (int i = threadIdx.x; i < SSA_S; i += SSA_K2_BLOCK) x0[i] = P.x0[i];
+        for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) rec_w[i] = P.rec[i];
+        for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_w[i] = P.nu_ent[i];
+        for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dent_w[i] = P.dent[i];
 #if !SSA_HAS_M3
-    for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
-        const ssa_u64 pk = P.pk[i];
-        const int n = (int)(pk & 3ull);
-        const int ms = (int)(pk >> 50);
-        k2_rxd d;
-        d.rate = P.rate[i];
-        d.modc = (ms != 0x3FFF) ? P.modc[i] : 0.0;
-        const int sa = n >= 1 ? (int)((pk >> 2) & 0x3FFF) : 0, sb = n >= 2 ? (int)((pk >> 18) & 0x3FFF) : 0;
-        const int ma = n >= 1 ? (int)((pk >> 16) & 3) : 0, mb = n >= 2 ? (int)((pk >> 32) & 3) : 0;
-        d.sab = sa | (sb << 16);
-        d.sms = (ms != 0x3FFF ? ms : 0);
-        d.mab = ma | (mb << 8);
-        d.pad = 0;
-        d.gw = P.gw[i];
-        rxd[i] = d;
-    }
+        k2_rxd* rxd_w = (k2_rxd*)(k2_smem_raw + P.rxd_offset);
+        for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
+            const ssa_u64 pk = P.pk[i];
+            const int n = (int)(pk & 3ull);
+            const int ms = (int)(pk >> 50);
+            k2_rxd d;
+            d.rate = P.rate[i];
+            d.modc = (ms != 0x3FFF) ? P.modc[i] : 0.0;
+            const int sa = n >= 1 ? (int)((pk >> 2) & 0x3FFF) : 0, sb = n >= 2 ? (int)((pk >> 18) & 0x3FFF) : 0;
+            const int ma = n >= 1 ? (int)((pk >> 16) & 3) : 0, mb = n >= 2 ? (int)((pk >> 32) & 3) : 0;
+            d.sab = sa | (sb << 16);
+            d.sms = (ms != 0x3FFF ? ms : 0);
+            d.mab = ma | (mb << 8);
+            d.pad = 0;
+            d.gw = P.gw[i];
+            rxd_w[i] = d;
+        }
 #endif
+        // the padding entries of every propensity row stay 0
+        for (int i = threadIdx.x; i < SSA_K2_WARPS * 2 * SSA_HL * SSA_AR; i += SSA_K2_BLOCK) {
+            const int w = i / (SSA_HL * SSA_AR), o = i - w * (SSA_HL * SSA_AR);
+            win0[(size_t)w * SSA_AWIN + o] = 0.0;
+        }
+    }
     __syncthreads();
 
     const double INF = __longlong_as_double(0x7FF0000000000000ll);
@@ -121,10 +159,14 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     const long long K = P.K;
     const ssa_u64 G = (ssa_u64)K + 1;
     ssa_u64 my_events = 0, my_ties = 0;
+    // scan masks: the source lane hl - o exists
+    const unsigned mk1 = hl >= 1 ? 0x3ff00000u : 0u, mk2 = hl >= 2 ? 0x3ff00000u : 0u;
+    const unsigned mk4 = hl >= 4 ? 0x3ff00000u : 0u, mk8 = hl >= 8 ? 0x3ff00000u : 0u;
+    const bool in_row = hl < SSA_P;          // this lane holds a position of lane*'s row
 
     // per-half trajectory state (uniform within the half)
     bool live = false;
-    ssa_u64 rel = 0, id = 0, e = 0, ties = 0;
+    ssa_u64 rel = 0, id = 0, e = 0, ties = 0, ebase = 0;
     double t = 0.0, s_next = 0.0;
     long long k = 0;
     int status = 0, absorbed = 0, err_r = -1;
@@ -132,7 +174,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     long long slot = -1;
     ssa_u64 hash = SSA_FNV_OFFSET;
 #endif
-    double Ec = 0.0, U2c = 0.0;
+    double Ec = 0.0, U2c = 0.0;              // (E, u2) of event ebase + hl
+    bool need_rng = true;                    // this half's buffer is used up (or a new trajectory)
 
     // a1 for this half: take the next id and initialise (half-warp collective)
     auto start = [&]() {
@@ -151,36 +194,44 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         for (int q = 0; q < SSA_P; ++q) {
             const int j = hl * SSA_P + q;
 #if SSA_HAS_M3
-            a[q * SSA_AS + hl] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+            a[hl * SSA_AR + q] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
 #else
-            a[q * SSA_AS + hl] = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
+            a[hl * SSA_AR + q] = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
 #endif
         }
         __syncwarp(HALF);
         t = 0.0; s_next = 0.0; e = 0; ties = 0; k = 0;
         status = 0; absorbed = 0; err_r = -1;
+        need_rng = true;
     };
     start();
 
     while (__any_sync(FULL, live)) {
-        // a2, amortised per half: lane l draws event e0 + l for the next 16 events
-        if ((e & 15ull) == 0) {
+        // a2: both halves refill their 16-event buffers together when either needs it
+        if (__any_sync(FULL, need_rng && live)) {
+            ebase = e;
             const ssa_u64 ee = e + (ssa_u64)hl;
             const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)ee, (ssa_u32)(ee >> 32), (ssa_u32)id,
                                                        (ssa_u32)(id >> 32), P.key0, P.key1);
             Ec = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
             U2c = ssa_u53(o.o3, o.o2);
+            need_rng = false;
         }
-        // a4: lane sum, scan over the half (width 16)
+        // a4: lane sum (two propensities per load), scan over the half (width 16)
         double L = 0.0;
 #pragma unroll
-        for (int q = 0; q < SSA_P; ++q) L = __dadd_rn(L, a[q * SSA_AS + hl]);
-        double v = L;
-#pragma unroll
-        for (int o = 1; o < SSA_HL; o <<= 1) v = ssa_scan_step(v, o, 0x1000);     // width 16
+        for (int q = 0; q + 1 < SSA_P; q += 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(a + hl * SSA_AR + q);
+            L = __dadd_rn(__dadd_rn(L, v2.x), v2.y);
+        }
+        if (SSA_P & 1) L = __dadd_rn(L, a[hl * SSA_AR + SSA_P - 1]);
+        double v = ssa_scan_step_m(L, 1, mk1);
+        v = ssa_scan_step_m(v, 2, mk2);
+        v = ssa_scan_step_m(v, 4, mk4);
+        v = ssa_scan_step_m(v, 8, mk8);
         const double a0 = __shfl_sync(FULL, v, SSA_HL - 1, SSA_HL);
         // a5
-        const int src = (int)(e & 15ull);
+        const int src = (int)(e - ebase);
         const double E = __shfl_sync(FULL, Ec, src, SSA_HL);
         const double u2 = __shfl_sync(FULL, U2c, src, SSA_HL);
         const unsigned a0hi = (unsigned)__double2hiint(a0);
@@ -190,16 +241,20 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         // propensity, a second scan gives s_q, p_q = v_{lane*-1} + s_q, q* = min{q : p_q > r}
         const double r = __dmul_rn(u2, a0);
         const unsigned bal = (__ballot_sync(FULL, v > r) >> (16 * h)) & 0xFFFFu;
-        const int ls = bal ? __ffs(bal) - 1 : 0;
-        const double base = __shfl_sync(FULL, v, ls > 0 ? ls - 1 : 0, SSA_HL);
-        double y = (hl < SSA_P && ls * SSA_P + hl < SSA_R) ? a[hl * SSA_AS + ls] : 0.0;
-#pragma unroll
-        for (int o = 1; o < SSA_HL; o <<= 1) y = ssa_scan_step(y, o, 0x1000);
-        const double p = (ls > 0) ? __dadd_rn(base, y) : y;
-        const unsigned bq = (__ballot_sync(FULL, hl < SSA_P && p > r) >> (16 * h)) & 0xFFFFu;
+        const int ls = __ffs(bal | 0x10000u) - 1;          // 16 when none (non-finite a0: rare path)
+        const int lsc = ls & 15;
+        const double base = __shfl_sync(FULL, v, lsc > 0 ? lsc - 1 : 0, SSA_HL);
+        double y = (in_row && lsc * SSA_P + hl < SSA_R) ? a[lsc * SSA_AR + hl] : 0.0;
+        y = ssa_scan_step_m(y, 1, mk1);
+        y = ssa_scan_step_m(y, 2, mk2);
+        y = ssa_scan_step_m(y, 4, mk4);
+        y = ssa_scan_step_m(y, 8, mk8);
+        const double p = (lsc > 0) ? __dadd_rn(base, y) : y;
+        const unsigned bq = (__ballot_sync(FULL, in_row && p > r) >> (16 * h)) & 0xFFFFu;
+        int j = lsc * SSA_P + (__ffs(bq) - 1);
 
         bool apply = live;
-        if (live && (!fast || tn > s_next)) {     // rare path of this half
+        if (live && (!fast || tn > s_next || bq == 0)) {     // rare path of this half
             bool fin = false;
             if (!fast) {
                 if (a0 > 0.0 && a0 < INF) {
@@ -212,7 +267,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                     int bad = SSA_R;
 #pragma unroll
                     for (int q = SSA_P - 1; q >= 0; --q)
-                        if (hl * SSA_P + q < SSA_R && !(fabs(a[q * SSA_AS + hl]) < INF)) bad = hl * SSA_P + q;
+                        if (hl * SSA_P + q < SSA_R && !(fabs(a[hl * SSA_AR + q]) < INF)) bad = hl * SSA_P + q;
 #pragma unroll
                     for (int o = 8; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(HALF, bad, o, SSA_HL));
                     err_r = bad < SSA_R ? bad : -1;
@@ -270,25 +325,20 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                 }
                 start();
                 apply = false;
-            }
-        }
-        // Both halves run the update and the recompute loops (a half that does not
-        // apply an event has empty ranges), so the two syncs are full-warp ones: a
-        // half mask compiles to a convergence check (MATCH/REDUX/VOTE) per sync.
-        {
-            int j = 0;
-            if (!apply) {
-            } else if (bq) {
-                j = ls * SSA_P + (__ffs(bq) - 1);
-            } else {
-                // rounding fallback (rare): the largest j <= lane*'s last index with a_j > 0
+            } else if (bq == 0) {
+                // rounding fallback: the largest j <= lane*'s last index with a_j > 0
                 int lp = -1;
 #pragma unroll
                 for (int q = 0; q < SSA_P; ++q)
-                    if (hl * SSA_P + q < SSA_R && a[q * SSA_AS + hl] > 0.0) lp = hl * SSA_P + q;
-                const unsigned m2 = (__ballot_sync(HALF, lp >= 0 && hl <= ls) >> (16 * h)) & 0xFFFFu;
+                    if (hl * SSA_P + q < SSA_R && a[hl * SSA_AR + q] > 0.0) lp = hl * SSA_P + q;
+                const unsigned m2 = (__ballot_sync(HALF, lp >= 0 && hl <= lsc) >> (16 * h)) & 0xFFFFu;
                 j = __shfl_sync(HALF, lp, 31 - __clz(m2), SSA_HL);
             }
+        }
+        if (!apply) j = 0;
+        // Both halves run the update and the recompute loops (a half that does not
+        // apply an event has empty ranges), so the two syncs are full-warp ones.
+        {
             // a8: state update (lane t of the half takes the t-th net change)
             const int4 rj = rec[j];
             const int nb = apply ? rj.x : 0, ne = apply ? rj.y : 0;
@@ -312,6 +362,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             if (apply) {
                 t = tn;
                 ++e;
+                need_rng = need_rng || (e - ebase >= 16);
 #if SSA_K2_DUMP
                 hash = (hash ^ (ssa_u64)j) * SSA_FNV_PRIME;
 #endif

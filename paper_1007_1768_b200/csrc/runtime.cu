@@ -897,16 +897,21 @@ static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block
     return k2_rxd_offset(S, R, P, n_ent, n_dep, block, half, rx) + 40 * (size_t)R;
 }
 
-// half-warp layout (k2_half.cuh): rx[R] (coefficient-3 models) | x0[S] | per warp, per half
-// (x[S] | a[17 P]) | rec[R] (16 B) | nu_ent | dent[n_dep] (8 B) | rxd[R] (40 B, 16-aligned)
+// half-warp layout (k2_half.cuh): rx[R] (coefficient-3 models) | x0[S] | (16-aligned) per warp, per
+// half (a[16 x 18] | x[S rounded up to even]) | rec[R] (16 B) | nu_ent | dent[n_dep] (8 B) | rxd[R] (40 B,
+// 16-aligned)
 struct K2HalfLayout {
     size_t rec = 0, dent = 0, rxd = 0, bytes = 0;
 };
 static K2HalfLayout k2_half_layout(int S, int R, int P, int n_ent, int n_dep, int block, bool rx)
 {
+    (void)P;
     K2HalfLayout L;
     const size_t warps = (size_t)(block / 32);
-    size_t b = (rx ? 32 * (size_t)R : 0) + 8 * (size_t)S + warps * 2 * 8 * ((size_t)S + 17 * (size_t)P);
+    const size_t awin = 16 * 18 + (((size_t)S + 1) & ~(size_t)1);
+    size_t b = (rx ? 32 * (size_t)R : 0) + 8 * (size_t)S;
+    b = (b + 15) & ~(size_t)15;
+    b += warps * 2 * 8 * awin;
     b = (b + 15) & ~(size_t)15;
     L.rec = b;
     b += 16 * (size_t)R + 4 * (size_t)std::max(n_ent, 1);
@@ -1026,7 +1031,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         const int n_dep_real = (int)dep_ent.size();
         if (dep_ent.empty()) dep_ent.push_back(0);
         // half-warp path: per-reaction records and dependency entries resolved for its
-        // propensity layout a[q*17 + l] (reaction l*PH + q, PH = ceil(R/16))
+        // propensity layout a[l*18 + q] (reaction l*PH + q, PH = ceil(R/16))
         const int PH = std::max(1, (R + 15) / 16);
         std::vector<int4> rec(R1);
         for (int j = 0; j < R; ++j) rec[j] = make_int4(nu_off[j], nu_off[j + 1], dep_off[j], dep_off[j + 1]);
@@ -1037,7 +1042,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
             const int n = (int)(w & 3ull);
             const ssa_u64 sa = n >= 1 ? (w >> 2) & 0x3FFF : 0, sb = n >= 2 ? (w >> 18) & 0x3FFF : 0;
             const ssa_u64 ma = n >= 1 ? (w >> 16) & 3 : 0, mb = n >= 2 ? (w >> 32) & 3 : 0;
-            const ssa_u64 slot = (ssa_u64)((jj % PH) * 17 + jj / PH);
+            const ssa_u64 slot = (ssa_u64)((jj / PH) * 18 + jj % PH);   // a[l*18 + q], reaction l*PH + q
             dent[q] = sa | (sb << 14) | (ma << 28) | (mb << 30) | (slot << 32) | ((ssa_u64)jj << 48);
         }
         // image layout (8-byte aligned sections): pk | gw | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
@@ -1223,7 +1228,6 @@ struct RunInfo {
     uint64_t h2d = 0, d2h = 0, reduce_bytes = 0, dump_bytes = 0;
     int launches = 0;
     uint64_t lanes = 0;   // SSA lanes launched (K1 threads that take trajectories)
-    int tail_passes = 0;  // K1 tail-compaction launches
 };
 
 // Reduce `count` elements per row from `in` down to one, writing the final
@@ -1440,20 +1444,18 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             info.h2d += sizeof(int) * ord.size();
         }
     }
-    // tail compaction (K1 plain / dump / profiling variants, not for small spread ensembles):
-    // two ping-pong buffers of suspended states and their counters
-    const int tail_lanes = (o && o->tail_lanes) ? o->tail_lanes : 16;
+    // tail compaction (K1 plain / dump / profiling variants, not for small spread ensembles): the
+    // suspended-trajectory buffer, its ready flags and the control words
+    const int tail_lanes = (o && o->tail_lanes) ? o->tail_lanes : -1;   // default off
     const bool mig = path == SSA_PATH_THREAD && !sw && !rec && !spread && tail_lanes > 0;
-    DevBuf migb[2], migc;
-    const ssa_u64 mig_rec = (ssa_u64)m->S + 6, mig_cap = (ssa_u64)grid * (ssa_u64)block;
-    ssa_u64* mig_host = nullptr;
+    DevBuf migb, migr, migc;
+    const ssa_u64 mig_rec = (ssa_u64)m->S + 6, mig_cap = 4 * (ssa_u64)grid * (ssa_u64)block;
+    ssa_u64 mig_host[4] = {0, 0, 0, 0};
     if (mig) {
-        CU(migb[0].alloc(sizeof(double) * mig_rec * mig_cap, st));
-        CU(migb[1].alloc(sizeof(double) * mig_rec * mig_cap, st));
+        CU(migb.alloc(sizeof(double) * mig_rec * mig_cap, st));
+        CU(migr.alloc(sizeof(unsigned) * mig_cap, st));
         CU(migc.alloc(sizeof(ssa_u64) * 4, st));
-        CU(cudaMallocHost(&mig_host, sizeof(ssa_u64) * 2));
     }
-    struct PinnedFree { ssa_u64* p; ~PinnedFree() { if (p) cudaFreeHost(p); } } mig_host_guard{mig_host};
     CU(statsb.alloc(sizeof(ssa_dev_stats), st));
     CU(work.alloc(sizeof(ssa_u64) * n_chunks, st));
     CU(cudaMemsetAsync(statsb.p, 0, sizeof(ssa_dev_stats), st));
@@ -1525,33 +1527,31 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             p.spread = spread ? 1 : 0;
             p.prof = prof;
             if (mig) {
-                ssa_u64* cnt = migc.as<ssa_u64>();   // [0] take index of the input, [1] suspended count
+                ssa_u64 ctl[4] = {0, 0, cn, 0};   // pushed, taken, trajectories to finish, warps running
+                CU(cudaMemcpyAsync(migc.p, ctl, sizeof ctl, cudaMemcpyHostToDevice, st));
+                CU(cudaMemsetAsync(migr.p, 0, sizeof(unsigned) * mig_cap, st));
+                CU(cudaStreamSynchronize(st));   // ctl is a local
                 p.mig_thresh = tail_lanes;
-                p.mig_in = nullptr; p.mig_in_n = 0; p.mig_in_take = cnt;
-                p.mig_out = migb[0].as<double>(); p.mig_out_n = cnt + 1;
-                CU(cudaMemsetAsync(cnt, 0, sizeof(ssa_u64) * 2, st));
+                p.mig_buf = migb.as<double>();
+                p.mig_ready = migr.as<unsigned>();
+                p.mig_cap = mig_cap;
+                p.mig_ctl = migc.as<ssa_u64>();
             }
             void* args[] = {&p};
             CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(spread ? 32 : block), args, smem, st));
             info.launches += 1;
             info.lanes = std::max<uint64_t>(info.lanes, (uint64_t)grid * (spread ? 1 : block));
-            // tail compaction: resume the suspended trajectories packed into whole warps,
-            // launch after launch, until none is suspended
-            for (int pass = 0; mig; ++pass) {
-                ssa_u64* cnt = migc.as<ssa_u64>();
-                CU(cudaMemcpyAsync(mig_host, cnt, sizeof(ssa_u64) * 2, cudaMemcpyDeviceToHost, st));
+            if (mig) {
+                CU(cudaMemcpyAsync(mig_host, migc.p, sizeof mig_host, cudaMemcpyDeviceToHost, st));
                 CU(cudaStreamSynchronize(st));
-                const ssa_u64 n_in = mig_host[1];
-                if (n_in == 0) break;
-                if (n_in > mig_cap) return fail(SSA_ERR_CUDA, "tail compaction: %llu suspended > %llu lanes",
-                                                (unsigned long long)n_in, (unsigned long long)mig_cap);
-                p.mig_in = migb[pass & 1].as<double>(); p.mig_in_n = n_in;
-                p.mig_out = migb[(pass + 1) & 1].as<double>();
-                CU(cudaMemsetAsync(cnt, 0, sizeof(ssa_u64) * 2, st));
-                const int g2 = (int)std::min<ssa_u64>((ssa_u64)grid, (n_in + block - 1) / block);
-                CU(cudaLaunchKernel((const void*)k1->fn, dim3(g2), dim3(block), args, smem, st));
-                info.launches += 1;
-                info.tail_passes += 1;
+                if (getenv("SSA_DEBUG_TAIL"))
+                    fprintf(stderr, "[ssa tail] chunk %llu: %llu suspended, %llu resumed, %llu unfinished\n",
+                            (unsigned long long)ch, (unsigned long long)mig_host[0], (unsigned long long)mig_host[1],
+                            (unsigned long long)mig_host[2]);
+                if (mig_host[0] != mig_host[1] || mig_host[2] != 0 || mig_host[3] != 0)
+                    return fail(SSA_ERR_CUDA, "tail compaction: %llu suspended, %llu resumed, %llu unfinished",
+                                (unsigned long long)mig_host[0], (unsigned long long)mig_host[1],
+                                (unsigned long long)mig_host[2]);
             }
         } else {
             ssa_k2_params p{};

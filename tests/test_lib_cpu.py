@@ -103,6 +103,27 @@ def test_k1_nvrtc_compiles_for_sm100a(ssa, netfn):
     assert nbytes > 1000
 
 
+def _trimolecular():
+    from inputs.networks import Network, _rx
+    return Network(("A", "B", "C"), (60, 5, 3), (
+        _rx([(0, 3)], [(1, 1)], 2e-4), _rx([(1, 1)], [(0, 3)], 0.3), _rx([(0, 2)], [(2, 1)], 1e-3),
+        _rx([(2, 1)], [(0, 2)], 0.2), _rx([(1, 1), (2, 1)], [(1, 1)], 0.05, mod=(0, -1e-3))))
+
+
+@pytest.mark.parametrize("netfn", [inputs.immigration_death, inputs.hiv, lambda: inputs.hiv("B"),
+                                   lambda: inputs.synthetic(64, 256, 4), _trimolecular,
+                                   lambda: inputs.empty_network((1, 2))])
+@pytest.mark.parametrize("half", [False, True])
+@pytest.mark.parametrize("dump", [False, True])
+def test_k2_nvrtc_compiles_for_sm100a(ssa, netfn, half, dump):
+    """Both warp-path kernels (one trajectory per warp, two per warp) compile for every
+    model class: coefficient-3 reactants (the general evaluator), modifiers, gates, R = 0."""
+    m = ssa.Model(netfn())
+    st, log, nbytes = m.k2_compile(256, dump, half, 3 if half else 4)
+    assert st == 0, log
+    assert nbytes > 1000
+
+
 def test_compute_fails_loudly_without_device(ssa):
     import torch
     if torch.cuda.is_available():
