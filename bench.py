@@ -64,7 +64,8 @@ def alg_instr_per_event(net, path: int) -> float:
     (DESIGN.md §7): what a minimal implementation of a2-a8 must issue."""
     philox = 40          # 10 rounds x (2 wide multiplies + 2 three-input xors)
     u53 = 6              # 2 x (shift/or + 2 exact adds)
-    plog = 35            # frexp, range fold, 1 divide (~8), 10-term Horner, recombination
+    plog = 21            # bits -> exponent, bucket index and fold (6), 2 table loads, r (1), 5-term Horner,
+                         # r^2 and ln(1+r) (2), e -> double, recombination (4) (DESIGN.md §2, R11)
     tau = 9              # IEEE divide (~8) + add
     props = 0
     for r in net.reactions:
@@ -82,7 +83,7 @@ def alg_instr_per_event(net, path: int) -> float:
 
 def alg_fp64_per_event(net) -> float:
     """Algorithmic FP64-pipe instructions per applied event of the thread path:
-    u53 (1 exact add each) 2, plog (in-range divide 8, Horner 10, recombination and fold 6) 24,
+    u53 (1 exact add each) 2, plog (r 1, Horner 5, r^2 and ln(1+r) 2, recombination 4) 12,
     tau (divide 8 + add) 9, per reaction the factor ops (C(x,2): add + 2 multiplies; C(x,3): 7),
     the products and k*h, prefix R-1 adds, selection R-1 compares, r = u2 a0, the grid compare,
     and the update's count adds (mean |nu_j| over reactions)."""
@@ -100,7 +101,7 @@ def alg_fp64_per_event(net) -> float:
             nu[sp] = nu.get(sp, 0) + m
         upd += sum(1 for v in nu.values() if v != 0)
     upd /= max(R, 1)
-    return 2 + 24 + 9 + props + 2 * max(R - 1, 0) + 1 + 1 + upd
+    return 2 + 12 + 9 + props + 2 * max(R - 1, 0) + 1 + 1 + upd
 
 
 def alg_warp_instr_per_event(net, lanes: int = 32) -> float:
@@ -110,7 +111,7 @@ def alg_warp_instr_per_event(net, lanes: int = 32) -> float:
     Per warp iteration: lane sum (P loads + P adds), log2(lanes)-step scan (2
     shuffles + add), 3 broadcasts, tau (IEEE divide 9 + add), grid check,
     selection, update and dependency recompute (one lane-parallel pass each),
-    Philox + u53 + plog amortised over `lanes` events, loop; divided by the
+    Philox 40 + u53 6 + plog 21 (-3 shared with tau) amortised over `lanes` events, loop; divided by the
     32/lanes trajectories a warp advances per iteration.  Selection: warp32 --
     r, each lane re-sums its P propensities from v_{l-1} with a compare each
     (2P), vprev shuffle, ballot/ffs/broadcast (2P + 5); warp16s -- r, ballot +
@@ -119,7 +120,7 @@ def alg_warp_instr_per_event(net, lanes: int = 32) -> float:
     P = max(1, -(-net.R // lanes))
     steps = 5 if lanes == 32 else 4
     select = (2 * P + 5) if lanes == 32 else (1 + 2 + 2 + 1 + 3 * 4 + 1 + 1 + 2)
-    per_iter = 2 * P + 3 * steps + 6 + 10 + 2 + select + 5 + 15 + 78 / lanes + 3
+    per_iter = 2 * P + 3 * steps + 6 + 10 + 2 + select + 5 + 15 + 64 / lanes + 3
     return per_iter / (32 // lanes)
 
 

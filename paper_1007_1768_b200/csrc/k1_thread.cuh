@@ -75,6 +75,10 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     const bool mig = P.mig_thresh > 0 && !P.spread;
     volatile ssa_u64* const mctl = P.mig_ctl;
 #endif
+    // plog's table in shared memory (lanes index it independently)
+    __shared__ __align__(16) double s_plog[128][4];
+    for (int q = threadIdx.x; q < 128 * 4; q += blockDim.x) (&s_plog[0][0])[q] = (&ssa_plog_tab[0][0])[q];
+    __syncthreads();
     // small ensembles (spread launch): one working lane per warp and one warp
     // per block, so each trajectory has an SM sub-partition to itself
     if (P.spread && (threadIdx.x & 31) != 0) return;
@@ -170,6 +174,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #if SSA_K1_MIG
     // suspended trajectory slot q: (x[S], t, e, k, rel, hash, ties) as S + 6 doubles
     auto mig_restore = [&](ssa_u64 q) {
+        SSA_CHECK(q < P.mig_cap, P.stats);
         while (((volatile unsigned*)P.mig_ready)[q] == 0u) __nanosleep(32);   // the pusher has reserved it
         __threadfence();
         const double* st = P.mig_buf + q * (ssa_u64)(SSA_S + 6);
@@ -283,12 +288,19 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // recomputes the whole propensity chain for the selection (a7)
 #pragma unroll
         for (int q = 0; q < SSA_R - 1; ++q) asm volatile("" : "+d"(c[q]));
+#if SSA_PLOG_DIV
+        const double E = -ssa_plog_div(ssa_u53(o.o1, o.o0), c_plog_div);   // speed A/B only
+#elif SSA_PLOG_GLOBAL
         const double E = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
+#else
+        const double E = -ssa_plog<true>(ssa_u53(o.o1, o.o0), c_plog, s_plog);
+#endif
         // a7, speculatively (used only if the event is applied): r = u2 a0,
         // j* = #{ j : c_j <= r } (c nondecreasing, r < a0), counted in four
         // independent partial sums to shorten the dependency chain.
         const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
         const int j = ssa_count_from<0>(c, r);
+        SSA_CHECK(j >= 0 && j < (SSA_R > 0 ? SSA_R : 1), P.stats);
         // a5: tau = E / a0 by the fast in-range IEEE division (speculative:
         // replaced on the rare path when a0 is outside [2^-900, 2^901))
         const unsigned a0hi = (unsigned)__double2hiint(a0);
@@ -330,6 +342,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
                                       (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
                     ties += near ? 1 : 0;
+                    SSA_CHECK(k <= K && rel < P.n_ids && rel < P.stride, P.stats);
                     int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
 #pragma unroll
                     for (int s = 0; s < SSA_S; ++s) {
@@ -338,6 +351,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     }
 #if SSA_K1_DUMP
                     if (slot >= 0) {
+                        SSA_CHECK((ssa_u64)slot < P.n_dump, P.stats);
                         const ssa_u64 base = (ssa_u64)slot * G + (ssa_u64)k;
 #pragma unroll
                         for (int s = 0; s < SSA_S; ++s) P.dump_states[base * SSA_S + s] = (int)x[s];
@@ -443,12 +457,18 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         long long got = 0;
         ssa_u64 base = 0;
         ssa_u64 seen = ~0ull, since = 0;   // safety: stop after 30 s without any progress of the launch
+        ssa_u64 pending = 0;               // since when suspended trajectories have been waiting (ns)
         for (;;) {
             if (wl == 0) {
                 got = 0;
                 const ssa_u64 pt = mctl[0], pb = mctl[1];
                 const ssa_u64 avail = pt > pb ? pt - pb : 0;
-                if (avail >= 32 || (avail > 0 && mctl[3] == 0)) {
+                ssa_u64 now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                if (avail == 0) pending = 0;
+                else if (pending == 0) pending = now;
+                // a full warp's worth, or whatever is left once no warp runs or it has waited 100 us
+                if (avail >= 32 || (avail > 0 && (mctl[3] == 0 || now - pending > 100000ull))) {
                     const ssa_u64 n = avail < 32 ? avail : 32;
                     if (atomicCAS((ssa_u64*)&P.mig_ctl[1], pb, pb + n) == pb) {
                         base = pb;
@@ -459,8 +479,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 } else if (mctl[2] == 0) {
                     got = -1;                   // every trajectory has finished
                 } else {
-                    ssa_u64 now;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
                     const ssa_u64 prog = mctl[2] * 0x9E3779B97F4A7C15ull + pt * 31 + pb;
                     if (prog != seen) { seen = prog; since = now; }
                     else if (now - since > 30000000000ull) got = -1;   // the host reports what is left

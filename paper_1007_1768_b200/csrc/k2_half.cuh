@@ -284,6 +284,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                     for (int s = hl; s < SSA_S; s += SSA_HL) {
                         const double xv = x[s];
                         ovf |= (xv > 2147483647.0) ? 1 : 0;
+                        SSA_CHECK(k <= K && rel < P.n_ids, P.stats);
                         P.staging[((ssa_u64)k * SSA_S + s) * P.stride + rel] = (int)xv;
 #if SSA_K2_DUMP
                         if (slot >= 0) P.dump_states[((ssa_u64)slot * G + (ssa_u64)k) * SSA_S + s] = (int)xv;
@@ -340,11 +341,15 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         // apply an event has empty ranges), so the two syncs are full-warp ones.
         {
             // a8: state update (lane t of the half takes the t-th net change)
+            SSA_CHECK(j >= 0 && j < (SSA_R > 0 ? SSA_R : 1), P.stats);
             const int4 rj = rec[j];
+            SSA_CHECK(!apply || (0 <= rj.x && rj.x <= rj.y && rj.y <= P.n_ent && 0 <= rj.z && rj.z <= rj.w &&
+                                 rj.w <= P.n_dep), P.stats);
             const int nb = apply ? rj.x : 0, ne = apply ? rj.y : 0;
             for (int q = nb + hl; q < ne; q += SSA_HL) {
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
+                SSA_CHECK(sp < SSA_S, P.stats);
                 x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));
             }
             __syncwarp();
@@ -352,6 +357,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             const int db = apply ? rj.z : 0, de = apply ? rj.w : 0;
             for (int q = db + hl; q < de; q += SSA_HL) {
                 const ssa_u64 d = dent[q];
+                SSA_CHECK((int)(d & 0x3FFF) < SSA_S && (int)((d >> 14) & 0x3FFF) < SSA_S &&
+                          (int)((d >> 32) & 0xFFFF) < SSA_HL * SSA_AR && (int)((d >> 32) & 0xFFFF) % SSA_AR < SSA_P &&
+                          (int)(d >> 48) < SSA_R, P.stats);
 #if !SSA_HAS_M3
                 a[(unsigned)(d >> 32) & 0xFFFFu] = k2h_propensity(d, rxd, x);
 #else

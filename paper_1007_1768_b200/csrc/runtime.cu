@@ -398,6 +398,8 @@ struct K1Gen {
     int sel = 0;   // sel=f64|i64|mix: selection compares as fp64 (FP64 pipe), int64 patterns (ALU), or alternating
     std::vector<int> hot;   // hot=a:b:...: reactions updated by predicated adds ahead of the jump table
     bool spread32 = true;   // small-ensemble launches use a (32, 1) launch-bounds variant (nospread32: off)
+    int plog = 0;           // plog=div: round 1's division-based log (speed A/B only, breaks parity);
+                            // plog=global: the table read through L1 instead of shared memory
     bool no_cskip = true;   // cskip: reuse the cold prefix (measured 1.6% slower on HIV: the warp-uniform
                             // branch splits the event loop's basic block; off by default)
 };
@@ -413,6 +415,8 @@ static K1Gen k1_gen()
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
         if (s.find("nospread32") != std::string::npos) r.spread32 = false;
+        if (s.find("plog=div") != std::string::npos) r.plog = 1;
+        if (s.find("plog=global") != std::string::npos) r.plog = 2;
         if (s.find("cskip") != std::string::npos && s.find("nocskip") == std::string::npos) r.no_cskip = false;
         const size_t h = s.find("hot=");
         if (h != std::string::npos) {
@@ -450,6 +454,8 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         o << "#define SSA_K1_RECORD 0\n";
     }
     o << "#define SSA_K1_PROF " << (spec && spec->prof ? 1 : 0) << "\n";
+    o << "#define SSA_PLOG_DIV " << (g.plog == 1 ? 1 : 0) << "\n#define SSA_PLOG_GLOBAL " << (g.plog == 2 ? 1 : 0) << "\n";
+    if (g.plog == 1) o << "__constant__ double c_plog_div[14] = SSA_PLOG_DIV_COEF_INIT;\n";
     // tail compaction (k1_thread.cuh): plain, dump and profiling variants
     o << "#define SSA_K1_MIG " << ((!sweep && record == 0) ? 1 : 0) << "\n";
     std::vector<int> hot;   // the dispatch profile's hot reactions (K1Spec, or the knob)
@@ -481,7 +487,7 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         o << "#define SSA_K(i) c_k[i]\n#define SSA_KP_PARAM\n#define SSA_KP_ARG\n";
     }
     o << "__constant__ double c_x0[" << S << "];\n";
-    o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
+    o << "__constant__ double c_plog[8] = SSA_PLOG_COEF_INIT;\n";
     // a3's modified rates k^ = max(0, k + d x_m) (R4) depend on x_m alone: each
     // distinct (k, d, m) is kept in a register (kh) and recomputed only after
     // an event that changes a modifier species (and at the start of a
@@ -779,11 +785,18 @@ static ssa_status nvrtc_compile(const std::string& src, std::vector<char>& cubin
 // model's own constant pool).
 // seed: the run's seed when the key schedule is compiled in (K1Gen::seed_imm),
 // else -1 (keys from the launch parameters).
+// SSA_DEBUG_CHECKS=1: the NVRTC kernels count out-of-range indices (ssa_device.cuh SSA_CHECK)
+static const char* debug_checks_prefix()
+{
+    static const bool on = getenv("SSA_DEBUG_CHECKS") && atoi(getenv("SSA_DEBUG_CHECKS")) != 0;
+    return on ? "#define SSA_DEBUG_CHECKS 1\n" : "";
+}
+
 static std::string k1_full_source(const ssa_model& m, int block, int minb, bool dump, const PoolLayout* sweep,
                                   long long seed = -1, int record = 0, const K1Spec* spec = nullptr)
 {
     const PoolLayout L = sweep ? *sweep : make_pool(m, 1, nullptr, nullptr);
-    return std::string(kSsaDeviceSrc) + "\n" +
+    return std::string(debug_checks_prefix()) + kSsaDeviceSrc + "\n" +
            gen_k1_model(m, block, minb, dump, sweep != nullptr, L, seed, seed != -1, record, spec) + "\n" +
            kK1ThreadSrc;
 }
@@ -954,14 +967,14 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
       << "\n#define SSA_K2_HALF " << (half ? 1 : 0)
       << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_HAS_MODS " << mods << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
-    o << "__constant__ double c_plog[14] = SSA_PLOG_COEF_INIT;\n";
+    o << "__constant__ double c_plog[8] = SSA_PLOG_COEF_INIT;\n";
     return o.str();
 }
 
 // half: two trajectories per warp (k2_half.cuh, order warp16), P = ceil(R/16)
 static std::string k2_full_source(const ssa_model& m, int P, int block, int minb, bool dump, bool half = false)
 {
-    return std::string(kSsaDeviceSrc) + "\n" + gen_k2_model(m, P, block, minb, dump, half) + "\n" + kK2WarpSrc +
+    return std::string(debug_checks_prefix()) + kSsaDeviceSrc + "\n" + gen_k2_model(m, P, block, minb, dump, half) + "\n" + kK2WarpSrc +
            "\n" + kK2HalfSrc;
 }
 
@@ -1679,6 +1692,9 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
 
 static ssa_status fill_result(const RunInfo& info, ssa_result* r)
 {
+    if (info.stats.pad[0])
+        return fail(SSA_ERR_CUDA, "device bounds checks failed %llu times (SSA_DEBUG_CHECKS)",
+                    (unsigned long long)info.stats.pad[0]);
     r->events = info.stats.events;
     r->near_ties = info.stats.near_ties;
     r->n_errors = info.stats.n_errors;

@@ -174,3 +174,33 @@ def test_gate_validation(ssa):
     ok = ssa.Model(Network(("A",), (1,), (_rx([(0, 1)], [], 1.0, mass_action=False, gates=[(0, 0)]),)))
     st, log, _ = ok.k1_compile()
     assert st == 0, log
+
+
+def test_device_plog_literals_match_the_pinned_definition():
+    """The device copy of plog's constants (csrc/ssa_device.cuh: the 128-row table and the
+    uniform coefficients) is the same pinned definition as the oracle's copy, which
+    tests/test_oracle_primitives.py recomputes in exact arithmetic.  The two files share no
+    code; this compares the literals."""
+    import re
+    from fractions import Fraction
+    from decimal import Decimal, getcontext
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dev = open(os.path.join(root, "paper_1007_1768_b200", "csrc", "ssa_device.cuh")).read()
+    body = dev[dev.index("ssa_plog_tab[128][4] = {"):]
+    body = body[:body.index("};")]
+    rows = re.findall(r"\{(-?0x[0-9a-fp.+-]+), (-?0x[0-9a-fp.+-]+), (-?0x[0-9a-fp.+-]+), 0\.0\}", body)
+    assert len(rows) == 128
+    getcontext().prec = 60
+    for i, r in enumerate(rows):
+        inv, th, tl = (float.fromhex(v) for v in r)
+        if i in (0, 127):
+            assert (inv, th, tl) == (1.0, 0.0, 0.0)
+            continue
+        c = Fraction(256 + 2 * i + 1, 256) / (2 if i >= 53 else 1)
+        assert inv == float(1 / c)
+        t = -Decimal(inv).ln()
+        assert th == float(t) and tl == float(t - Decimal(th))
+    coef = dev[dev.index("#define SSA_PLOG_COEF_INIT"):]
+    coef = [float.fromhex(v) for v in re.findall(r"-?0x1\.[0-9a-f]+p[-+]\d+", coef[:coef.index("}")])]
+    assert coef[:6] == [float(Fraction((-1) ** (k + 1), k)) for k in (7, 6, 5, 4, 3, 2)]
+    assert coef[6:] == [float.fromhex("0x1.62e42fee00000p-1"), float.fromhex("0x1.a39ef35793c76p-33")]

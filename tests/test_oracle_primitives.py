@@ -129,15 +129,25 @@ def test_plog_special_values(oracle_lib):
     assert abs(O.plog(1 - d) + d) <= 2 * np.spacing(d)
 
 
+def _plog_table(src):
+    body = src[src.index("PLOG_TAB[128][3] = {"):]
+    body = body[:body.index("};")]
+    rows = re.findall(r"\{(-?0x[0-9a-fp.+-]+), (-?0x[0-9a-fp.+-]+), (-?0x[0-9a-fp.+-]+)\}", body)
+    return [tuple(float.fromhex(v) for v in r) for r in rows]
+
+
 def test_plog_constants_are_what_they_claim():
-    """The literals in ssa_oracle.c: C_k == fl(1/(2k+1)), sqrt2, ln2 split."""
+    """The literals of the oracle's plog (R11): Q_k == fl((-1)^(k+1)/k) for
+    k = 2..7; the ln 2 split; and every table row -- inv_i = fl(1/c_i) with c_i the
+    centre of bucket i (halved for i >= 53), inv = 1 for i = 0 and 127, T_hi = fl(-ln inv_i)
+    and T_lo = fl(-ln inv_i - T_hi) -- recomputed in exact / 60-digit arithmetic."""
     src = open(os.path.join(ROOT, "oracle", "ssa_oracle.c")).read()
-    lits = re.findall(r"(0x1\.[0-9a-f]+p[-+]\d+),\s*/\*\s*1/(\d+)\s*\*/", src)
-    assert len(lits) == 10
-    for hexlit, den in lits:
-        assert float.fromhex(hexlit) == float(Fraction(1, int(den)))
-    sq = float.fromhex(re.search(r"SQRT2 = (0x[0-9a-fp.+-]+);", src).group(1))
-    assert sq == float(np.sqrt(2.0))
+    lits = re.findall(r"(-?0x1\.[0-9a-f]+p[-+]\d+),\s*/\*\s*(-?)1/(\d+)\s*\*/", src)
+    assert [int(d) for _, _, d in lits] == [2, 3, 4, 5, 6, 7]
+    for hexlit, sign, den in lits:
+        k = int(den)
+        assert float.fromhex(hexlit) == float(Fraction((-1) ** (k + 1), k))
+        assert (sign == "-") == (k % 2 == 0)
     hi = float.fromhex(re.search(r"LN2_HI = (0x[0-9a-fp.+-]+);", src).group(1))
     lo = float.fromhex(re.search(r"LN2_LO = (0x[0-9a-fp.+-]+);", src).group(1))
     getcontext().prec = 60
@@ -145,3 +155,36 @@ def test_plog_constants_are_what_they_claim():
     # hi has at most 32 significant bits so e*hi is exact for |e| < 2^21
     assert 0.5 <= hi < 1 and (Fraction(hi) * 2**32).denominator == 1
     assert abs(Decimal(hi) + Decimal(lo) - ln2) < Decimal(2) ** -80
+    tab = _plog_table(src)
+    assert len(tab) == 128
+    for i, (inv, th, tl) in enumerate(tab):
+        if i in (0, 127):
+            assert inv == 1.0 and th == 0.0 and tl == 0.0
+            continue
+        c = Fraction(256 + 2 * i + 1, 256) / (2 if i >= 53 else 1)
+        assert inv == float(1 / c), i
+        t = -Decimal(inv).ln()
+        assert th == float(t) and tl == float(t - Decimal(th)), i
+
+
+def test_plog_buckets_and_fold(oracle_lib):
+    """The bucket structure of plog: near u = 1 from both sides (buckets 0 and 127, inv = 1)
+    ln u ~ u - 1 to the last bit; across every bucket edge and the fold at m = 1.4140625 the
+    result stays within 2 ulp of logl (monotonicity across an edge is not part of the definition:
+    neighbours may differ by an ulp the other way)."""
+    O = oracle_lib
+    for d in (2.0 ** -53, 2.0 ** -40, 2.0 ** -20, 2.0 ** -9):
+        x = 1 - d
+        assert abs(Decimal(O.plog(x)) - Decimal(x).ln()) <= Decimal(np.spacing(abs(float(Decimal(x).ln()))))
+    edges = []
+    for e in (-1, -7, -30):
+        for i in range(128):
+            m = 1 + i / 128
+            for v in (np.nextafter(m, 0), m, np.nextafter(m, 2)):
+                if 1 <= v < 2:
+                    edges.append(v * 2.0 ** e)
+    u = np.array(sorted(edges))
+    p = O.plog_n(u)
+    ref = np.log(u.astype(np.longdouble))
+    ulp = np.spacing(np.abs(ref.astype(np.float64))).astype(np.longdouble)
+    assert np.abs((p.astype(np.longdouble) - ref) / ulp).astype(np.float64).max() <= 2.0
