@@ -76,9 +76,17 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     volatile ssa_u64* const mctl = P.mig_ctl;
 #endif
     // plog's table in shared memory (lanes index it independently)
-    __shared__ __align__(16) double s_plog[128][4];
-    for (int q = threadIdx.x; q < 128 * 4; q += blockDim.x) (&s_plog[0][0])[q] = (&ssa_plog_tab[0][0])[q];
+    __shared__ __align__(16) double s_plog_[128][4];
+    for (int q = threadIdx.x; q < 128 * 4; q += blockDim.x) (&s_plog_[0][0])[q] = (&ssa_plog_tab[0][0])[q];
     __syncthreads();
+    // the table's address computed once and kept opaque: otherwise the loop re-derives the
+    // shared window base (S2R of the CTA id) every event
+    const double (*s_plog)[4];
+    {
+        unsigned sa = (unsigned)__cvta_generic_to_shared(&s_plog_[0][0]);
+        asm volatile("" : "+r"(sa));
+        s_plog = (const double (*)[4])__cvta_shared_to_generic(sa);
+    }
     // small ensembles (spread launch): one working lane per warp and one warp
     // per block, so each trajectory has an SM sub-partition to itself
     if (P.spread && (threadIdx.x & 31) != 0) return;
