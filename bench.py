@@ -659,6 +659,8 @@ def main():
                 ("alg_thread_instr_per_event" if path == 1 else "alg_warp_instr_per_event"): I, "kernel_ms": k1_ms,
                 "peak_basis": f"{n_sm} SMs x 4 issue slots/clk x {sm_max:.0f} MHz (MEASURED_PEAKS.json sm_max_mhz)"}
     if path == 1:
+        # round 1 counted plog at 35 (its division-based log): the same achieved rate on that count
+        roofline["frac_at_round1_count"] = per_rank_events * (I + 14) / 32.0 / (k1_ms / 1e3) / 1e9 / peak
         # the co-bound: the FP64 pipe issues 0.497 warp-instructions per clock per SMSP
         # (measured, profiles/r1h_pipe_peaks.txt), and about half of K1's work is FP64
         F = alg_fp64_per_event(net)
