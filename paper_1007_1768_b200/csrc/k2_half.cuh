@@ -220,6 +220,16 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         }
         // a4: lane sum -- a pairwise tree over the row's 16 positions (P propensities, then the
         // zero padding; R34, oracle mode 3), two per load, depth 4 -- then the scan over the half
+#if SSA_K2H_SEQSUM
+        // speed A/B only (not the pinned order): round 2's first sequential lane sum
+        double L = 0.0;
+#pragma unroll
+        for (int q = 0; q + 1 < SSA_P; q += 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(a + hl * SSA_AR + q);
+            L = __dadd_rn(__dadd_rn(L, v2.x), v2.y);
+        }
+        if (SSA_P & 1) L = __dadd_rn(L, a[hl * SSA_AR + SSA_P - 1]);
+#else
         double t8[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -235,6 +245,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
 #pragma unroll
             for (int q = 0; q + w < 8; q += 2 * w) t8[q] = __dadd_rn(t8[q], t8[q + w]);
         const double L = t8[0];
+#endif
         double v = ssa_scan_step_m(L, 1, mk1);
         v = ssa_scan_step_m(v, 2, mk2);
         v = ssa_scan_step_m(v, 4, mk4);
@@ -359,7 +370,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             const int db = apply ? rj.z : 0, de = apply ? rj.w : 0;
             // this lane's first dependency entry, loaded before the update (a table entry:
             // it does not wait for the new counts)
+#if SSA_K2H_NOPRE
+            const ssa_u64 d0 = 0ull;
+#else
             const ssa_u64 d0 = (db + hl < de) ? dent[db + hl] : 0ull;
+#endif
             for (int q = nb + hl; q < ne; q += SSA_HL) {
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
@@ -369,7 +384,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             __syncwarp();
             // a3: the half recomputes dep(j), one entry per lane
             for (int q = db + hl; q < de; q += SSA_HL) {
+#if SSA_K2H_NOPRE
+                const ssa_u64 d = dent[q];
+#else
                 const ssa_u64 d = (q == db + hl) ? d0 : dent[q];
+#endif
                 SSA_CHECK((int)(d & 0x3FFF) < SSA_S && (int)((d >> 14) & 0x3FFF) < SSA_S &&
                           (int)((d >> 32) & 0xFFFF) < SSA_HL * SSA_AR && (int)((d >> 32) & 0xFFFF) % SSA_AR < SSA_P &&
                           (int)(d >> 48) < SSA_R, P.stats);

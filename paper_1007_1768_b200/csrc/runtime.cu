@@ -968,6 +968,11 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
       << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_HAS_MODS " << mods << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
     o << "__constant__ double c_plog[8] = SSA_PLOG_COEF_INIT;\n";
+    // speed A/B knobs of the half-warp kernel (SSA_K2_GEN): seqsum (sequential lane sums: not
+    // the pinned warp16s order), nopre (no dependency-entry prefetch)
+    static const std::string k2g = getenv("SSA_K2_GEN") ? getenv("SSA_K2_GEN") : "";
+    o << "#define SSA_K2H_SEQSUM " << (k2g.find("seqsum") != std::string::npos ? 1 : 0) << "\n";
+    o << "#define SSA_K2H_NOPRE " << (k2g.find("nopre") != std::string::npos ? 1 : 0) << "\n";
     return o.str();
 }
 
