@@ -110,6 +110,14 @@ typedef struct {
  * than 4 gates. */
 ssa_status ssa_model_create_ex(int32_t n_species, const int64_t* initial_counts, int32_t n_reactions,
                                const ssa_reaction* reactions, const ssa_reaction_ext* ext, ssa_model** out);
+/* Species names (SURVEY.md §8(b)'s nullable `names`; the paper's models name their species,
+ * e.g. Table 1's U0, U, T, Z4, Z5, I4, I5, V4, V5, F): attach n_species
+ * NUL-terminated names (deep-copied) to a model, or NULL to clear them.  Names are labels
+ * only; no computation reads them.  Errors: SSA_ERR_INVALID_ARG (null model, a null name). */
+ssa_status ssa_model_set_names(ssa_model* model, const char* const* names);
+/* The name of species `index`, or NULL if none was set or index is out of range.  The
+ * pointer stays valid until the model is destroyed or its names are set again. */
+const char* ssa_model_species_name(const ssa_model* model, int32_t index);
 void ssa_model_destroy(ssa_model* model);
 int32_t ssa_model_n_species(const ssa_model* model);
 int32_t ssa_model_n_reactions(const ssa_model* model);

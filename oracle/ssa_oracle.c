@@ -370,9 +370,8 @@ int oracle_propensities(const oracle_model *M, const int64_t *x, double *a, int3
 /*         lane* = min{ l : v_l > r };  p = v_{lane*-1} (0 for lane 0), then  */
 /*         p += a_j over lane*'s reactions in order, j* = first j with p > r; */
 /*         if none, j* = the largest j <= lane*'s last index with a_j > 0.    */
-/*  mode 3 "warp16s" (the half-warp path since round 2): each lane's sum is */
-/*         a pairwise tree over its 16 positions (P propensities, zeros);     */
-/*         scan and lane* as mode 2; then lane*'s P propensities (padded to 16 */
+/*  mode 3 "warp16s" (the half-warp path since round 2): lane sums, scan and */
+/*         lane* as mode 2; then lane*'s P propensities (padded with 0 to 16  */
 /*         positions) are Hillis-Steele scanned over the 16 positions         */
 /*         (offsets 1,2,4,8) into s_q, p_q = v_{lane*-1} + s_q (s_q for lane  */
 /*         0), j* = lane*'s q-th reaction for the first q with p_q > r; if    */
@@ -402,31 +401,12 @@ static int select_sequential(const double *a, int R, double r)
  * the L lane sums with offsets 1, 2, 4, ... < L, a0 = v_{L-1}. */
 static int mode_lanes(int mode) { return (mode == 2 || mode == 3) ? 16 : 32; }
 
-/* mode 3's lane sum: a pairwise tree over the lane's 16 positions (its P
- * propensities, then zeros): ((a0 + a1) + (a2 + a3)) + ... -- depth 4 instead
- * of a 16-long sequential chain (R34). */
-static double lane_sum_tree(const double *a, int R, int P, int l)
-{
-    double t[16];
-    for (int q = 0; q < 16; ++q) {
-        const int j = l * P + q;
-        t[q] = (q < P && j < R) ? a[j] : 0.0;
-    }
-    for (int w = 1; w < 16; w *= 2)
-        for (int q = 0; q + w < 16; q += 2 * w) t[q] = t[q] + t[q + w];
-    return t[0];
-}
-
 static void warp_scan_mode(const double *a, int R, int L, int mode, double v[32])
 {
     int P = (R + L - 1) / L;
     if (P < 1) P = 1;
     double lsum[32];
     for (int l = 0; l < L; ++l) {
-        if (mode == 3) {
-            lsum[l] = lane_sum_tree(a, R, P, l);
-            continue;
-        }
         double s = 0.0;
         for (int j = l * P; j < (l + 1) * P && j < R; ++j) s = s + a[j];
         lsum[l] = s;

@@ -4,9 +4,8 @@
 // generated section defines SSA_K2_HALF = 1.
 //
 // Order "warp16s" (R13, R34; oracle mode 3): lane l of the half owns
-// the P = ceil(R/16) contiguous reactions l*P + q; lane sums as a pairwise tree
-// over the 16 positions (P propensities, then zeros), then an inclusive
-// Hillis-Steele scan over the 16 lanes (offsets 1, 2,
+// the P = ceil(R/16) contiguous reactions l*P + q; lane sums from 0.0 in q
+// order, then an inclusive Hillis-Steele scan over the 16 lanes (offsets 1, 2,
 // 4, 8; the shuffles are segmented with width 16), a0 = v_15, lane* = min{l :
 // v_l > r}.  The step inside lane* is a second 16-position Hillis-Steele scan
 // over lane*'s propensities, one per lane of the half (lane q reads lane*'s
@@ -218,10 +217,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             U2c = ssa_u53(o.o3, o.o2);
             need_rng = false;
         }
-        // a4: lane sum -- a pairwise tree over the row's 16 positions (P propensities, then the
-        // zero padding; R34, oracle mode 3), two per load, depth 4 -- then the scan over the half
-#if SSA_K2H_SEQSUM
-        // speed A/B only (not the pinned order): round 2's first sequential lane sum
+        // a4: lane sum (sequential, two propensities per load), scan over the half (width 16).
+        // (A pairwise-tree lane sum -- a 4-deep chain instead of 16 -- measured 2% slower.)
         double L = 0.0;
 #pragma unroll
         for (int q = 0; q + 1 < SSA_P; q += 2) {
@@ -229,23 +226,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             L = __dadd_rn(__dadd_rn(L, v2.x), v2.y);
         }
         if (SSA_P & 1) L = __dadd_rn(L, a[hl * SSA_AR + SSA_P - 1]);
-#else
-        double t8[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            if (2 * q < SSA_P) {
-                const double2 v2 = *reinterpret_cast<const double2*>(a + hl * SSA_AR + 2 * q);
-                t8[q] = __dadd_rn(v2.x, v2.y);      // position 2q+1 >= P holds 0.0
-            } else {
-                t8[q] = 0.0;
-            }
-        }
-#pragma unroll
-        for (int w = 1; w < 8; w *= 2)
-#pragma unroll
-            for (int q = 0; q + w < 8; q += 2 * w) t8[q] = __dadd_rn(t8[q], t8[q + w]);
-        const double L = t8[0];
-#endif
         double v = ssa_scan_step_m(L, 1, mk1);
         v = ssa_scan_step_m(v, 2, mk2);
         v = ssa_scan_step_m(v, 4, mk4);
@@ -368,13 +348,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                                  rj.w <= P.n_dep), P.stats);
             const int nb = apply ? rj.x : 0, ne = apply ? rj.y : 0;
             const int db = apply ? rj.z : 0, de = apply ? rj.w : 0;
-            // this lane's first dependency entry, loaded before the update (a table entry:
-            // it does not wait for the new counts)
-#if SSA_K2H_NOPRE
-            const ssa_u64 d0 = 0ull;
-#else
-            const ssa_u64 d0 = (db + hl < de) ? dent[db + hl] : 0ull;
-#endif
             for (int q = nb + hl; q < ne; q += SSA_HL) {
                 const int ent = nu_ent[q];
                 const int sp = ent & 0xFFFF;
@@ -384,11 +357,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             __syncwarp();
             // a3: the half recomputes dep(j), one entry per lane
             for (int q = db + hl; q < de; q += SSA_HL) {
-#if SSA_K2H_NOPRE
                 const ssa_u64 d = dent[q];
-#else
-                const ssa_u64 d = (q == db + hl) ? d0 : dent[q];
-#endif
                 SSA_CHECK((int)(d & 0x3FFF) < SSA_S && (int)((d >> 14) & 0x3FFF) < SSA_S &&
                           (int)((d >> 32) & 0xFFFF) < SSA_HL * SSA_AR && (int)((d >> 32) & 0xFFFF) % SSA_AR < SSA_P &&
                           (int)(d >> 48) < SSA_R, P.stats);

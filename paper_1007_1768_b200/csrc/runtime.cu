@@ -112,6 +112,7 @@ struct DevCache {
 struct ssa_model {
     int S = 0, R = 0;
     std::vector<long long> x0;
+    std::vector<std::string> names;   // optional species labels (ssa_model_set_names)
     std::vector<RxI> rx;
     mutable std::mutex mu;
     mutable std::map<int, DevCache> dev;
@@ -247,6 +248,27 @@ extern "C" void ssa_model_destroy(ssa_model* m)
     }
     if (m->pinned_const) cudaFreeHost(m->pinned_const);
     delete m;
+}
+
+extern "C" ssa_status ssa_model_set_names(ssa_model* m, const char* const* names)
+{
+    if (!m) return fail(SSA_ERR_INVALID_ARG, "model is null");
+    std::vector<std::string> v;
+    if (names) {
+        for (int s = 0; s < m->S; ++s) {
+            if (!names[s]) return fail(SSA_ERR_INVALID_ARG, "name of species %d is null", s);
+            v.emplace_back(names[s]);
+        }
+    }
+    std::lock_guard<std::mutex> lk(m->mu);
+    m->names.swap(v);
+    return SSA_OK;
+}
+
+extern "C" const char* ssa_model_species_name(const ssa_model* m, int32_t index)
+{
+    if (!m || index < 0 || index >= m->S || m->names.empty()) return nullptr;
+    return m->names[(size_t)index].c_str();
 }
 
 extern "C" int32_t ssa_model_n_species(const ssa_model* m) { return m ? m->S : 0; }
@@ -968,11 +990,6 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
       << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_HAS_MODS " << mods << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
     o << "__constant__ double c_plog[8] = SSA_PLOG_COEF_INIT;\n";
-    // speed A/B knobs of the half-warp kernel (SSA_K2_GEN): seqsum (sequential lane sums: not
-    // the pinned warp16s order), nopre (no dependency-entry prefetch)
-    static const std::string k2g = getenv("SSA_K2_GEN") ? getenv("SSA_K2_GEN") : "";
-    o << "#define SSA_K2H_SEQSUM " << (k2g.find("seqsum") != std::string::npos ? 1 : 0) << "\n";
-    o << "#define SSA_K2H_NOPRE " << (k2g.find("nopre") != std::string::npos ? 1 : 0) << "\n";
     return o.str();
 }
 

@@ -97,6 +97,10 @@ def lib():
         L.ssa_model_create_ex.argtypes = [C.c_int32, P(C.c_int64), C.c_int32, P(ssa_reaction), P(ssa_reaction_ext),
                                           P(C.c_void_p)]
         L.ssa_model_create_ex.restype = C.c_int
+        L.ssa_model_set_names.argtypes = [C.c_void_p, P(C.c_char_p)]
+        L.ssa_model_set_names.restype = C.c_int
+        L.ssa_model_species_name.argtypes = [C.c_void_p, C.c_int32]
+        L.ssa_model_species_name.restype = C.c_char_p
         L.ssa_model_destroy.argtypes = [C.c_void_p]
         L.ssa_model_destroy.restype = None
         L.ssa_model_n_species.argtypes = [C.c_void_p]
@@ -182,6 +186,18 @@ class Model:
         _check(lib().ssa_model_create_ex(self.S, x0.ctypes.data_as(C.POINTER(C.c_int64)), self.R, rx, ext,
                                          C.byref(h)))
         self.handle = h
+        names = getattr(network, "species", None)
+        if names:
+            arr = (C.c_char_p * self.S)(*[str(n).encode() for n in names])
+            _check(lib().ssa_model_set_names(self.handle, arr))
+
+    def species_names(self):
+        """The species names attached to the model (ssa_model_species_name)."""
+        out = []
+        for s in range(self.S):
+            v = lib().ssa_model_species_name(self.handle, s)
+            out.append(None if v is None else v.decode())
+        return out
 
     def close(self):
         if getattr(self, "handle", None):

@@ -204,3 +204,15 @@ def test_device_plog_literals_match_the_pinned_definition():
     coef = [float.fromhex(v) for v in re.findall(r"-?0x1\.[0-9a-f]+p[-+]\d+", coef[:coef.index("}")])]
     assert coef[:6] == [float(Fraction((-1) ** (k + 1), k)) for k in (7, 6, 5, 4, 3, 2)]
     assert coef[6:] == [float.fromhex("0x1.62e42fee00000p-1"), float.fromhex("0x1.a39ef35793c76p-33")]
+
+
+def test_species_names(ssa):
+    """ssa_model_set_names / ssa_model_species_name (SURVEY.md §8(b)'s nullable names)."""
+    m = ssa.Model(inputs.hiv())
+    assert m.species_names() == list(inputs.networks.HIV_SPECIES)
+    lib = ssa.lib()
+    assert lib.ssa_model_set_names(m.handle, None) == 0
+    assert m.species_names() == [None] * m.S
+    assert lib.ssa_model_species_name(m.handle, 99) is None
+    bad = (C.c_char_p * m.S)(*([b"x"] * (m.S - 1) + [None]))
+    assert lib.ssa_model_set_names(m.handle, bad) == 1
