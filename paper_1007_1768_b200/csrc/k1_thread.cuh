@@ -350,12 +350,12 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                     const bool near = (tn < INF && fabs(__dadd_rn(tn, -s_next)) <= tol) ||
                                       (e > 0 && fabs(__dadd_rn(t, -s_next)) <= tol);
                     ties += near ? 1 : 0;
-                    SSA_CHECK(k <= K && rel < P.n_ids && rel < P.stride, P.stats);
-                    int* dst = P.staging + (ssa_u64)k * SSA_S * P.stride + rel;
+                    SSA_CHECK(k <= K && rel < P.n_ids && (ssa_u64)(k + 1) * SSA_S <= P.stride, P.stats);
+                    int* dst = P.staging + rel * P.stride + (ssa_u64)k * SSA_S;   // trajectory-major row
 #pragma unroll
                     for (int s = 0; s < SSA_S; ++s) {
                         if (x[s] > 2147483647.0) status = 2;
-                        dst[(ssa_u64)s * P.stride] = (int)x[s];
+                        dst[s] = (int)x[s];
                     }
 #if SSA_K1_DUMP
                     if (slot >= 0) {

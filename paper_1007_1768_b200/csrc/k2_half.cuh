@@ -286,7 +286,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                         const double xv = x[s];
                         ovf |= (xv > 2147483647.0) ? 1 : 0;
                         SSA_CHECK(k <= K && rel < P.n_ids, P.stats);
-                        P.staging[((ssa_u64)k * SSA_S + s) * P.stride + rel] = (int)xv;
+                        P.staging[rel * P.stride + (ssa_u64)k * SSA_S + s] = (int)xv;   // trajectory-major row
 #if SSA_K2_DUMP
                         if (slot >= 0) P.dump_states[((ssa_u64)slot * G + (ssa_u64)k) * SSA_S + s] = (int)xv;
 #endif

@@ -73,31 +73,40 @@ static __device__ __forceinline__ void wf_merge_full(double& mA, double& m2A, do
     m2A = __dadd_rn(__dadd_rn(m2A, m2B), __dmul_rn(__dmul_rn(d, d), half_h));
 }
 
-static __device__ __forceinline__ void tree_block_full(const int4 q0, const int4 q1, double& mean, double& m2)
+// The staged samples are trajectory-major (runtime.cu): trajectory i's grid samples form a row of
+// `row` ints (cells rounded up to 8), element (i, cell) at i*row + cell.  A K3 block reduces one
+// 2048-id tile for a group of 8 consecutive cells: thread t holds ids [8t, 8t+8), and each of its
+// ids' 8 cells is one 32-byte sector (two 16-byte loads), so the tile's samples are read as whole
+// sectors exactly once.  Per cell the reduction is the same canonical tree as before (8 adjacent
+// leaves per thread, then the warp and block levels).
+#define SSA_TREE_CG 8
+
+// the 8-leaf fold of one cell over a thread's 8 ids, full leaves: the integer fast path when all
+// counts are below 2^20 (exact: see below), else the division-free fp64 merges
+static __device__ __forceinline__ void fold8_full(const int (&c)[8], double& mm, double& vv)
 {
-    __shared__ double shm[SSA_TREE_BLOCK / 32], shq[SSA_TREE_BLOCK / 32];
-    // 8 adjacent leaves per thread: levels h = 1, 2, 4.
-    double mm, vv;
     const unsigned lim = 1u << 20;
-    if ((unsigned)q0.x < lim && (unsigned)q0.y < lim && (unsigned)q0.z < lim && (unsigned)q0.w < lim &&
-        (unsigned)q1.x < lim && (unsigned)q1.y < lim && (unsigned)q1.z < lim && (unsigned)q1.w < lim) {
-        // Counts below 2^20: every operation of these three merge levels is
-        // exact in fp64 (means are multiples of 2^-3 below 2^20, deltas have
-        // <= 22 significant bits so their squares <= 44, the M2 sums stay below
-        // 2^49 with <= 4 fractional bits), so the tree yields the exact
-        // mean = S1/8 and M2 = (8 S2 - S1^2)/8 -- computed here in integers,
-        // bitwise equal to the fp64 merges and without their FP64 work.
-        const unsigned long long s1 = (unsigned long long)q0.x + q0.y + q0.z + q0.w + q1.x + q1.y + q1.z + q1.w;
-        const unsigned long long s2 =
-            (unsigned long long)q0.x * q0.x + (unsigned long long)q0.y * q0.y + (unsigned long long)q0.z * q0.z +
-            (unsigned long long)q0.w * q0.w + (unsigned long long)q1.x * q1.x + (unsigned long long)q1.y * q1.y +
-            (unsigned long long)q1.z * q1.z + (unsigned long long)q1.w * q1.w;
+    bool small = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) small = small && (unsigned)c[i] < lim;
+    if (small) {
+        // Counts below 2^20: every operation of these three merge levels is exact in fp64
+        // (means are multiples of 2^-3 below 2^20, deltas have <= 22 significant bits so
+        // their squares <= 44, the M2 sums stay below 2^49 with <= 4 fractional bits), so the
+        // tree yields the exact mean = S1/8 and M2 = (8 S2 - S1^2)/8 -- computed here in
+        // integers, bitwise equal to the fp64 merges and without their FP64 work.
+        unsigned long long s1 = 0, s2 = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            s1 += (unsigned long long)c[i];
+            s2 += (unsigned long long)c[i] * (unsigned long long)c[i];
+        }
         mm = __dmul_rn((double)s1, 0.125);
         vv = __dmul_rn((double)(8ull * s2 - s1 * s1), 0.125);
     } else {
-        double m[8] = {(double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w,
-                       (double)q1.x, (double)q1.y, (double)q1.z, (double)q1.w};
-        double v[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        double m[8], v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) { m[i] = (double)c[i]; v[i] = 0.0; }
         wf_merge_full(m[0], v[0], m[1], v[1], 0.5);
         wf_merge_full(m[2], v[2], m[3], v[3], 0.5);
         wf_merge_full(m[4], v[4], m[5], v[5], 0.5);
@@ -108,95 +117,82 @@ static __device__ __forceinline__ void tree_block_full(const int4 q0, const int4
         mm = m[0];
         vv = v[0];
     }
+}
+
+// Full tiles only: tile = blockIdx.x (< count / SPAN), cell group = blockIdx.y (+ 65535 * z)
+__global__ void __launch_bounds__(SSA_TREE_BLOCK, 2) ssa_tree_leaf_full(const int* __restrict__ staging,
+                                                                       ssa_u64 row, ssa_u64 cells, ssa_tree_out out)
+{
+    __shared__ double shm[SSA_TREE_CG][SSA_TREE_BLOCK / 32], shq[SSA_TREE_CG][SSA_TREE_BLOCK / 32];
+    const ssa_u64 cg = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    const ssa_u64 c0 = cg * SSA_TREE_CG;
+    if (c0 >= cells) return;
+    const ssa_u64 tile = blockIdx.x;
+    const ssa_u64 id0 = tile * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
+    int v[SSA_TREE_CG][8];                                // [cell][leaf]
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int4* p = reinterpret_cast<const int4*>(staging + (id0 + i) * row + c0);
+        const int4 a = p[0], b = p[1];
+        v[0][i] = a.x; v[1][i] = a.y; v[2][i] = a.z; v[3][i] = a.w;
+        v[4][i] = b.x; v[5][i] = b.y; v[6][i] = b.z; v[7][i] = b.w;
+    }
+    double mm[SSA_TREE_CG], vv[SSA_TREE_CG];
+#pragma unroll
+    for (int c = 0; c < SSA_TREE_CG; ++c) fold8_full(v[c], mm[c], vv[c]);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     // warp levels: subtrees of 8*o leaves, h/2 = 4*o
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const double mb = __shfl_down_sync(0xffffffffu, mm, o);
-        const double vb = __shfl_down_sync(0xffffffffu, vv, o);
-        if ((lane & (2 * o - 1)) == 0) wf_merge_full(mm, vv, mb, vb, 4.0 * o);
+#pragma unroll
+        for (int c = 0; c < SSA_TREE_CG; ++c) {
+            const double mb = __shfl_down_sync(0xffffffffu, mm[c], o);
+            const double vb = __shfl_down_sync(0xffffffffu, vv[c], o);
+            if ((lane & (2 * o - 1)) == 0) wf_merge_full(mm[c], vv[c], mb, vb, 4.0 * o);
+        }
     }
-    if (lane == 0) { shm[warp] = mm; shq[warp] = vv; }
+    if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < SSA_TREE_CG; ++c) { shm[c][warp] = mm[c]; shq[c][warp] = vv[c]; }
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < SSA_TREE_CG && c0 + threadIdx.x < cells) {
+        const int c = threadIdx.x;
         double a[SSA_TREE_BLOCK / 32], b[SSA_TREE_BLOCK / 32];
 #pragma unroll
-        for (int i = 0; i < SSA_TREE_BLOCK / 32; ++i) { a[i] = shm[i]; b[i] = shq[i]; }
+        for (int i = 0; i < SSA_TREE_BLOCK / 32; ++i) { a[i] = shm[c][i]; b[i] = shq[c][i]; }
         // block levels: subtrees of 256*o leaves, h/2 = 128*o
 #pragma unroll
         for (int o = 1; o < SSA_TREE_BLOCK / 32; o <<= 1)
 #pragma unroll
             for (int i = 0; i + o < SSA_TREE_BLOCK / 32; i += 2 * o) wf_merge_full(a[i], b[i], a[i + o], b[i + o], 128.0 * o);
-        mean = a[0];
-        m2 = b[0];
+        const ssa_u64 o = (c0 + c) * out.row_stride + tile * out.elem_stride + out.offset;
+        out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = a[0]; out.m2[o] = b[0];
     }
 }
 
-// Full tiles only (launched over the first count / SPAN tiles of each row):
-// every thread issues the loads of its 8 leaves in TWO adjacent tiles before
-// reducing either, so each thread keeps 64 B in flight (the kernel is HBM
-// bound); no general-path code, so it stays small in registers.
-__global__ void __launch_bounds__(SSA_TREE_BLOCK, 4) ssa_tree_leaf_full(const int* __restrict__ staging,
-                                                                       ssa_u64 stride, ssa_u64 n_full,
-                                                                       ssa_u64 rows, ssa_tree_out out)
-{
-    const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
-    if (row >= rows) return;
-    const ssa_u64 t0 = 2ull * blockIdx.x;                 // first tile of this block
-    const int* src = staging + row * stride + (ssa_u64)threadIdx.x * 8;
-    const bool two = t0 + 1 < n_full;
-    const int4 a0 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN));
-    const int4 a1 = __ldcs(reinterpret_cast<const int4*>(src + t0 * SSA_TREE_SPAN + 4));
-    int4 b0 = make_int4(0, 0, 0, 0), b1 = b0;
-    if (two) {
-        b0 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN));
-        b1 = __ldcs(reinterpret_cast<const int4*>(src + (t0 + 1) * SSA_TREE_SPAN + 4));
-    }
-    double mean = 0.0, m2 = 0.0;
-    tree_block_full(a0, a1, mean, m2);
-    if (threadIdx.x == 0) {
-        const ssa_u64 o = row * out.row_stride + t0 * out.elem_stride + out.offset;
-        out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
-    }
-    if (two) {
-        __syncthreads();                                   // shared scratch of tree_block_full reused
-        tree_block_full(b0, b1, mean, m2);
-        if (threadIdx.x == 0) {
-            const ssa_u64 o = row * out.row_stride + (t0 + 1) * out.elem_stride + out.offset;
-            out.n[o] = (double)SSA_TREE_SPAN; out.mean[o] = mean; out.m2[o] = m2;
-        }
-    }
-}
-
-// leaves: staging row r = blockIdx.y (+ 65535 * blockIdx.z), ids [0, count);
-// blocks start at tile `first` (the tiles before it are full and reduced by
-// ssa_tree_leaf_full)
-__global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __restrict__ staging, ssa_u64 stride,
-                                                                ssa_u64 count, ssa_u64 rows, ssa_u64 first,
+// General leaves (a tile with ids past `count`: empty leaves n = 0, the identity), tiles from `first`
+__global__ void __launch_bounds__(SSA_TREE_BLOCK) ssa_tree_leaf(const int* __restrict__ staging, ssa_u64 row,
+                                                                ssa_u64 cells, ssa_u64 count, ssa_u64 first,
                                                                 ssa_tree_out out)
 {
-    const ssa_u64 row = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
-    if (row >= rows) return;
+    const ssa_u64 cg = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    const ssa_u64 c0 = cg * SSA_TREE_CG;
+    if (c0 >= cells) return;
     const ssa_u64 tile = first + blockIdx.x;
-    const ssa_u64 base = tile * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
-    const int* src = staging + row * stride;
-    ssa_welford v[8];
-    if (base + 8 <= count && (((uintptr_t)(src + base)) & 15) == 0) {
-        const int4 q0 = *reinterpret_cast<const int4*>(src + base);
-        const int4 q1 = *reinterpret_cast<const int4*>(src + base + 4);
-        v[0] = ssa_welford_leaf(q0.x); v[1] = ssa_welford_leaf(q0.y);
-        v[2] = ssa_welford_leaf(q0.z); v[3] = ssa_welford_leaf(q0.w);
-        v[4] = ssa_welford_leaf(q1.x); v[5] = ssa_welford_leaf(q1.y);
-        v[6] = ssa_welford_leaf(q1.z); v[7] = ssa_welford_leaf(q1.w);
-    } else {
+    const ssa_u64 id0 = tile * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
+    for (int c = 0; c < SSA_TREE_CG; ++c) {               // block-uniform loop (tree_block syncs)
+        ssa_welford v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
-            v[i] = (base + i < count) ? ssa_welford_leaf(src[base + i]) : ssa_welford_empty();
-    }
-    ssa_welford w = tree_block(fold8(v));
-    if (threadIdx.x == 0) {
-        const ssa_u64 o = row * out.row_stride + tile * out.elem_stride + out.offset;
-        out.n[o] = w.n; out.mean[o] = w.mean; out.m2[o] = w.m2;
+            v[i] = (id0 + i < count && c0 + c < cells) ? ssa_welford_leaf(staging[(id0 + i) * row + c0 + c])
+                                                        : ssa_welford_empty();
+        ssa_welford w = tree_block(fold8(v));
+        if (threadIdx.x == 0 && c0 + c < cells) {
+            const ssa_u64 o = (c0 + c) * out.row_stride + tile * out.elem_stride + out.offset;
+            out.n[o] = w.n; out.mean[o] = w.mean; out.m2[o] = w.m2;
+        }
+        __syncthreads();                                  // tree_block's shared scratch is reused
     }
 }
 
@@ -245,24 +241,24 @@ static dim3 tree_grid(ssa_u64 blocks_x, ssa_u64 rows)
     return dim3((unsigned)blocks_x, (unsigned)y, (unsigned)z);
 }
 
-cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 count, ssa_u64 rows,
+cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 row, ssa_u64 count, ssa_u64 cells,
                                  const ssa_tree_out& out, cudaStream_t st, int* launches)
 {
     const ssa_u64 bx = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
-    // full tiles through the division-free kernel (needs 16-byte aligned rows)
-    const bool aligned = stride % 4 == 0 && ((uintptr_t)staging % 16) == 0;
+    const ssa_u64 groups = (cells + SSA_TREE_CG - 1) / SSA_TREE_CG;
+    // full tiles through the division-free kernel (16-byte aligned rows)
+    const bool aligned = row % 8 == 0 && ((uintptr_t)staging % 16) == 0;
     const ssa_u64 n_full = aligned ? count / SSA_TREE_SPAN : 0;
     if (n_full) {
-        ssa_tree_leaf_full<<<tree_grid((n_full + 1) / 2, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, n_full,
-                                                                                          rows, out);
+        ssa_tree_leaf_full<<<tree_grid(n_full, groups), SSA_TREE_BLOCK, 0, st>>>(staging, row, cells, out);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         ++*launches;
     }
     if (bx > n_full || bx == 0) {
         ++*launches;
-        ssa_tree_leaf<<<tree_grid(bx ? bx - n_full : 1, rows), SSA_TREE_BLOCK, 0, st>>>(staging, stride, count, rows,
-                                                                                       n_full, out);
+        ssa_tree_leaf<<<tree_grid(bx ? bx - n_full : 1, groups), SSA_TREE_BLOCK, 0, st>>>(staging, row, cells, count,
+                                                                                         n_full, out);
     }
     return cudaGetLastError();
 }

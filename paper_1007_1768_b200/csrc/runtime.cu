@@ -1446,8 +1446,13 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
 
     // buffers
     DevBuf staging, tiles, croots, statsb, work, dids, dstates, de, dt_, dsum, pconst, ptev, ptord;
-    const ssa_u64 stride = sw ? (C + 3) / 4 * 4 : C;     // rows 16-byte aligned for the vector loads of K3
-    CU(staging.alloc(sizeof(int) * stride * cells, st));
+    // staging is trajectory-major: trajectory rel's grid samples are one row of `stride` ints
+    // (cells rounded up to 8: rows of whole 32-byte sectors), element (rel, k*S + s).  The SSA
+    // kernels write a crossing's S counts contiguously, so a lane fills whole sectors over its
+    // consecutive crossings (no partial-sector read-modify-writes in DRAM), and K3 reads each
+    // trajectory's 8-cell groups as whole sectors.
+    const ssa_u64 stride = (cells + 7) / 8 * 8;
+    CU(staging.alloc(sizeof(int) * stride * C, st));
     const ssa_u64 seg = sw ? sw->N : C;                   // ids per reduced segment (a point, or the chunk)
     const ssa_u64 n_tiles = (seg + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
     if (n_tiles > 1) CU(tiles.alloc(sizeof(double) * 3 * cells * n_tiles, st));
@@ -1612,7 +1617,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         const ssa_u64 n_seg = sw ? cn / sw->N : 1;
         for (ssa_u64 q = 0; q < n_seg; ++q) {
             const ssa_u64 sn = sw ? sw->N : cn;
-            const int* src = staging.as<int>() + q * seg;
+            const int* src = staging.as<int>() + q * seg * stride;
             ssa_tree_out seg_out;
             if (sw) {
                 const RangeOut& pr = sw->roots[(size_t)(cb / sw->N + q)];

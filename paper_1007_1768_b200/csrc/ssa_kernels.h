@@ -31,7 +31,9 @@ struct ssa_tree_out {
 };
 
 
-cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 stride, ssa_u64 count, ssa_u64 rows,
+// staging: trajectory-major, element (trajectory i, cell) at i*row + cell; reduces ids [0, count)
+// of every cell into out (element (cell, tile))
+cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 row, ssa_u64 count, ssa_u64 cells,
                                  const ssa_tree_out& out, cudaStream_t st, int* launches);
 cudaError_t ssa_tree_merge_launch(const ssa_tree_in& in, ssa_u64 count, ssa_u64 rows, const ssa_tree_out& out,
                                   cudaStream_t st);
