@@ -348,15 +348,24 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                                  rj.w <= P.n_dep), P.stats);
             const int nb = apply ? rj.x : 0, ne = apply ? rj.y : 0;
             const int db = apply ? rj.z : 0, de = apply ? rj.w : 0;
-            for (int q = nb + hl; q < ne; q += SSA_HL) {
-                const int ent = nu_ent[q];
-                const int sp = ent & 0xFFFF;
-                SSA_CHECK(sp < SSA_S, P.stats);
-                x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));
+            // (one pass of 16 lanes covers the longest net-change list and, for most models,
+            // the longest dependency list: single passes without loop control then)
+#pragma unroll 2
+            for (int q0 = 0; q0 < SSA_NU_MAX; q0 += SSA_HL) {
+                const int q = nb + q0 + hl;
+                if (q < ne) {
+                    const int ent = nu_ent[q];
+                    const int sp = ent & 0xFFFF;
+                    SSA_CHECK(sp < SSA_S, P.stats);
+                    x[sp] = __dadd_rn(x[sp], (double)(ent >> 16));
+                }
             }
             __syncwarp();
             // a3: the half recomputes dep(j), one entry per lane
-            for (int q = db + hl; q < de; q += SSA_HL) {
+#pragma unroll 2
+            for (int q0 = 0; q0 < SSA_DEP_MAX; q0 += SSA_HL) {
+                const int q = db + q0 + hl;
+                if (q >= de) continue;
                 const ssa_u64 d = dent[q];
                 SSA_CHECK((int)(d & 0x3FFF) < SSA_S && (int)((d >> 14) & 0x3FFF) < SSA_S &&
                           (int)((d >> 32) & 0xFFFF) < SSA_HL * SSA_AR && (int)((d >> 32) & 0xFFFF) % SSA_AR < SSA_P &&
