@@ -55,6 +55,24 @@ def test_union_immigration_death_mid_size(S, kx):
     assert np.array_equal(got.mean, mean) and np.array_equal(got.var, var)
 
 
+@pytest.mark.parametrize("gt,ch", [(1, 0), (2, 0), (7, 32), (0, 32)])
+def test_union_small_tiles(S, monkeypatch, gt, ch):
+    """Tiles of 1, 2 or 7 X-groups and staging chunks of 32 events (the
+    SSA_UNION_GT / SSA_UNION_CH test hooks) put group, tile, chunk and run
+    boundaries everywhere: same bitwise output as the oracle."""
+    net = inputs.immigration_death()
+    n, t_end, seed = 16, 30.0, 11
+    if gt:
+        monkeypatch.setenv("SSA_UNION_GT", str(gt))
+    if ch:
+        monkeypatch.setenv("SSA_UNION_CH", str(ch))
+    for kx in (1, 5, 64):
+        got = S.run_union(S.Model(net), n, t_end, seed, kx)
+        t, mean, var, cnt = _oracle(net, n, t_end, seed, kx)
+        assert np.array_equal(got.times, t) and np.array_equal(got.count, cnt.astype(float))
+        assert np.array_equal(got.mean, mean) and np.array_equal(got.var, var)
+
+
 def test_union_hiv_short(S):
     """The paper's HIV model (Fig. 4's 16 trajectories), over a short horizon."""
     net = inputs.hiv()
