@@ -25,8 +25,9 @@
 // otherwise the compiler re-derives the shared window base (S2R of the CTA id
 // + LEA) inside the event loop.
 //
-// Random numbers: each lane of a half holds (E, u2) of event base + lane for
-// 16 events.  Both halves refill at the same iteration (when either has used
+// Random numbers: lane l of a half draws (E, u2) of event base + l into the half's
+// 16-entry buffer in shared memory; every lane reads event e's pair with one
+// broadcast load.  Both halves refill at the same iteration (when either has used
 // its 16): they then stay in step, so the Philox + plog pass -- a divergent
 // branch when only one half takes it -- runs once per 16 iterations, not twice.
 // A half's early refill re-draws the same counter-based values.
@@ -40,9 +41,25 @@
 #if SSA_K2_HALF
 #define SSA_HL 16
 #define SSA_AR 18                            // row stride of a[] (doubles)
-#define SSA_AWIN (SSA_HL * SSA_AR + ((SSA_S + 1) & ~1))   // per-half window (doubles, even)
+#define SSA_XW ((SSA_S + 2) & ~1)            // x[S] and the constant x_S = 1.0, rounded up to even
+#define SSA_AWIN (SSA_HL * SSA_AR + SSA_XW + 32)   // per-half window (doubles, even): a | x | (E, u2)[16]
 
-#if !SSA_HAS_M3
+#if SSA_K2_FE
+// Fast evaluator (runtime.cu k2_fe_ok): a = k * ((x_a * (x_b - d)) * s) with (d, s) = (0, 1) or,
+// for a reactant of coefficient 2 (b = a), (1, 1/2); a missing factor reads x_S = 1.0.  The
+// operations are those of k2_propensity_d for the same reaction: f1 * f2 with f = x or C(x, 2) =
+// (x (x - 1)) * 0.5 and the absent factor 1.0, then k * h -- so the bits are the same.
+// w: sa | sb << 16 | d << 41 (| slot, reaction in a dependency entry)
+static __device__ __forceinline__ double k2h_fe(ssa_u64 w, double rate, const double* __restrict__ x)
+{
+    const unsigned lo = (unsigned)w, hi = (unsigned)(w >> 32);
+    const double xa = x[lo & 0xFFFFu], xb = x[lo >> 16];
+    const unsigned f = (hi >> 9) & 1u;
+    const double nd = __hiloint2double(f ? (int)0xBFF00000 : (int)0x80000000, 0);   // -1.0 or -0.0
+    const double sc = __hiloint2double((int)(0x3FF00000u - (f << 20)), 0);           // 0.5 or 1.0
+    return __dmul_rn(rate, __dmul_rn(__dmul_rn(xa, __dadd_rn(xb, nd)), sc));
+}
+#elif !SSA_HAS_M3
 // dependency entry: sa | sb << 14 | ma << 28 | mb << 30 | slot << 32 | reaction << 48
 static __device__ __forceinline__ double k2h_propensity(ssa_u64 de, const k2_rxd* __restrict__ rxd,
                                                         const double* __restrict__ x)
@@ -104,11 +121,16 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     double* win0 = (double*)(((unsigned long long)(x0 + SSA_S) + 15ull) & ~15ull);
     double* a = k2h_opaque(win0 + ((size_t)warp * 2 + h) * SSA_AWIN);   // a[l*18 + q]: reaction l*P + q
     double* x = k2h_opaque(win0 + ((size_t)warp * 2 + h) * SSA_AWIN + SSA_HL * SSA_AR);
+    double2* eub = k2h_opaque((double2*)(win0 + ((size_t)warp * 2 + h) * SSA_AWIN + SSA_HL * SSA_AR + SSA_XW));
     const int4* rec = k2h_opaque((const int4*)(k2_smem_raw + P.rec_offset));   // {nu b, nu e, dep b, dep e}
     const int* nu_ent = k2h_opaque((const int*)(k2_smem_raw + P.rec_offset + 16 * SSA_R));
     const ssa_u64* dent = k2h_opaque((const ssa_u64*)(k2_smem_raw + P.dent_offset));
 #if !SSA_HAS_M3
     const k2_rxd* rxd = k2h_opaque((const k2_rxd*)(k2_smem_raw + P.rxd_offset));
+#endif
+#if SSA_K2_FE
+    const double* rt = k2h_opaque((const double*)(k2_smem_raw + P.rxd_offset));     // rate[R]
+    const ssa_u64* __restrict__ rfe = P.rfe;                                          // (start only)
 #endif
     {
         int4* rec_w = (int4*)(k2_smem_raw + P.rec_offset);
@@ -127,7 +149,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) rec_w[i] = P.rec[i];
         for (int i = threadIdx.x; i < P.n_ent; i += SSA_K2_BLOCK) nu_w[i] = P.nu_ent[i];
         for (int i = threadIdx.x; i < P.n_dep; i += SSA_K2_BLOCK) dent_w[i] = P.dent[i];
-#if !SSA_HAS_M3
+#if SSA_K2_FE
+        for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
+            ((double*)(k2_smem_raw + P.rxd_offset))[i] = P.rate[i];
+        }
+#elif !SSA_HAS_M3
         k2_rxd* rxd_w = (k2_rxd*)(k2_smem_raw + P.rxd_offset);
         for (int i = threadIdx.x; i < SSA_R; i += SSA_K2_BLOCK) {
             const ssa_u64 pk = P.pk[i];
@@ -174,7 +200,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
     long long slot = -1;
     ssa_u64 hash = SSA_FNV_OFFSET;
 #endif
-    double Ec = 0.0, U2c = 0.0;              // (E, u2) of event ebase + hl
     bool need_rng = true;                    // this half's buffer is used up (or a new trajectory)
 
     // a1 for this half: take the next id and initialise (half-warp collective)
@@ -189,15 +214,19 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         hash = SSA_FNV_OFFSET;
 #endif
         for (int s = hl; s < SSA_S; s += SSA_HL) x[s] = x0[s];
+        if (hl == 0) x[SSA_S] = 1.0;                 // the fast evaluator's missing factor
         __syncwarp(HALF);
 #pragma unroll
         for (int q = 0; q < SSA_P; ++q) {
             const int j = hl * SSA_P + q;
 #if SSA_HAS_M3
-            a[hl * SSA_AR + q] = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+            const double aj = (live && j < SSA_R) ? k2_propensity(rx[j], x) : 0.0;
+#elif SSA_K2_FE
+            const double aj = (live && j < SSA_R) ? k2h_fe(rfe[j], rt[j], x) : 0.0;
 #else
-            a[hl * SSA_AR + q] = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
+            const double aj = (live && j < SSA_R) ? k2_propensity_d(rxd[j], x) : 0.0;
 #endif
+            a[hl * SSA_AR + q] = aj;
         }
         __syncwarp(HALF);
         t = 0.0; s_next = 0.0; e = 0; ties = 0; k = 0;
@@ -213,12 +242,14 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
             const ssa_u64 ee = e + (ssa_u64)hl;
             const ssa_philox_out o = ssa_philox4x32_10((ssa_u32)ee, (ssa_u32)(ee >> 32), (ssa_u32)id,
                                                        (ssa_u32)(id >> 32), P.key0, P.key1);
-            Ec = -ssa_plog(ssa_u53(o.o1, o.o0), c_plog);
-            U2c = ssa_u53(o.o3, o.o2);
+            eub[hl] = make_double2(-ssa_plog(ssa_u53(o.o1, o.o0), c_plog), ssa_u53(o.o3, o.o2));
             need_rng = false;
+            __syncwarp();
         }
         // a4: lane sum (sequential, two propensities per load), scan over the half (width 16).
-        // (A pairwise-tree lane sum -- a 4-deep chain instead of 16 -- measured 2% slower.)
+        // (A pairwise-tree lane sum -- a 4-deep chain instead of 16 -- measured 2% slower; so did
+        // rows kept in registers with the changed entries reloaded, and row sums re-done only by
+        // the lanes whose rows changed: DESIGN.md §6.)
         double L = 0.0;
 #pragma unroll
         for (int q = 0; q + 1 < SSA_P; q += 2) {
@@ -232,9 +263,10 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
         v = ssa_scan_step_m(v, 8, mk8);
         const double a0 = __shfl_sync(FULL, v, SSA_HL - 1, SSA_HL);
         // a5
-        const int src = (int)(e - ebase);
-        const double E = __shfl_sync(FULL, Ec, src, SSA_HL);
-        const double u2 = __shfl_sync(FULL, U2c, src, SSA_HL);
+        // (E, u2) of event e: one broadcast load (a half with no work left may hold a stale
+        // ebase: the mask keeps its -- unused -- index inside the buffer)
+        const double2 eu = eub[(int)(e - ebase) & 15];
+        const double E = eu.x, u2 = eu.y;
         const unsigned a0hi = (unsigned)__double2hiint(a0);
         const bool fast = a0hi - (123u << 20) < ((1923u - 123u) << 20);   // a0 in [2^-900, 2^901)
         double tn = __dadd_rn(t, ssa_ddiv_inrange(E, a0));
@@ -367,13 +399,17 @@ extern "C" __global__ void __launch_bounds__(SSA_K2_BLOCK, SSA_K2_MINB) ssa_k2(c
                 const int q = db + q0 + hl;
                 if (q >= de) continue;
                 const ssa_u64 d = dent[q];
-                SSA_CHECK((int)(d & 0x3FFF) < SSA_S && (int)((d >> 14) & 0x3FFF) < SSA_S &&
-                          (int)((d >> 32) & 0xFFFF) < SSA_HL * SSA_AR && (int)((d >> 32) & 0xFFFF) % SSA_AR < SSA_P &&
-                          (int)(d >> 48) < SSA_R, P.stats);
-#if !SSA_HAS_M3
-                a[(unsigned)(d >> 32) & 0xFFFFu] = k2h_propensity(d, rxd, x);
+                const unsigned dhi = (unsigned)(d >> 32);
+                SSA_CHECK((int)(dhi & 0x1FFu) < SSA_HL * SSA_AR && (int)(dhi & 0x1FFu) % SSA_AR < SSA_P &&
+                          (int)(dhi >> 16) < SSA_R, P.stats);
+#if SSA_K2_FE
+                SSA_CHECK((int)(d & 0xFFFF) <= SSA_S && (int)((d >> 16) & 0xFFFF) <= SSA_S, P.stats);
+                a[dhi & 0x1FFu] = k2h_fe(d, rt[dhi >> 16], x);
+#elif !SSA_HAS_M3
+                SSA_CHECK((int)(d & 0x3FFF) < SSA_S && (int)((d >> 14) & 0x3FFF) < SSA_S, P.stats);
+                a[dhi & 0x1FFu] = k2h_propensity(d, rxd, x);
 #else
-                a[(unsigned)(d >> 32) & 0xFFFFu] = k2_propensity(rx[(int)(d >> 48)], x);
+                a[dhi & 0x1FFu] = k2_propensity(rx[(int)(dhi >> 16)], x);
 #endif
             }
             __syncwarp();

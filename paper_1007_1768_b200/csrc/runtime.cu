@@ -100,6 +100,7 @@ struct K2Dev {
     int *dep_off = nullptr, *dep_ent = nullptr;
     int4* rec = nullptr;                    // half-warp path: per-reaction {nu b, nu e, dep b, dep e}
     ssa_u64* dent = nullptr;                // half-warp path: resolved dependency entries
+    ssa_u64* rfe = nullptr;                 // half-warp path: fast-evaluator terms per reaction
     std::map<std::string, K2Kernel> kern;   // "block/dump" -> NVRTC-compiled K2
 };
 
@@ -917,6 +918,34 @@ static bool has_m3(const ssa_model& m)
     return false;
 }
 
+// Half-warp fast evaluator (k2_half.cuh, SSA_K2_FE): every propensity has the form
+// k * ((x_a * (x_b - d)) * s) -- no modifier, no gates, and a reactant multiset that is
+// empty, {i}, {i, j} with coefficients 1, or {2i} (x_S = 1.0 stands in for a missing
+// factor).  Each form performs exactly the operations of the general evaluator.
+static bool k2_fe_ok(const ssa_model& m)
+{
+    for (auto& q : m.rx) {
+        if (q.mod_sp >= 0 || !q.gates.empty()) return false;
+        if (!q.mass_action) continue;
+        if (q.reac.size() > 2) return false;
+        if (q.reac.size() == 2 && (q.reac[0].second != 1 || q.reac[1].second != 1)) return false;
+        if (q.reac.size() == 1 && q.reac[0].second > 2) return false;
+    }
+    return true;
+}
+
+// (species a, species b, flag d = 1 / s = 1/2) of reaction j's fast-evaluator form
+static void k2_fe_terms(const ssa_model& m, int j, ssa_u64* sa, ssa_u64* sb, ssa_u64* f)
+{
+    const RxI& q = m.rx[j];
+    const ssa_u64 one = (ssa_u64)m.S;
+    *sa = one; *sb = one; *f = 0;
+    if (!q.mass_action || q.reac.empty()) return;
+    if (q.reac.size() == 2) { *sa = (ssa_u64)q.reac[0].first; *sb = (ssa_u64)q.reac[1].first; return; }
+    *sa = (ssa_u64)q.reac[0].first;
+    if (q.reac[0].second == 2) { *sb = *sa; *f = 1; }
+}
+
 // rx: whether the packed table is staged (models with coefficient-3 reactants)
 static size_t k2_rxd_offset(int S, int R, int P, int n_ent, int n_dep, int block, bool half = false, bool rx = true)
 {
@@ -933,17 +962,17 @@ static size_t k2_smem_bytes(int S, int R, int P, int n_ent, int n_dep, int block
 }
 
 // half-warp layout (k2_half.cuh): rx[R] (coefficient-3 models) | x0[S] | (16-aligned) per warp, per
-// half (a[16 x 18] | x[S rounded up to even]) | rec[R] (16 B) | nu_ent | dent[n_dep] (8 B) | rxd[R] (40 B,
-// 16-aligned)
+// half (a[16 x 18] | x[S + 1 rounded up to even] | (E, u2)[16]) | rec[R] (16 B) | nu_ent | dent[n_dep] (8 B) |
+// (16-aligned) rxd[R] (40 B) -- or, with the fast evaluator, rate[R] (8 B)
 struct K2HalfLayout {
     size_t rec = 0, dent = 0, rxd = 0, bytes = 0;
 };
-static K2HalfLayout k2_half_layout(int S, int R, int P, int n_ent, int n_dep, int block, bool rx)
+static K2HalfLayout k2_half_layout(int S, int R, int P, int n_ent, int n_dep, int block, bool rx, bool fe)
 {
     (void)P;
     K2HalfLayout L;
     const size_t warps = (size_t)(block / 32);
-    const size_t awin = 16 * 18 + (((size_t)S + 1) & ~(size_t)1);
+    const size_t awin = 16 * 18 + (((size_t)S + 2) & ~(size_t)1) + 32;
     size_t b = (rx ? 32 * (size_t)R : 0) + 8 * (size_t)S;
     b = (b + 15) & ~(size_t)15;
     b += warps * 2 * 8 * awin;
@@ -955,7 +984,7 @@ static K2HalfLayout k2_half_layout(int S, int R, int P, int n_ent, int n_dep, in
     b += 8 * (size_t)std::max(n_dep, 1);
     b = (b + 15) & ~(size_t)15;
     L.rxd = b;
-    L.bytes = b + (rx ? 0 : 40 * (size_t)R);
+    L.bytes = b + (rx ? 0 : (fe ? 8 * (size_t)R : 40 * (size_t)R));
     return L;
 }
 
@@ -987,6 +1016,7 @@ static std::string gen_k2_model(const ssa_model& m, int P, int block, int minb, 
     o << "#define SSA_S " << m.S << "\n#define SSA_R " << m.R << "\n#define SSA_P " << P << "\n#define SSA_K2_BLOCK "
       << block << "\n#define SSA_K2_MINB " << minb << "\n#define SSA_K2_DUMP " << (dump ? 1 : 0)
       << "\n#define SSA_K2_HALF " << (half ? 1 : 0)
+      << "\n#define SSA_K2_FE " << ((half && k2_fe_ok(m)) ? 1 : 0)
       << "\n#define SSA_HAS_M3 " << m3 << "\n#define SSA_HAS_GATES " << gates << "\n#define SSA_HAS_MODS " << mods << "\n#define SSA_NU_MAX " << nu_max << "\n#define SSA_DEP_MAX " << dep_max
       << "\n";
     o << "__constant__ double c_plog[8] = SSA_PLOG_COEF_INIT;\n";
@@ -1070,16 +1100,36 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         const int PH = std::max(1, (R + 15) / 16);
         std::vector<int4> rec(R1);
         for (int j = 0; j < R; ++j) rec[j] = make_int4(nu_off[j], nu_off[j + 1], dep_off[j], dep_off[j + 1]);
-        std::vector<ssa_u64> dent(dep_ent.size(), 0);
-        for (size_t q = 0; q < (size_t)n_dep_real; ++q) {
-            const int jj = dep_ent[q];
-            const ssa_u64 w = pk[jj];
-            const int n = (int)(w & 3ull);
-            const ssa_u64 sa = n >= 1 ? (w >> 2) & 0x3FFF : 0, sb = n >= 2 ? (w >> 18) & 0x3FFF : 0;
-            const ssa_u64 ma = n >= 1 ? (w >> 16) & 3 : 0, mb = n >= 2 ? (w >> 32) & 3 : 0;
-            const ssa_u64 slot = (ssa_u64)((jj / PH) * 18 + jj % PH);   // a[l*18 + q], reaction l*PH + q
-            dent[q] = sa | (sb << 14) | (ma << 28) | (mb << 30) | (slot << 32) | ((ssa_u64)jj << 48);
+        const bool fe = k2_fe_ok(m);
+        std::vector<ssa_u64> dent(dep_ent.size(), 0), rfe(R1, 0);
+        for (int j = 0; j < R; ++j) {
+            for (int q = dep_off[j]; q < dep_off[j + 1]; ++q) {
+                const int jj = dep_ent[q];
+                const ssa_u64 row = (ssa_u64)(jj / PH);
+                const ssa_u64 slot = row * 18 + (ssa_u64)(jj % PH);   // a[l*18 + q], reaction l*PH + q
+                ssa_u64 w;
+                if (fe) {
+                    // sa | sb << 16 | slot << 32 | d << 41 | reaction << 48
+                    ssa_u64 sa, sb, f;
+                    k2_fe_terms(m, jj, &sa, &sb, &f);
+                    w = sa | (sb << 16) | (f << 41);
+                } else {
+                    // sa | sb << 14 | ma << 28 | mb << 30 | slot << 32 | reaction << 48
+                    const ssa_u64 pw = pk[jj];
+                    const int n = (int)(pw & 3ull);
+                    const ssa_u64 sa = n >= 1 ? (pw >> 2) & 0x3FFF : 0, sb = n >= 2 ? (pw >> 18) & 0x3FFF : 0;
+                    const ssa_u64 ma = n >= 1 ? (pw >> 16) & 3 : 0, mb = n >= 2 ? (pw >> 32) & 3 : 0;
+                    w = sa | (sb << 14) | (ma << 28) | (mb << 30);
+                }
+                dent[q] = w | (slot << 32) | ((ssa_u64)jj << 48);
+            }
         }
+        if (fe)
+            for (int j = 0; j < R; ++j) {
+                ssa_u64 sa, sb, f;
+                k2_fe_terms(m, j, &sa, &sb, &f);
+                rfe[j] = sa | (sb << 16) | (f << 41);
+            }
         // image layout (8-byte aligned sections): pk | gw | rate | modc | x0 | nu_off | nu_ent | dep_off | dep_ent
         const size_t o_pk = 0, o_gw = o_pk + 8 * R1, o_rate = o_gw + 8 * R1, o_modc = o_rate + 8 * R1,
                      o_x0 = o_modc + 8 * R1;
@@ -1089,7 +1139,8 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         const size_t o_dent = o_doff + ((4 * dep_off.size() + 7) & ~(size_t)7);
         const size_t o_rec = (o_dent + 4 * dep_ent.size() + 15) & ~(size_t)15;
         const size_t o_hd = o_rec + 16 * R1;
-        const size_t bytes = o_hd + 8 * dent.size();
+        const size_t o_rfe = o_hd + 8 * dent.size();
+        const size_t bytes = o_rfe + 8 * R1;
         CU(cudaMallocHost(&k.host_image, bytes));
         char* h = (char*)k.host_image;
         memcpy(h + o_pk, pk.data(), 8 * R1);
@@ -1103,6 +1154,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         memcpy(h + o_dent, dep_ent.data(), 4 * dep_ent.size());
         memcpy(h + o_rec, rec.data(), 16 * R1);
         memcpy(h + o_hd, dent.data(), 8 * dent.size());
+        memcpy(h + o_rfe, rfe.data(), 8 * R1);
         CU(cudaMalloc(&k.dev_image, bytes));
         CU(cudaMemcpy(k.dev_image, k.host_image, bytes, cudaMemcpyHostToDevice));
         char* d = (char*)k.dev_image;
@@ -1117,6 +1169,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         k.dep_ent = (int*)(d + o_dent);
         k.rec = (int4*)(d + o_rec);
         k.dent = (ssa_u64*)(d + o_hd);
+        k.rfe = (ssa_u64*)(d + o_rfe);
         k.image_bytes = bytes;
         k.P = P;
         k.n_ent = n_ent_real;
@@ -1139,7 +1192,7 @@ static ssa_status ensure_k2(const ssa_model& m, int dev, int block, int minb, bo
         CU(cudaLibraryGetKernel(&kk.fn, kk.lib, "ssa_k2"));
         const bool m3 = has_m3(m);
         if (half) {
-            const K2HalfLayout hl = k2_half_layout(S, R, PL, k.n_ent, k.n_dep, block, m3);
+            const K2HalfLayout hl = k2_half_layout(S, R, PL, k.n_ent, k.n_dep, block, m3, k2_fe_ok(m));
             kk.smem = hl.bytes;
             kk.rxd_offset = hl.rxd;
             kk.rec_offset = hl.rec;
@@ -1599,7 +1652,7 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
             p.pk = k2->pk; p.gw = k2->gw; p.rate = k2->rate; p.modc = k2->modc; p.x0 = k2->x0; p.nu_off = k2->nu_off; p.nu_ent = k2->nu_ent;
             p.dep_off = k2->dep_off; p.dep_ent = k2->dep_ent;
             p.rxd_offset = k2k->rxd_offset;
-            p.rec = k2->rec; p.dent = k2->dent;
+            p.rec = k2->rec; p.dent = k2->dent; p.rfe = k2->rfe;
             p.rec_offset = k2k->rec_offset; p.dent_offset = k2k->dent_offset;
             p.id_begin = cb; p.n_ids = cn; p.staging = staging.as<int>(); p.stride = stride; p.dt = dt; p.K = K;
             p.key0 = key0; p.key1 = key1; p.work = work.as<ssa_u64>() + ch;
