@@ -49,6 +49,14 @@ def profiled_activity(workload: str, kernel: str):
             "source": e.get("activity_source")}
 
 
+def lsu_wavefronts_per_event(workload: str):
+    """Shared-memory (LSU data pipe) wavefronts per applied event of K2 from the committed ncu
+    capture named in profiles/traffic.json (None when absent)."""
+    if not os.path.exists(TRAFFIC_FILE):
+        return None
+    return json.load(open(TRAFFIC_FILE)).get(workload, {}).get("ssa_k2", {}).get("lsu_wavefronts_per_event")
+
+
 def measured_traffic(workload: str, kernel: str, default_size: bool):
     """DRAM read+write bytes per launch of `kernel` from the committed ncu pass (profiles/traffic.json),
     for the default-size workload only (other sizes: None)."""
@@ -682,6 +690,20 @@ def main():
                                  "alg_fp64_thread_instr_per_event": F,
                                  "peak_basis": f"{n_sm} SMs x 4 SMSPs x {FP64_PER_SMSP_CLK} FP64 warp-inst/clk "
                                                f"(scripts/pipe_peaks.cu) x {sm_max:.0f} MHz"}
+
+    if path != 1:
+        # K2's co-bound: the shared-memory (LSU data) pipe, one wavefront per clock per SM; K2's
+        # propensity rows, state, model tables and shuffles all pass through it.
+        # Wavefronts per applied event from the committed ncu capture of the same kernel.
+        W = lsu_wavefronts_per_event(workload)
+        if W:
+            l_ach = per_rank_events * W / (k1_ms / 1e3) / 1e9
+            l_peak = n_sm * sm_max * 1e6 / 1e9
+            roofline["lsu_pipe"] = {"achieved": l_ach, "peak": l_peak, "unit": "Gwavefronts/s",
+                                    "frac": l_ach / l_peak, "wavefronts_per_event": W,
+                                    "peak_basis": f"{n_sm} SMs x 1 shared-memory wavefront/clk x {sm_max:.0f} MHz",
+                                    "source": "profiles/traffic.json (ncu l1tex__data_pipe_lsu_wavefronts_mem_shared "
+                                              "per applied event)"}
 
     # secondary: the chunk reduction (K3) reads the staged grid samples once -- HBM bound
     hbm_peak = float(peaks.get("hbm_gbs", 7700.0))
