@@ -119,15 +119,17 @@ static __device__ __forceinline__ void fold8_full(const int (&c)[8], double& mm,
     }
 }
 
-// Full tiles only: tile = blockIdx.x (< count / SPAN), cell group = blockIdx.y (+ 65535 * z)
+// Full tiles only: cell group = blockIdx.x, tile = blockIdx.y (+ 65535 * z) (< count / SPAN).  Consecutive
+// blocks take consecutive cell groups of one tile, so the blocks resident together read whole
+// trajectory rows front to back (DRAM page locality) instead of one 32-byte sector per row.
 __global__ void __launch_bounds__(SSA_TREE_BLOCK, 2) ssa_tree_leaf_full(const int* __restrict__ staging,
                                                                        ssa_u64 row, ssa_u64 cells, ssa_tree_out out)
 {
     __shared__ double shm[SSA_TREE_CG][SSA_TREE_BLOCK / 32], shq[SSA_TREE_CG][SSA_TREE_BLOCK / 32];
-    const ssa_u64 cg = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
+    const ssa_u64 cg = (ssa_u64)blockIdx.x;
     const ssa_u64 c0 = cg * SSA_TREE_CG;
     if (c0 >= cells) return;
-    const ssa_u64 tile = blockIdx.x;
+    const ssa_u64 tile = (ssa_u64)blockIdx.y + 65535ull * blockIdx.z;
     const ssa_u64 id0 = tile * SSA_TREE_SPAN + (ssa_u64)threadIdx.x * 8;
     int v[SSA_TREE_CG][8];                                // [cell][leaf]
 #pragma unroll
@@ -250,7 +252,9 @@ cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 row, ssa_u64 count,
     const bool aligned = row % 8 == 0 && ((uintptr_t)staging % 16) == 0;
     const ssa_u64 n_full = aligned ? count / SSA_TREE_SPAN : 0;
     if (n_full) {
-        ssa_tree_leaf_full<<<tree_grid(n_full, groups), SSA_TREE_BLOCK, 0, st>>>(staging, row, cells, out);
+        const dim3 g((unsigned)groups, (unsigned)(n_full < 65535ull ? n_full : 65535ull),
+                     (unsigned)((n_full + 65534ull) / 65535ull));
+        ssa_tree_leaf_full<<<g, SSA_TREE_BLOCK, 0, st>>>(staging, row, cells, out);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         ++*launches;

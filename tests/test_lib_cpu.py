@@ -216,3 +216,19 @@ def test_species_names(ssa):
     assert lib.ssa_model_species_name(m.handle, 99) is None
     bad = (C.c_char_p * m.S)(*([b"x"] * (m.S - 1) + [None]))
     assert lib.ssa_model_set_names(m.handle, bad) == 1
+
+
+def test_halfwarp_fast_evaluator_selection():
+    """The half-warp K2's fast evaluator (k2_half.cuh SSA_K2_FE) is compiled in only for plain
+    mass-action networks (no modifier, no gate, reactant multisets {}, {i}, {i, j}, {2i}); HIV
+    (modifiers) and coefficient-3 networks keep the general evaluator."""
+    import inputs
+    from paper_1007_1768_b200 import ssa as S
+    half = 2
+    syn = S.Model(inputs.config(3).network)
+    assert "#define SSA_K2_FE 1" in S._k2_source(syn, 256, half)
+    assert "#define SSA_K2_FE 0" in S._k2_source(syn, 256, 0)          # one-trajectory-per-warp K2
+    hiv = S.Model(inputs.config(2).network)
+    assert "#define SSA_K2_FE 0" in S._k2_source(hiv, 256, half)
+    dim = S.Model(inputs.config(1).network)                           # 2 S1 -> S2: the {2i} form
+    assert "#define SSA_K2_FE 1" in S._k2_source(dim, 256, half)
