@@ -134,10 +134,12 @@ __global__ void __launch_bounds__(SSA_TREE_BLOCK, 2) ssa_tree_leaf_full(const in
     int v[SSA_TREE_CG][8];                                // [cell][leaf]
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int4* p = reinterpret_cast<const int4*>(staging + (id0 + i) * row + c0);
-        const int4 a = p[0], b = p[1];
-        v[0][i] = a.x; v[1][i] = a.y; v[2][i] = a.z; v[3][i] = a.w;
-        v[4][i] = b.x; v[5][i] = b.y; v[6][i] = b.z; v[7][i] = b.w;
+        // one 32-byte load per id (LDG.256): the whole sector in one request (two 16-byte loads
+        // sent 2.5x the bytes to L2, profiles/r2z_k3_summary.txt)
+        asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v[0][i]), "=r"(v[1][i]), "=r"(v[2][i]), "=r"(v[3][i]), "=r"(v[4][i]), "=r"(v[5][i]),
+                       "=r"(v[6][i]), "=r"(v[7][i])
+                     : "l"(staging + (id0 + i) * row + c0));
     }
     double mm[SSA_TREE_CG], vv[SSA_TREE_CG];
 #pragma unroll
@@ -248,8 +250,8 @@ cudaError_t ssa_tree_leaf_launch(const int* staging, ssa_u64 row, ssa_u64 count,
 {
     const ssa_u64 bx = (count + SSA_TREE_SPAN - 1) / SSA_TREE_SPAN;
     const ssa_u64 groups = (cells + SSA_TREE_CG - 1) / SSA_TREE_CG;
-    // full tiles through the division-free kernel (16-byte aligned rows)
-    const bool aligned = row % 8 == 0 && ((uintptr_t)staging % 16) == 0;
+    // full tiles through the division-free kernel (32-byte aligned rows: one sector per id and group)
+    const bool aligned = row % 8 == 0 && ((uintptr_t)staging % 32) == 0;
     const ssa_u64 n_full = aligned ? count / SSA_TREE_SPAN : 0;
     if (n_full) {
         const dim3 g((unsigned)groups, (unsigned)(n_full < 65535ull ? n_full : 65535ull),
