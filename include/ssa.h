@@ -129,7 +129,9 @@ uint64_t ssa_grid_size(double t_end, double sample_dt);
 /* --------------------------------------------------------------- options */
 /* THREAD: one trajectory per thread, sequential summation order; WARP: one
  * trajectory per warp, order warp32; HALFWARP: two trajectories per warp
- * (16 lanes each), order warp16. */
+ * (16 lanes each), order warp16s (R34; the oracle's mode 3).  The order
+ * fixes the rounding of the total and of the selection, so results are bitwise
+ * reproducible per path (result->path_used reports it). */
 enum { SSA_PATH_AUTO = 0, SSA_PATH_THREAD = 1, SSA_PATH_WARP = 2, SSA_PATH_HALFWARP = 3 };
 enum { SSA_REDUCE_MEAN = 1, SSA_REDUCE_VAR = 2 };
 
