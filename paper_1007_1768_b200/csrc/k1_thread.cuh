@@ -74,6 +74,18 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     bool may_suspend = true;                          // a resumed lane first crosses its pending grid point
     const bool mig = P.mig_thresh > 0 && !P.spread;
     volatile ssa_u64* const mctl = P.mig_ctl;
+    // time-sliced trajectories (P.seg > 1): job q of [0, seg * n_ids) is phase q / n_ids of
+    // trajectory q % n_ids; phase p runs from the grid crossing where phase p - 1 stopped to the
+    // one at index kb(p) = (p + 1) G / seg (the last phase to the end).  Jobs are handed out in
+    // order, so the launch ends with the last phases -- 1/seg of a trajectory each -- instead of
+    // whole trajectories running on an emptying GPU.  seg_ready[rel] = the next phase to run
+    // (seg: finished); the state crosses phases through seg_buf as (x[S], t, e, k, hash, ties).
+    const int seg = (P.seg > 1 && !P.spread && !mig) ? P.seg : 1;
+    int seg_p = 0;
+    long long seg_kb = K + 2;
+    auto seg_kb_of = [&](int p) -> long long {
+        return p + 1 < seg ? (long long)(((ssa_u64)(p + 1) * G) / (ssa_u64)seg) : K + 2;
+    };
 #endif
     // plog's table in shared memory (lanes index it independently)
     __shared__ __align__(16) double s_plog_[128][4];
@@ -107,6 +119,41 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #if SSA_K1_SWEEP
     ssa_u64 my_ptl = 0;                 // this lane's sweep point (chunk-local)
 #endif
+#if SSA_K1_MIG
+    // time slices: trajectory rel's state between phases, S + 6 doubles at seg_buf[rel]
+    auto seg_save = [&]() {
+        double* st = P.seg_buf + rel * (ssa_u64)(SSA_S + 6);
+#pragma unroll
+        for (int s = 0; s < SSA_S; ++s) __stcg(st + s, x[s]);
+        __stcg(st + SSA_S, t);
+        __stcg(st + SSA_S + 1, __longlong_as_double((long long)e));
+        __stcg(st + SSA_S + 2, __longlong_as_double(k));
+        __stcg(st + SSA_S + 3, __longlong_as_double((long long)ties));
+        __stcg(st + SSA_S + 4, __longlong_as_double((long long)hash));
+    };
+    auto seg_restore = [&](ssa_u64 r) {
+        const double* st = P.seg_buf + r * (ssa_u64)(SSA_S + 6);
+#pragma unroll
+        for (int s = 0; s < SSA_S; ++s) x[s] = __ldcg(st + s);     // L2: written by another SM
+        t = __ldcg(st + SSA_S);
+        e = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 1));
+        k = __double_as_longlong(__ldcg(st + SSA_S + 2));
+        ties = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 3));
+        hash = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 4));
+        rel = r;
+        vid = P.id_begin + rel;
+        id = vid;
+#if SSA_K1_DUMP
+        slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
+#endif
+        ssa_khat(x, kh SSA_KP_ARG);
+        s_next = (k <= K) ? __dmul_rn((double)k, dt) : INF;
+        status = 0; absorbed = 0; err_r = -1;
+#if SSA_CSKIP
+        lo_dirty = true;
+#endif
+    };
+#endif
     // a1: take the next trajectory id (atomic counter) and initialise it
     auto start = [&]() -> bool {
 #if SSA_K1_SWEEP
@@ -131,8 +178,30 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             kp = s_k + ptl * (ssa_u64)P.n_pool;
         }
 #else
-        rel = atomicAdd(P.work, 1ull);
-        if (rel >= P.n_ids) return false;
+#if SSA_K1_MIG
+        if (seg > 1) {
+            for (;;) {
+                const ssa_u64 q = atomicAdd(P.work, 1ull);
+                if (q >= (ssa_u64)seg * P.n_ids) return false;
+                const int ph = (int)(q / P.n_ids);
+                rel = q - (ssa_u64)ph * P.n_ids;
+                if (ph == 0) { seg_p = 0; seg_kb = seg_kb_of(0); break; }   // a fresh trajectory (below)
+                // phase ph - 1 of this trajectory was handed out n_ids jobs ago: wait for its state
+                unsigned r;
+                while ((r = ((volatile unsigned*)P.seg_ready)[rel]) < (unsigned)ph) __nanosleep(64);
+                if (r > (unsigned)ph) continue;      // finished, or stopped at a later boundary
+                __threadfence();
+                seg_restore(rel);
+                seg_p = ph;
+                seg_kb = seg_kb_of(ph);
+                return true;
+            }
+        } else
+#endif
+        {
+            rel = atomicAdd(P.work, 1ull);
+            if (rel >= P.n_ids) return false;
+        }
 #endif
         vid = P.id_begin + rel;
 #if !SSA_K1_SWEEP
@@ -328,6 +397,18 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 continue;
             }
 #endif
+#if SSA_K1_MIG
+            // time slice: at the first crossing at or past this phase's boundary, hand the
+            // trajectory to its next phase's job (the candidate is a function of (x, t, e): the
+            // resumed lane recomputes it bit for bit and processes this crossing)
+            if (seg > 1 && k >= seg_kb && status == 0 && fast) {
+                seg_save();
+                __threadfence();
+                atomicExch(&P.seg_ready[rel], (unsigned)(seg_p + 1));
+                live = start();
+                continue;
+            }
+#endif
             bool fin = false;
             if (!fast) {
                 if (a0 > 0.0 && a0 < INF) {
@@ -377,6 +458,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             }
             if (fin) {
                 // trajectory done: per-trajectory records, then refill (a1)
+#if SSA_K1_MIG
+                if (seg > 1) atomicExch(&P.seg_ready[rel], (unsigned)seg);   // later phases: nothing to do
+#endif
                 my_events += e;
                 my_ties += ties;
 #if SSA_K1_SWEEP

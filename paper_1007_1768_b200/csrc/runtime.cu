@@ -59,6 +59,9 @@ static ssa_status fail(ssa_status st, const char* fmt, ...)
     } while (0)
 
 // ------------------------------------------------------------------ model
+// K1 phases per trajectory (time slicing, k1_thread.cuh); profiles/r2z_seg_ab.txt
+#define SSA_TSLICES 32
+
 struct RxI {
     std::vector<std::pair<int, int>> reac;   // (species, coef) in declared order
     std::vector<std::pair<int, long long>> nu; // nonzero net change, species ascending
@@ -1549,6 +1552,19 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         CU(migr.alloc(sizeof(unsigned) * mig_cap, st));
         CU(migc.alloc(sizeof(ssa_u64) * 4, st));
     }
+    // time-sliced trajectories (K1 plain / dump / profiling variants): each trajectory runs as
+    // SSA_TSLICES phases handed out phase by phase, so a launch ends with short last phases instead
+    // of whole trajectories on an emptying GPU (bitwise neutral).  Used when a launch
+    // has more trajectories than resident lanes; SSA_K1_SEG overrides the phase count (1 = off).
+    int tslices = SSA_TSLICES;
+    if (const char* sv = getenv("SSA_K1_SEG")) tslices = std::max(1, std::min(64, atoi(sv)));
+    if (path != SSA_PATH_THREAD || sw || rec || spread || mig || (ssa_u64)C <= (ssa_u64)grid * (ssa_u64)block)
+        tslices = 1;
+    DevBuf segb, segr;
+    if (tslices > 1) {
+        CU(segb.alloc(sizeof(double) * ((size_t)m->S + 6) * (size_t)C, st));
+        CU(segr.alloc(sizeof(unsigned) * (size_t)C, st));
+    }
     CU(statsb.alloc(sizeof(ssa_dev_stats), st));
     CU(work.alloc(sizeof(ssa_u64) * n_chunks, st));
     CU(cudaMemsetAsync(statsb.p, 0, sizeof(ssa_dev_stats), st));
@@ -1629,6 +1645,12 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
                 p.mig_ready = migr.as<unsigned>();
                 p.mig_cap = mig_cap;
                 p.mig_ctl = migc.as<ssa_u64>();
+            }
+            if (tslices > 1 && cn > (ssa_u64)grid * (ssa_u64)block) {
+                CU(cudaMemsetAsync(segr.p, 0, sizeof(unsigned) * (size_t)cn, st));
+                p.seg = tslices;
+                p.seg_buf = segb.as<double>();
+                p.seg_ready = segr.as<unsigned>();
             }
             void* args[] = {&p};
             CU(cudaLaunchKernel((const void*)k1->fn, dim3(grid), dim3(spread ? 32 : block), args, smem, st));

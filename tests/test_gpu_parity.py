@@ -250,6 +250,46 @@ def test_tail_compaction_is_bitwise_neutral(S, monkeypatch, capfd):
         assert np.array_equal(r.mean, a.mean) and np.array_equal(r.m2, a.m2) and r.events == a.events
 
 
+def test_time_slices_are_bitwise_neutral(S, monkeypatch):
+    """K1 time-sliced trajectories (SSA_K1_SEG = phases per trajectory): the jobs
+    are (phase, trajectory) pairs handed out phase by phase, a trajectory's state crosses phases
+    through memory at a grid crossing, and the resumed lane recomputes the pending candidate.
+    1, 2, 3 and 7 phases give bitwise identical grids, counters and dumps (ragged chunk, early
+    die-outs and absorbing trajectories included), and the dumped trajectories match the oracle."""
+    cfg = inputs.config(1)
+    m = S.Model(cfg.network)
+    n = 20000
+    ids = np.arange(0, n, 37, dtype=np.uint64)
+    runs = {}
+    for sv in ("1", "2", "3", "7"):
+        monkeypatch.setenv("SSA_K1_SEG", sv)
+        runs[sv] = S.run(m, n, cfg.t_end, cfg.dt, cfg.seed, path=THREAD, dump_ids=ids, chunk=8192)
+    off = runs["1"]
+    for sv in ("2", "3", "7"):
+        r = runs[sv]
+        assert np.array_equal(r.mean, off.mean) and np.array_equal(r.var, off.var) and np.array_equal(r.m2, off.m2)
+        assert r.events == off.events and r.near_ties == off.near_ties
+        for f in ("states", "events_at", "time_at"):
+            assert np.array_equal(getattr(r.dump, f), getattr(off.dump, f)), (sv, f)
+        assert r.dump.summary.tobytes() == off.dump.summary.tobytes()
+    gx, ge, gt, sm = oracle_replay(cfg.network, ids[:64], cfg.seed, cfg.t_end, cfg.dt, 0)
+    r = runs["7"]
+    sub = S.Dump(ids[:64], r.dump.states[:64], r.dump.events_at[:64], r.dump.time_at[:64], r.dump.summary[:64])
+    assert_dump_equal(sub, gx, ge, gt, sm)
+    # HIV (profiling run, then the hot-set variant; ~11% of the trajectories die out early)
+    hm = S.Model(inputs.config(2).network)
+    hids = np.arange(0, 40000, 211, dtype=np.uint64)
+    monkeypatch.setenv("SSA_K1_SEG", "1")
+    a = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD, dump_ids=hids)
+    a2 = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD)
+    monkeypatch.setenv("SSA_K1_SEG", "4")
+    b = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD, dump_ids=hids)
+    c = S.run(hm, 40000, 6.0, 1.0, 3, path=THREAD)
+    for r in (a2, b, c):
+        assert np.array_equal(r.mean, a.mean) and np.array_equal(r.m2, a.m2) and r.events == a.events
+    assert np.array_equal(b.dump.states, a.dump.states) and b.dump.summary.tobytes() == a.dump.summary.tobytes()
+
+
 def test_reduction_paths_bitwise_equal(S):
     """K3's full-tile kernel takes an integer fast path for 8-leaf groups below
     2^20 and the fp64 Chan merges otherwise; both must give the canonical
