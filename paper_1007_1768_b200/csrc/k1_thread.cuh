@@ -74,13 +74,19 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
     bool may_suspend = true;                          // a resumed lane first crosses its pending grid point
     const bool mig = P.mig_thresh > 0 && !P.spread;
     volatile ssa_u64* const mctl = P.mig_ctl;
+#endif
+#if SSA_K1_SEG
     // time-sliced trajectories (P.seg > 1): job q of [0, seg * n_ids) is phase q / n_ids of
     // trajectory q % n_ids; phase p runs from the grid crossing where phase p - 1 stopped to the
     // one at index kb(p) = (p + 1) G / seg (the last phase to the end).  Jobs are handed out in
     // order, so the launch ends with the last phases -- 1/seg of a trajectory each -- instead of
     // whole trajectories running on an emptying GPU.  seg_ready[rel] = the next phase to run
     // (seg: finished); the state crosses phases through seg_buf as (x[S], t, e, k, hash, ties).
+#if SSA_K1_MIG
     const int seg = (P.seg > 1 && !P.spread && !mig) ? P.seg : 1;
+#else
+    const int seg = (P.seg > 1 && !P.spread) ? P.seg : 1;
+#endif
     int seg_p = 0;
     long long seg_kb = K + 2;
     auto seg_kb_of = [&](int p) -> long long {
@@ -119,7 +125,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
 #if SSA_K1_SWEEP
     ssa_u64 my_ptl = 0;                 // this lane's sweep point (chunk-local)
 #endif
-#if SSA_K1_MIG
+#if SSA_K1_SEG
     // time slices: trajectory rel's state between phases, S + 6 doubles at seg_buf[rel]
     auto seg_save = [&]() {
         double* st = P.seg_buf + rel * (ssa_u64)(SSA_S + 6);
@@ -142,7 +148,9 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         hash = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 4));
         rel = r;
         vid = P.id_begin + rel;
-        id = vid;
+#if !SSA_K1_SWEEP
+        id = vid;                              // (a sweep's RNG key id is set by the job mapping)
+#endif
 #if SSA_K1_DUMP
         slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
 #endif
@@ -153,6 +161,20 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         lo_dirty = true;
 #endif
     };
+    // phase 0 of a job: take it; later phases: wait for and reload the state (true: resumed)
+    auto seg_take = [&](int ph, bool& resumed) -> bool {
+        resumed = false;
+        if (ph == 0) { seg_p = 0; seg_kb = seg_kb_of(0); return true; }
+        unsigned r;
+        while ((r = ((volatile unsigned*)P.seg_ready)[rel]) < (unsigned)ph) __nanosleep(64);
+        if (r > (unsigned)ph) return false;      // finished, or stopped at a later boundary
+        __threadfence();
+        seg_restore(rel);
+        seg_p = ph;
+        seg_kb = seg_kb_of(ph);
+        resumed = true;
+        return true;
+    };
 #endif
     // a1: take the next trajectory id (atomic counter) and initialise it
     auto start = [&]() -> bool {
@@ -161,8 +183,16 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             // sweep points are interleaved in the order lanes take work (w mod
             // points), so trajectories of short and long points mix over the
             // whole launch; the staging column stays point-major (dense per point)
+#if SSA_K1_SEG
+          for (;;) {
+            const ssa_u64 q = atomicAdd(P.work, 1ull);
+            if (q >= (ssa_u64)seg * P.n_ids) return false;
+            const int ph = seg > 1 ? (int)(q / P.n_ids) : 0;
+            const ssa_u64 w = q - (ssa_u64)ph * P.n_ids;
+#else
             const ssa_u64 w = atomicAdd(P.work, 1ull);
             if (w >= P.n_ids) return false;
+#endif
             ssa_u64 ptl;
             if (P.pt_order) {
                 // points in the given order (costliest first, measured by an earlier run)
@@ -176,25 +206,27 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             my_ptl = ptl;
             rel = ptl * P.n_per_point + id;
             kp = s_k + ptl * (ssa_u64)P.n_pool;
+#if SSA_K1_SEG
+            bool resumed;
+            if (!seg_take(ph, resumed)) continue;
+            if (resumed) return true;
+            break;
+          }
+#endif
         }
 #else
-#if SSA_K1_MIG
+#if SSA_K1_SEG
         if (seg > 1) {
             for (;;) {
                 const ssa_u64 q = atomicAdd(P.work, 1ull);
                 if (q >= (ssa_u64)seg * P.n_ids) return false;
                 const int ph = (int)(q / P.n_ids);
                 rel = q - (ssa_u64)ph * P.n_ids;
-                if (ph == 0) { seg_p = 0; seg_kb = seg_kb_of(0); break; }   // a fresh trajectory (below)
-                // phase ph - 1 of this trajectory was handed out n_ids jobs ago: wait for its state
-                unsigned r;
-                while ((r = ((volatile unsigned*)P.seg_ready)[rel]) < (unsigned)ph) __nanosleep(64);
-                if (r > (unsigned)ph) continue;      // finished, or stopped at a later boundary
-                __threadfence();
-                seg_restore(rel);
-                seg_p = ph;
-                seg_kb = seg_kb_of(ph);
-                return true;
+                // (phase ph - 1 of this trajectory was handed out n_ids jobs ago)
+                bool resumed;
+                if (!seg_take(ph, resumed)) continue;
+                if (resumed) return true;
+                break;                                 // a fresh trajectory (below)
             }
         } else
 #endif
@@ -397,7 +429,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
                 continue;
             }
 #endif
-#if SSA_K1_MIG
+#if SSA_K1_SEG
             // time slice: at the first crossing at or past this phase's boundary, hand the
             // trajectory to its next phase's job (the candidate is a function of (x, t, e): the
             // resumed lane recomputes it bit for bit and processes this crossing)
@@ -458,7 +490,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             }
             if (fin) {
                 // trajectory done: per-trajectory records, then refill (a1)
-#if SSA_K1_MIG
+#if SSA_K1_SEG
                 if (seg > 1) atomicExch(&P.seg_ready[rel], (unsigned)seg);   // later phases: nothing to do
 #endif
                 my_events += e;
