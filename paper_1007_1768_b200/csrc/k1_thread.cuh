@@ -148,9 +148,7 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         hash = (ssa_u64)__double_as_longlong(__ldcg(st + SSA_S + 4));
         rel = r;
         vid = P.id_begin + rel;
-#if !SSA_K1_SWEEP
-        id = vid;                              // (a sweep's RNG key id is set by the job mapping)
-#endif
+        id = vid;
 #if SSA_K1_DUMP
         slot = P.n_dump ? ssa_dump_slot(P.dump_ids, P.n_dump, vid) : -1ll;
 #endif
@@ -183,16 +181,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             // sweep points are interleaved in the order lanes take work (w mod
             // points), so trajectories of short and long points mix over the
             // whole launch; the staging column stays point-major (dense per point)
-#if SSA_K1_SEG
-          for (;;) {
-            const ssa_u64 q = atomicAdd(P.work, 1ull);
-            if (q >= (ssa_u64)seg * P.n_ids) return false;
-            const int ph = seg > 1 ? (int)(q / P.n_ids) : 0;
-            const ssa_u64 w = q - (ssa_u64)ph * P.n_ids;
-#else
             const ssa_u64 w = atomicAdd(P.work, 1ull);
             if (w >= P.n_ids) return false;
-#endif
             ssa_u64 ptl;
             if (P.pt_order) {
                 // points in the given order (costliest first, measured by an earlier run)
@@ -206,13 +196,6 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             my_ptl = ptl;
             rel = ptl * P.n_per_point + id;
             kp = s_k + ptl * (ssa_u64)P.n_pool;
-#if SSA_K1_SEG
-            bool resumed;
-            if (!seg_take(ph, resumed)) continue;
-            if (resumed) return true;
-            break;
-          }
-#endif
         }
 #else
 #if SSA_K1_SEG

@@ -484,8 +484,10 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
     if (g.plog == 1) o << "__constant__ double c_plog_div[14] = SSA_PLOG_DIV_COEF_INIT;\n";
     // tail compaction (k1_thread.cuh): plain, dump and profiling variants
     o << "#define SSA_K1_MIG " << ((!sweep && record == 0) ? 1 : 0) << "\n";
-    // time-sliced trajectories (k1_thread.cuh): plain, dump, profiling and sweep variants
-    o << "#define SSA_K1_SEG " << (record == 0 ? 1 : 0) << "\n";
+    // time-sliced trajectories (k1_thread.cuh): plain, dump and profiling variants (not sweeps: their
+    // costliest-first order hands out the long trajectories' phases ~1 round of lanes apart, so
+    // phase p + 1 would often wait for phase p -- 13% slower on the Fig. 4 sweep with 32 phases)
+    o << "#define SSA_K1_SEG " << ((!sweep && record == 0) ? 1 : 0) << "\n";
     std::vector<int> hot;   // the dispatch profile's hot reactions (K1Spec, or the knob)
     for (int hj : (!g.hot.empty() ? g.hot : (spec ? spec->hot : std::vector<int>())))
         if (hj >= 0 && hj < R) hot.push_back(hj);
@@ -1554,13 +1556,13 @@ static ssa_status run_range(const ssa_model* m, ssa_u64 id_begin, ssa_u64 id_end
         CU(migr.alloc(sizeof(unsigned) * mig_cap, st));
         CU(migc.alloc(sizeof(ssa_u64) * 4, st));
     }
-    // time-sliced trajectories (K1 plain / dump / profiling / sweep variants): each trajectory runs as
+    // time-sliced trajectories (K1 plain / dump / profiling variants): each trajectory runs as
     // SSA_TSLICES phases handed out phase by phase, so a launch ends with short last phases instead
     // of whole trajectories on an emptying GPU (bitwise neutral).  Used when a launch
     // has more trajectories than resident lanes; SSA_K1_SEG overrides the phase count (1 = off).
     int tslices = SSA_TSLICES;
     if (const char* sv = getenv("SSA_K1_SEG")) tslices = std::max(1, std::min(64, atoi(sv)));
-    if (path != SSA_PATH_THREAD || rec || spread || mig || (ssa_u64)C <= (ssa_u64)grid * (ssa_u64)block)
+    if (path != SSA_PATH_THREAD || sw || rec || spread || mig || (ssa_u64)C <= (ssa_u64)grid * (ssa_u64)block)
         tslices = 1;
     DevBuf segb, segr;
     if (tslices > 1) {

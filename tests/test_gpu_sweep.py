@@ -140,3 +140,4 @@ def test_sweep_rerun_costliest_first_is_bitwise(S):
     for f in ("states", "events_at", "time_at"):
         assert np.array_equal(getattr(a.dump, f), getattr(b.dump, f)), f
     assert a.dump.summary.tobytes() == b.dump.summary.tobytes()
+
