@@ -392,6 +392,38 @@ def test_numeric_error_reported(S):
         assert np.array_equal(r.dump.summary["events"], sm["events"])
 
 
+def test_time_slices_errors_and_absorption(S, monkeypatch):
+    """Time-sliced K1 at more trajectories than resident lanes (so the slicing is active): a
+    numeric error that strikes only some trajectories, late in their horizon, is reported with the
+    same status, error count, first erroring id and reaction as without slicing, and absorbed
+    trajectories (pure death reaching 0, then a0 = 0 for the rest of the grid) give the same grids."""
+    n = 160000                                   # > 148 SMs x 512 resident lanes
+    # A grows by immigration; B doubles at rate 1e-3 per B and its propensity overflows at B = 2:
+    # only trajectories whose B fires within the horizon err
+    net = Network(("A", "B"), (0, 1), (
+        _rx([], [(0, 1)], 5.0),
+        _rx([(1, 1)], [(1, 2)], 2e-6),
+        _rx([(1, 2)], [(1, 3)], 1e308),           # 2B -> 3B: C(3, 2) * 1e308 = inf once B = 3
+    ))
+    m = S.Model(net)
+    res = {}
+    for sv in ("1", "8"):
+        monkeypatch.setenv("SSA_K1_SEG", sv)
+        res[sv] = S.run(m, n, 40.0, 1.0, 11, path=THREAD, raise_on_error=False)
+    a, b = res["1"], res["8"]
+    assert a.status == 3 and 0 < a.n_errors < n, (a.status, a.n_errors)
+    assert (b.status, b.n_errors, b.first_error_id, b.first_error_reaction, b.events) == \
+        (a.status, a.n_errors, a.first_error_id, a.first_error_reaction, a.events)
+    # absorption: pure death from 3 molecules at rate 0.2 over 30 time units
+    pd = S.Model(inputs.pure_death(k=0.2, x0=3))
+    monkeypatch.setenv("SSA_K1_SEG", "1")
+    c = S.run(pd, n, 30.0, 0.5, 5, path=THREAD)
+    monkeypatch.setenv("SSA_K1_SEG", "8")
+    d = S.run(pd, n, 30.0, 0.5, 5, path=THREAD)
+    assert c.events == d.events and np.array_equal(c.mean, d.mean) and np.array_equal(c.m2, d.m2)
+    assert c.mean[-1, 0] < 0.01                  # nearly every trajectory absorbed by t = 30
+
+
 @pytest.mark.parametrize("path", [THREAD, WARP, HALF])
 def test_overflow_reported(S, path):
     net = Network(("A",), (2**31 - 5,), (_rx([], [(0, 1)], 100.0),))
