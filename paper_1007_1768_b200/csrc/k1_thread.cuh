@@ -39,7 +39,11 @@ static __device__ __forceinline__ int ssa_count_from(const double (&c)[SSA_R > 0
     int jp[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int q = LO; q < SSA_R - 1; ++q) {
-        if (SSA_K1_SEL == 1 || (SSA_K1_SEL == 2 && (q & 1)))
+        if (SSA_K1_SEL == 3)
+            // speed A/B only: high words alone (a tie of high words miscounts; no fallback)
+            asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+                : "+r"(jp[q & 3]) : "r"(__double2hiint(c[q])), "r"(__double2hiint(r)));
+        else if (SSA_K1_SEL == 1 || (SSA_K1_SEL == 2 && (q & 1)))
             // c_j, r >= +0 and not NaN: their bit patterns order as int64 (ALU pipe)
             asm("{\n\t.reg .pred p;\n\tsetp.le.s64 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
                 : "+r"(jp[q & 3]) : "l"(__double_as_longlong(c[q])), "l"(__double_as_longlong(r)));
@@ -49,6 +53,25 @@ static __device__ __forceinline__ int ssa_count_from(const double (&c)[SSA_R > 0
     }
     return LO + ((jp[0] + jp[1]) + (jp[2] + jp[3]));
 }
+
+#if SSA_K1_SELX
+// a7 on the ALU pipe: j0 = #{ j in [0, R-2] : hi(c_j) < hi(r) }.  For c_j, r >= 0 finite the
+// high words order as int32, so hi(c_j) < hi(r) implies c_j < r and hi(c_j) > hi(r) implies
+// c_j > r: j0 <= j*, and j0 == j* unless hi(c_j0) == hi(r) (c is nondecreasing, so only the
+// first entry not counted can tie).  ssa_apply_sel (runtime.cu) checks that tie in the update's
+// own jump-table case and recounts in fp64 when it occurs (~1e-6 of events): the same j* as
+// ssa_count_from, bit for bit.
+static __device__ __forceinline__ int ssa_count_hi(const double (&c)[SSA_R > 0 ? SSA_R : 1], double r)
+{
+    int jp[4] = {0, 0, 0, 0};
+    const int hr = __double2hiint(r);
+#pragma unroll
+    for (int q = 0; q < SSA_R - 1; ++q)
+        asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t@p add.s32 %0, %0, 1;\n\t}"
+            : "+r"(jp[q & 3]) : "r"(__double2hiint(c[q])), "r"(hr));
+    return (jp[0] + jp[1]) + (jp[2] + jp[3]);
+}
+#endif
 
 extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(const ssa_k1_params P)
 {
@@ -391,7 +414,11 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
         // j* = #{ j : c_j <= r } (c nondecreasing, r < a0), counted in four
         // independent partial sums to shorten the dependency chain.
         const double r = __dmul_rn(ssa_u53(o.o3, o.o2), a0);
+#if SSA_K1_SELX
+        int j = ssa_count_hi(c, r);   // j0 <= j*: made exact by ssa_apply_sel
+#else
         const int j = ssa_count_from<0>(c, r);
+#endif
         SSA_CHECK(j >= 0 && j < (SSA_R > 0 ? SSA_R : 1), P.stats);
         // a5: tau = E / a0 by the fast in-range IEEE division (speculative:
         // replaced on the rare path when a0 is outside [2^-900, 2^901))
@@ -534,6 +561,8 @@ extern "C" __global__ void __launch_bounds__(SSA_K1_BLOCK, SSA_K1_MINB) ssa_k1(c
             }
             ssa_apply_rec(j, x, out);
         }
+#elif SSA_K1_SELX
+        j = ssa_apply_sel(j, x, c, r);   // j* exact from here on
 #else
         ssa_apply(j, x);
 #endif

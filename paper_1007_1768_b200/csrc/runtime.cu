@@ -440,6 +440,8 @@ static K1Gen k1_gen()
         if (s.find("keys=param") != std::string::npos) r.seed_imm = false;
         if (s.find("sel=i64") != std::string::npos) r.sel = 1;
         if (s.find("sel=mix") != std::string::npos) r.sel = 2;
+        if (s.find("sel=hi32") != std::string::npos) r.sel = 3;   // speed A/B only (no tie fallback)
+        if (s.find("sel=hi32x") != std::string::npos) r.sel = 4;  // high words + exact tie fallback
         if (s.find("nospread32") != std::string::npos) r.spread32 = false;
         if (s.find("plog=div") != std::string::npos) r.plog = 1;
         if (s.find("plog=global") != std::string::npos) r.plog = 2;
@@ -704,6 +706,39 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
         for (int s2 = 0; s2 < S; ++s2) o << (s2 ? ", " : "") << "\"+d\"(x[" << s2 << "])";
         o << "\n    : \"r\"(j)" << (rec ? ", \"l\"(out)" : "") << (rec ? "\n    : \"memory\"" : "") << ");\n";
     };
+    // a7 + a8 with the selection counted on the high words (K1Gen::sel 4, k1_thread.cuh
+    // ssa_count_hi): j0 <= j*, equal unless hi(c_j0) == hi(r).  The hot reactions check that tie
+    // in their predicate; every jump-table case checks it for its own c_j (the case R-1 cannot
+    // tie: j0 = R-1 means c_j < r for all j <= R-2).  A tie skips the update, recounts in fp64
+    // and applies through ssa_apply.  Operands: %0..%(S-1) = x, %S = tie, %(S+1) = j0,
+    // %(S+2) = hi(r), %(S+3+q) = hi(c_q) for q <= R-2.
+    const bool selx = g.sel == 4 && use_brx && record == 0 && S + R + 2 <= 120;
+    o << "#define SSA_K1_SELX " << (selx ? 1 : 0) << "\n";
+    auto emit_brx_sel = [&]() {
+        const std::string pfx = "ssa_applys_";
+        o << "  asm volatile(\"{\\n\\t.reg .pred pt;\\n\\t" << pfx << "tab: .branchtargets ";
+        for (int jj = 0; jj < R; ++jj) o << (jj ? ", " : "") << pfx << jj;
+        o << ";\\n\\tbrx.idx %" << S + 1 << ", " << pfx << "tab;\\n\\t";
+        for (int jj = 0; jj < R; ++jj) {
+            o << pfx << jj << ":\\n\\t";
+            if (jj <= R - 2)
+                o << "setp.eq.s32 pt, %" << S + 3 + jj << ", %" << S + 2 << ";\\n\\t@pt bra " << pfx << "tie;\\n\\t";
+            for (auto& d : m.rx[jj].nu) {
+                double v = (double)d.second;
+                unsigned long long bits;
+                memcpy(&bits, &v, 8);
+                char hx[32];
+                snprintf(hx, sizeof hx, "0d%016llX", bits);
+                o << "add.rn.f64 %" << d.first << ", %" << d.first << ", " << hx << ";\\n\\t";
+            }
+            o << "bra " << pfx << "end;\\n\\t";
+        }
+        o << pfx << "tie:\\n\\tmov.u32 %" << S << ", 1;\\n\\t" << pfx << "end:\\n\\t}\"\n    : ";
+        for (int s2 = 0; s2 < S; ++s2) o << "\"+d\"(x[" << s2 << "]), ";
+        o << "\"+r\"(tie)\n    : \"r\"(j), \"r\"(hr)";
+        for (int q = 0; q + 1 < R; ++q) o << ", \"r\"(__double2hiint(c[" << q << "]))";
+        o << ");\n";
+    };
     o << "static __device__ __forceinline__ void ssa_apply(int j, double (&x)[SSA_S]) {\n";
     if (use_brx) {
         if (!hot.empty()) {
@@ -732,6 +767,26 @@ static std::string gen_k1_model(const ssa_model& m, int block, int minb, bool du
             o << " break;\n";
         }
         o << "  default: break;\n  }\n  (void)x;\n}\n";
+    }
+    if (selx) {
+        o << "static __device__ __forceinline__ int ssa_apply_sel(int j, double (&x)[SSA_S], "
+             "const double (&c)[SSA_R], double r) {\n  const int hr = __double2hiint(r);\n  int tie = 0;\n";
+        o << "  bool hot = false;\n";
+        for (int hj : hot) {
+            // one predicate, no short circuit (keeps the adds predicated, as in ssa_apply)
+            o << "  if ((j == " << hj << ")";
+            if (hj <= R - 2) o << " & (__double2hiint(c[" << hj << "]) != hr)";
+            o << ") { hot = true;";
+            for (auto& d : m.rx[hj].nu)
+                o << " x[" << d.first << "] = __dadd_rn(x[" << d.first << "], " << d.second << ".0);";
+            o << " }\n";
+        }
+        o << "  if (!hot) {\n";
+        emit_brx_sel();
+        o << "  }\n";
+        // the tie (hi(c_j0) == hi(r)): j* = #{ q <= R-2 : c_q <= r } in fp64, as ssa_count_from
+        o << "  if (tie) {\n    int js = 0;\n#pragma unroll\n    for (int q = 0; q < SSA_R - 1; ++q) js += c[q] <= r ? 1 : 0;\n"
+             "    j = js;\n    ssa_apply(j, x);\n  }\n  return j;\n}\n";
     }
     if (record == 1) {
         // pre-event counts of the species reaction j changes, in nu order, then x += nu_j
