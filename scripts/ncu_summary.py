@@ -86,10 +86,13 @@ def main():
             stall_tot[c] += v
             st += v
         stall_ins.append((st, s))
-    it = collections.Counter(c for c in counts if c > 0).most_common(1)[0][0]
+    # the event loop's body: the per-instruction count that carries the most executed instructions
+    # (count x multiplicity), so once-per-warp prologue instructions cannot win by being many
+    mult = collections.Counter(c for c in counts if c > 0)
+    it = max(mult, key=lambda c: c * mult[c])
     tot = sum(ops.values())
     lines.append("")
-    lines.append(f"warp-iterations of the event loop (mode of per-instruction counts): {it}")
+    lines.append(f"warp-iterations of the event loop (the per-instruction count carrying the most instructions): {it}")
     lines.append(f"warp instructions per loop iteration: {tot / it:.1f}   (SIMT: {tot_th / max(tot, 1):.2f} threads/inst)")
     if events:
         lines.append(f"events in launch: {events:.4g}  -> warp instructions per event: {tot / events:.3f}")
